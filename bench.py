@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""bench.py -- Trotter steps/s of the adiabatic 3-SAT evolution (BASELINE.json metric).
+
+Workload (N = 1): BASELINE configs[3] -- the checked-in unique-solution n = 30
+instance (inputs/instances/usa_n30_s1030.cnf), T = 200, K = 10^4 midpoint
+schedule (dt = 0.02). One bench "step" = one qaa_evolve call over the next
+window of `--chunk` consecutive Trotter steps of that schedule (windows cycle
+through the 10^4-step schedule) followed by qaa_success_prob (A9), i.e. every
+per-step row of SURVEY §8(a) runs inside the timed region; load (A1-A3) and
+init (A4) run once before it. `value` = Trotter steps per second (max over
+ranks), inputs resident in HBM. The 16 GiB state is > 126 MB L2, so no L2
+flush is needed between steps.
+
+`e2e` = the same metric through the public API with host buffers: each e2e
+step loads the instance from host memory, initialises, evolves one window and
+reads P_succ back (H2D/D2H inside the timed region).
+
+`--impl reference` times the CPU oracle (oracle/, as it stands) instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from inputs import cnf  # noqa: E402
+
+N_DEFAULT = 30
+T_TOTAL = 200.0
+K_TOTAL = 10_000
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=None, help="qubits (default 30 + log2(gpus))")
+    ap.add_argument("--chunk", type=int, default=20, help="Trotter steps per bench step")
+    ap.add_argument("--row-bits", type=int, default=3)
+    ap.add_argument("--step-spanning", type=int, default=1)
+    ap.add_argument("--ctas-per-sm", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-n", type=int, default=26)
+    return ap.parse_args()
+
+
+def schedule_window(w: int, chunk: int):
+    """Window w of the K_TOTAL-step midpoint schedule: (T_window, s_k array)."""
+    k0 = (w * chunk) % K_TOTAL
+    ks = (np.arange(k0, k0 + chunk) % K_TOTAL).astype(np.float64)
+    return T_TOTAL / K_TOTAL * chunk, (ks + 0.5) / K_TOTAL
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{device}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 7 and p[0].replace(".", "").isdigit():
+                    rows.append(p)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def traffic_from_profiles():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------- CPU oracle timing
+def oracle_sample(n_target: int, n_sample: int, steps: int = 2):
+    """Time the oracle's Trotter step (O-5..O-7) on a seeded instance of n_sample
+    qubits and scale per amplitude-qubit to n_target (cost ~ (n+1) 2^n)."""
+    from oracle import oracle
+    oracle.build()
+    cl = cnf.random_instance(n_sample, int(round(4.5 * n_sample)), 1000 + n_sample)
+    E = oracle.energy_table(n_sample, cl)
+    psi = oracle.init_uniform(n_sample)
+    T, s = schedule_window(0, steps)
+    t0 = time.perf_counter()
+    oracle.evolve(n_sample, E, psi, T, steps, s)
+    dt = (time.perf_counter() - t0) / steps
+    scale = (2.0 ** (n_target - n_sample)) * (n_target + 1) / (n_sample + 1)
+    return dt, dt * scale, oracle.num_threads()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n = args.n or (N_DEFAULT + (args.gpus.bit_length() - 1))
+    ns = args.cpu_sample_n
+    for _ in range(args.warmup):
+        oracle_sample(n, ns, 1)
+    per = []
+    for _ in range(args.steps):
+        dt, scaled, cores = oracle_sample(n, ns, 1)
+        per.append(scaled)
+    t_step = float(np.mean(per))
+    val = 1.0 / t_step
+    sample = (f"oracle Trotter step on a seeded n={ns} instance, 1 step per bench step, scaled by "
+              f"2^{n - ns}*(n+1)/(n_s+1) to n={n}")
+    line = {"impl": "reference", "metric": "trotter_steps_per_s", "value": val, "unit": "steps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"n={n} unique-solution 3-SAT, T=200, K=1e4 (dt=0.02)",
+                                            "n": n},
+            "cpu_baseline": {"value": val, "unit": "steps/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        world = args.gpus if world == 1 else world
+    torch.cuda.set_device(local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1103_1399_b200 as q
+
+    n = args.n or (N_DEFAULT + (world.bit_length() - 1))
+    if world > 1:
+        raise SystemExit("sharded multi-GPU evolve is not built in this round (DESIGN.md §7)")
+    cl, sol = cnf.load_instance(n) if os.path.exists(cnf.instance_path(n)) else (
+        cnf.random_instance(n, int(round(4.5 * n)), 1000 + n), None)
+    stream = torch.cuda.current_stream(local)
+    ctx = q.Context(local, stream=stream.cuda_stream)
+    ctx.set_option(q.OPT_ROW_BITS, args.row_bits)
+    ctx.set_option(q.OPT_STEP_SPANNING, args.step_spanning)
+    ctx.set_option(q.OPT_CTAS_PER_SM, args.ctas_per_sm)
+    ctx.load_instance(n, cl)
+    ctx.init_uniform()
+    chunk = args.chunk
+    w = 0
+    for _ in range(args.warmup):
+        T, s = schedule_window(w, chunk)
+        ctx.evolve(T, chunk, s)
+        ctx.success_prob()
+        w += 1
+    torch.cuda.synchronize()
+    ctx.reset_stats()
+    ctx.set_option(q.OPT_PROFILE, 1)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            T, s = schedule_window(w, chunk)
+            ctx.evolve(T, chunk, s)
+            p_succ = ctx.success_prob()
+            w += 1
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    st = ctx.stats()
+    ctx.set_option(q.OPT_PROFILE, 0)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    trotter = args.steps * chunk
+    value = trotter / (ms / 1e3)
+    # roofline of the dominant kernel (qaa_pass_kernel): algorithmic bytes per
+    # launch = 32 B/amp (read + write psi) + 1 B/amp (E) on D passes.
+    L = st["n_local"]
+    amps = 1 << L
+    npass = st["pass_launches"]
+    n_d = trotter  # one D per Trotter step
+    alg_bytes = npass * 32 * amps + n_d * amps
+    kernel_ms = st["pass_kernel_ms"]
+    achieved = alg_bytes / (kernel_ms / 1e3) / 1e9 if kernel_ms > 0 else None
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs", 6650.0)
+    tr = traffic_from_profiles()
+    traffic = None
+    if tr and tr.get("n") == n and tr.get("bytes_per_launch"):
+        traffic = tr["bytes_per_launch"]
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "kernel": "qaa_pass_kernel", "launches": npass,
+                "avg_launch_ms": kernel_ms / max(npass, 1),
+                "alg_bytes_per_launch": alg_bytes / max(npass, 1),
+                "kernel_share_of_step": kernel_ms / ms if ms > 0 else None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback B200_PROFILING.md"}
+    clocks = clk.summary()
+    gpu_launches = st["kernel_launches_total"]
+
+    # ---------------------------------------------------------------- e2e
+    e2e = None
+    if not args.no_e2e:
+        ctx2 = q.Context(local, stream=stream.cuda_stream)
+        ctx2.set_option(q.OPT_ROW_BITS, args.row_bits)
+        ctx2.set_option(q.OPT_STEP_SPANNING, args.step_spanning)
+        lits = np.ascontiguousarray(np.asarray(cl, dtype=np.int32).reshape(-1))
+        pinned = torch.from_numpy(lits).pin_memory().numpy()
+        e2e_steps = max(2, min(args.steps, 4))
+        T, s = schedule_window(0, chunk)
+        ctx2.load_instance(n, pinned.reshape(-1, 3))  # warm (allocations)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(e2e_steps):
+            T, s = schedule_window(i, chunk)
+            ctx2.load_instance(n, pinned.reshape(-1, 3))
+            ctx2.init_uniform()
+            ctx2.evolve(T, chunk, s)
+            ctx2.success_prob()
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        emax = ctx2.max_energy()
+        ctx2.close()
+        if world > 1:
+            t = torch.tensor([e2e_s], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        h2d = 32 * len(cl) + chunk * ((emax + 1) * 16 + 12)
+        d2h = 16 + 8
+        e2e = {"value": e2e_steps * chunk / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+               "includes": "load_instance (H2D clauses, energy table, Z) + init + evolve(window) + success_prob (D2H)"}
+
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0:
+        try:
+            dt, scaled, cores = oracle_sample(n, args.cpu_sample_n, 2)
+            cpu = {"value": 1.0 / scaled, "unit": "steps/s", "cores": cores, "kind": "oracle",
+                   "sample": f"2 oracle Trotter steps on a seeded n={args.cpu_sample_n} instance "
+                             f"({dt:.3f} s/step), scaled by 2^{n - args.cpu_sample_n}*(n+1)/(n_s+1) to n={n}"}
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "oracle",
+                   "sample": f"failed: {e}"}
+    ctx.close()
+    if rank == 0:
+        line = {"metric": "trotter_steps_per_s", "value": value, "unit": "steps/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": f"n={n} unique-solution 3-SAT (inputs/instances), T=200, K=1e4 (dt=0.02), "
+                                       f"{chunk} Trotter steps + P_succ per bench step",
+                           "n": n, "m": len(cl), "chunk": chunk, "row_bits": args.row_bits,
+                           "step_spanning": args.step_spanning, "passes_per_step":
+                               st["passes_per_step_num"] / st["passes_per_step_den"], "tile_groups": st["groups"],
+                           "l2": "state 16 GiB >> 126 MB L2 (no flush needed)",
+                           "parallelism": f"dp{world}" if world > 1 else "single"},
+                "effective_hbm_gbs": alg_bytes / (ms / 1e3) / 1e9,
+                "algorithmic_gbs_33B": 33 * amps * trotter / (ms / 1e3) / 1e9,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+                "clocks": clocks, "p_succ_last": p_succ}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

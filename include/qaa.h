@@ -1,0 +1,211 @@
+/*
+ * qaa.h -- C-ABI of libqaa: B200-native first-order Trotter evolution of the
+ * quantum adiabatic algorithm for 3-SAT (Diaz-Pier, Venegas-Andraca,
+ * Gomez-Munoz, arXiv 1103.1399).
+ *
+ * Citations: "P:n" is line n of the paper's text; "R<k>" is reading
+ * k in DESIGN.md (where the paper is silent or garbled); "SURVEY §8" is the
+ * hot-path scope table.
+ *
+ * What is computed (Eq. 1 at P:69-72):
+ *   H(s) = (1 - s) H_B + s H_P,  H_B = sum_j (1 - sigma^x_j)/2   (R1, R2)
+ *   H_P  = diag(E),  E(x) = number of clauses all of whose literals are false
+ *          under assignment x (constant 1, duplicates counted, R4/R5)
+ *   psi_0 = 2^{-n/2} sum_x |x>
+ *   K first-order Trotter steps of length dt = T/K; step k uses s_k (midpoint
+ *   (k+1/2)/K unless a schedule is given, R8) and applies
+ *   exp(-i dt s_k H_P) first, then exp(-i dt (1 - s_k) H_B)      (R7)
+ *
+ * Conventions (R-conventions): basis index x, bit j-1 of x is
+ * variable x_j (x_1 least significant), bit value 1 = true. Amplitudes are
+ * complex128 stored interleaved (re, im), i.e. torch.complex128 /
+ * cuDoubleComplex layout. hbar = 1; all reported values are raw (no
+ * renormalisation, R12).
+ *
+ * Error model: every call returns a qaa_status; nothing aborts, exits or
+ * throws across the ABI. qaa_last_error(ctx) names the offending argument.
+ * USAGE, INPUT and CAP leave the context usable. A CUDA or NCCL failure
+ * poisons the context: every later call except qaa_destroy returns
+ * QAA_E_STATE. A context is used by one host thread at a time.
+ *
+ * Asynchrony: init and evolve are enqueued on the context's stream and return
+ * without a host synchronisation; the reductions (success_prob, energy,
+ * norm2, sigma_x) and copies synchronise the stream before returning.
+ */
+#ifndef QAA_H
+#define QAA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  QAA_OK = 0,
+  QAA_E_USAGE = 1, /* bad argument value or call order the caller controls */
+  QAA_E_INPUT = 2, /* malformed instance (literal 0 or |literal| > n)       */
+  QAA_E_CAP = 3,   /* problem exceeds a capacity (device memory, m > 255)   */
+  QAA_E_STATE = 4, /* call out of order (e.g. evolve before init), or the
+                      context is poisoned by an earlier CUDA/NCCL error      */
+  QAA_E_CUDA = 5,  /* CUDA runtime error (poisons the context)              */
+  QAA_E_NCCL = 6   /* NCCL error (poisons the context)                      */
+} qaa_status;
+
+typedef struct qaa_ctx qaa_ctx;
+
+/* Creation parameters. All pointers are borrowed: the caller keeps
+ * ownership and must keep them valid for the life of the context.
+ *  device        CUDA device ordinal.
+ *  stream        cudaStream_t to enqueue on; NULL = the library creates one.
+ *  rank, world   this process's rank and the number of ranks (world = 1, or
+ *                a power of two up to 8 when the state is sharded over GPUs
+ *                on its top log2(world) qubits).
+ *  nccl_id       128-byte ncclUniqueId shared by all ranks (world > 1), else NULL.
+ *  state         optional caller-owned device buffer for the local state
+ *                (>= 16 * 2^L bytes, 256-byte aligned); NULL = library-owned.
+ *  state_bytes   its size in bytes. */
+typedef struct {
+  int device;
+  void* stream;
+  int rank;
+  int world;
+  const void* nccl_id;
+  void* state;
+  size_t state_bytes;
+} qaa_config;
+
+/* Create a context. Errors: USAGE (NULL pointers, world not in {1,2,4,8},
+ * rank out of range), CUDA (device/stream setup), NCCL (communicator). */
+qaa_status qaa_create(const qaa_config* cfg, qaa_ctx** out);
+
+/* Release every library-owned resource. Safe on a poisoned context and on NULL. */
+void qaa_destroy(qaa_ctx* ctx);
+
+/* Human-readable description of the last error on this context (never NULL). */
+const char* qaa_last_error(const qaa_ctx* ctx);
+
+/* Load a 3-SAT instance: n variables, m clauses, lits = 3*m
+ * DIMACS-signed literals +-(1..n), clause c = lits[3c..3c+2] (copied; the
+ * caller keeps ownership). Builds the energy table E (uint8 per basis state,
+ * SURVEY §8 A2) and the solution set Z = {x : E(x) = 0} (A3) on the
+ * device; resets the state to "uninitialised". Tautological clauses never
+ * count; duplicates count with multiplicity (R5). m = 0 is allowed (E = 0).
+ * Errors: USAGE (n < 1, m < 0, lits == NULL with m > 0, n - log2(world) < 1),
+ * INPUT (a literal 0 or |l| > n), CAP (m > 255, or the local state plus
+ * tables do not fit in device memory or a caller-owned state buffer).
+ * Synchronises the stream. Collective when world > 1. */
+qaa_status qaa_load_instance(qaa_ctx* ctx, int n, int m, const int32_t* lits);
+
+/* psi <- 2^{-n/2} for every x. Errors: STATE (no instance). */
+qaa_status qaa_init_uniform(qaa_ctx* ctx);
+
+/* Test hook: psi <- |x> (basis state, x < 2^n). Errors: STATE, USAGE. */
+qaa_status qaa_init_basis(qaa_ctx* ctx, uint64_t x);
+
+/* Apply `steps` first-order Trotter steps of total time T:
+ * dt = T/steps, s_k = schedule[k] if schedule != NULL (host array of `steps`
+ * doubles in [0, 1]) else (k + 0.5)/steps. T = 0 is the identity.
+ * Coefficients are computed on the host in binary64 (R11). Enqueued on the
+ * stream; returns without a host sync. The state is left in canonical layout.
+ * Errors: STATE (no init), USAGE (T < 0 or not finite, steps < 1, a schedule
+ * value outside [0, 1]). Collective when world > 1 (identical arguments). */
+qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t steps, const double* schedule);
+
+/* *out = sum_{x in Z} |psi[x]|^2 (raw; 0 for an UNSAT instance).
+ * Deterministic (fixed reduction tree). Synchronises; same value on all ranks. */
+qaa_status qaa_success_prob(qaa_ctx* ctx, double* out);
+
+/* *out = <psi|H(s)|psi> (raw) = (1-s) sum_j (||psi||^2 - <sigma^x_j>)/2 + s sum_x E(x)|psi[x]|^2.
+ * Errors: USAGE (s outside [0, 1]). Synchronises. Collective. */
+qaa_status qaa_energy(qaa_ctx* ctx, double s, double* out);
+
+/* *out = ||psi||^2 (raw). Synchronises. Collective. */
+qaa_status qaa_norm2(qaa_ctx* ctx, double* out);
+
+/* out[j] = <psi|sigma^x_{j}|psi> for qubit j = 0..n-1 (variable x_{j+1}); `out`
+ * holds n doubles. Synchronises. Collective. */
+qaa_status qaa_sigma_x(qaa_ctx* ctx, double* out);
+
+/* *out = |Z|, the number of satisfying assignments (all ranks). */
+qaa_status qaa_num_solutions(qaa_ctx* ctx, uint64_t* out);
+
+/* *out = max_x E(x) over the whole instance. */
+qaa_status qaa_max_energy(qaa_ctx* ctx, uint32_t* out);
+
+/* Copy amplitudes [first, first+count) of the canonical global index space
+ * to host memory dst (2*count doubles, caller-owned). Each rank copies the
+ * part it owns and leaves the rest of dst untouched. Synchronises.
+ * Errors: USAGE (range outside [0, 2^n)), STATE (no instance). */
+qaa_status qaa_copy_state(qaa_ctx* ctx, uint64_t first, uint64_t count, double* dst_host);
+
+/* Overwrite amplitudes [first, first+count) from host memory (2*count doubles).
+ * Marks the state initialised. Synchronises. Test and checkpoint hook. */
+qaa_status qaa_set_state(qaa_ctx* ctx, uint64_t first, uint64_t count, const double* src_host);
+
+/* Copy energy-table entries E(x), x in [first, first+count), to host (uint8).
+ * Each rank copies the part it owns. Synchronises. */
+qaa_status qaa_copy_energy_table(qaa_ctx* ctx, uint64_t first, uint64_t count, uint8_t* dst_host);
+
+/* Device pointer of the local state (2^L complex128), for zero-copy wrapping. */
+qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
+
+/* ---------------------------------------------------------------- tuning / stats */
+
+/* Options (take effect at the next load/evolve):
+ *  QAA_OPT_ROW_BITS      c in {3, 4, 5}: log2 of the contiguous amplitude run
+ *                        every tile keeps (128/256/512-byte rows). Default 3.
+ *  QAA_OPT_PROFILE       1 = record a CUDA event pair around every pass kernel
+ *                        launch of evolve (read back with qaa_get_stats).
+ *  QAA_OPT_STEP_SPANNING 1 (default) = merge the last tile group of step k with
+ *                        the first of step k+1 around D_{k+1};
+ *                        0 = one D per step in the first pass only.
+ *  QAA_OPT_CTAS_PER_SM   persistent-grid CTAs per SM for the pass kernel (1 or 2). */
+enum {
+  QAA_OPT_ROW_BITS = 1,
+  QAA_OPT_PROFILE = 2,
+  QAA_OPT_STEP_SPANNING = 3,
+  QAA_OPT_CTAS_PER_SM = 4
+};
+qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value);
+
+typedef struct {
+  int64_t evolve_calls;      /* since the last reset */
+  int64_t trotter_steps;     /* total Trotter steps applied */
+  int64_t pass_launches;     /* pass-kernel launches (HBM passes over the state) */
+  int64_t other_launches;    /* every other kernel launched by evolve */
+  int64_t passes_per_step_num, passes_per_step_den; /* steady-state ratio of the plan */
+  double pass_kernel_ms;     /* sum of event-timed pass-kernel durations (QAA_OPT_PROFILE) */
+  int64_t pass_kernels_timed;
+  int64_t bytes_per_pass;    /* algorithmic bytes one pass launch moves: 32 B/amp (+1 B/amp E for D passes, averaged) */
+  int64_t amps_local;
+  int n, n_local, groups, tile_bits, row_bits;
+  int64_t kernel_launches_total; /* every kernel this context launched since reset */
+} qaa_stats;
+qaa_status qaa_get_stats(qaa_ctx* ctx, qaa_stats* out);
+qaa_status qaa_reset_stats(qaa_ctx* ctx);
+
+/* ------------------------------------------------------------- host-only planner */
+
+/* Pure host function (no device needed): describe the pass plan evolve uses
+ * for n_local local qubits, row bits c and K steps. Writes up to `cap`
+ * records of QAA_PLAN_RECORD int32 each:
+ *   {group, pre_step, d_step, post_step, pre_lo, pre_hi, post_lo, post_hi,
+ *    n_exchanges, n_shuffles}
+ * where steps are -1 when absent and (lo, hi) are the low/high 32 bits of the
+ * mask of physical qubits rotated for pre_step / post_step. *count = number of
+ * passes (may exceed cap). For n_local <= 12 (resident kernel) every step is
+ * one record {0, -1, k, k, mask, 0, mask, 0, 0, 0}... with pre_mask 0.
+ * Used by the CPU tests of the schedule logic. */
+#define QAA_PLAN_RECORD 10
+qaa_status qaa_plan_describe(int n_local, int row_bits, int step_spanning, int64_t K,
+                             int32_t* records, int64_t cap, int64_t* count);
+
+/* Library version string. */
+const char* qaa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QAA_H */

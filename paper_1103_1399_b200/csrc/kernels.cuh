@@ -1,0 +1,87 @@
+// kernels.cuh -- device-side entry points of libqaa (launch wrappers). The
+// C-ABI in qaa_api.cu is the only caller.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "plan.hpp"
+
+namespace qaa {
+
+// Arguments of one fused Trotter pass (K4). Passed by value
+// (lives in the kernel's constant parameter bank).
+struct PassArgs {
+  double2* psi;            // local state, canonical/physical layout
+  const uint8_t* E;        // energy table, same indexing as psi
+  const double2* phi;      // D row: Phi[e] for e = 0..n_phi-1 (nullptr: no D)
+  int n_phi;
+  int e_pattern;           // register pattern in which D is applied (-1: none)
+  int final_pattern;
+  int nops;
+  double coef[2];          // rotation coefficient per slot (t = tan beta, or cot beta)
+  int form[2];             // 0: tangent form (psi0 + i t psi1); 1: cot form (u psi0 + i psi1)
+  int64_t ntiles;
+  int phys[TILE_BITS];
+  int nseg;
+  int seg_src[MAX_SEGS], seg_dst[MAX_SEGS], seg_len[MAX_SEGS];
+  Op ops[MAX_OPS];
+};
+
+constexpr size_t PASS_SMEM_BYTES = sizeof(double2) * TILE + sizeof(double2) * 256;
+
+cudaError_t launch_pass(const PassArgs& a, int grid, cudaStream_t st);
+cudaError_t pass_kernel_setup();  // opt-in shared memory size
+
+// Whole-evolution kernel for L <= 12 local qubits: one CTA keeps the state in
+// shared memory for all K steps (SURVEY §7 hard part 5; latency-bound sizes).
+struct ResidentArgs {
+  double2* psi;
+  const uint8_t* E;
+  int L;
+  int64_t K;
+  const double2* phi_all;   // K rows of n_phi entries
+  int n_phi;
+  const double* coef;       // K coefficients
+  const int32_t* form;      // K forms
+};
+cudaError_t launch_resident(const ResidentArgs& a, cudaStream_t st);
+
+// Energy table (K1; the paper's kernel):
+// E[x] = sum_c [(xg & M_c) == V_c], xg = x_offset + x, also folding
+// max(E) and the zero count into the given device counters.
+cudaError_t launch_energy_table(uint8_t* E, int64_t N, uint64_t x_offset, const uint64_t* MV, int m,
+                                unsigned* d_max, unsigned long long* d_zeros, int num_sms, cudaStream_t st);
+// Z compaction (A3): writes x_offset + x for every E[x] == 0 (order unspecified).
+cudaError_t launch_compact_zeros(const uint8_t* E, int64_t N, uint64_t x_offset, uint64_t* Z,
+                                 unsigned long long* d_count, int num_sms, cudaStream_t st);
+
+// Initial states (K3).
+cudaError_t launch_fill(double2* psi, int64_t N, double re, double im, int num_sms, cudaStream_t st);
+cudaError_t launch_set_one(double2* psi, int64_t idx, cudaStream_t st);
+
+// Reductions (K5). Deterministic: fixed grid, fixed trees.
+// basic: partial[b*3 + {0,1,2}] = {sum |psi|^2, sum E|psi|^2, sum_{E=0} |psi|^2}
+constexpr int RED_BLOCKS_PER_SM = 2;
+cudaError_t launch_obs_basic(const double2* psi, const uint8_t* E, int64_t N, double* partial, int grid,
+                             cudaStream_t st);
+// sigma^x pair sums for the tile bits of one group geometry (k <= 12 tile bits):
+// partial[b*12 + j] = sum over pairs of tile-local bit j of Re(conj(psi0) psi1).
+struct SigmaArgs {
+  const double2* psi;
+  int k;                    // tile bits (12, or L when L <= 12)
+  uint32_t mask;            // tile-local bits to evaluate
+  int phys[TILE_BITS];
+  int nseg;
+  int seg_src[MAX_SEGS], seg_dst[MAX_SEGS], seg_len[MAX_SEGS];
+  int64_t ntiles;
+};
+cudaError_t launch_obs_sigma(const SigmaArgs& a, double* partial, int grid, cudaStream_t st);
+// sum of |psi[Z[i]]|^2 over a sorted list (1 block).
+cudaError_t launch_gather_success(const double2* psi, const uint64_t* Z, int64_t nz, uint64_t x_offset,
+                                  double* out, cudaStream_t st);
+// out[j] = sum_b partial[b*stride + j] for j < nvals, fixed order (1 block).
+cudaError_t launch_reduce_partials(const double* partial, int nblocks, int stride, int nvals, double* out,
+                                   cudaStream_t st);
+
+}  // namespace qaa

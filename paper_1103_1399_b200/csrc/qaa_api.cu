@@ -1,0 +1,841 @@
+// qaa_api.cu -- the C-ABI of libqaa (include/qaa.h): context, validation,
+// host coefficient builder (H1), pass planning (H2, plan.cpp) and launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/qaa.h"
+#include "kernels.cuh"
+#include "plan.hpp"
+
+using namespace qaa;
+
+namespace {
+constexpr int64_t ZLIST_CAP = 1 << 16;  // keep Z as a sorted list up to this size
+constexpr int RESIDENT_MAX_L = TILE_BITS;
+
+struct ClauseRecHost {
+  uint64_t mhi, vhi;
+  uint32_t spread[4];
+};
+static_assert(sizeof(ClauseRecHost) == 32, "clause record layout");
+}  // namespace
+
+struct qaa_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int rank = 0, world = 1, gbits = 0;
+  int num_sms = 148;
+  // state
+  double2* state = nullptr;
+  bool own_state = false;
+  size_t state_cap_bytes = 0;
+  // instance
+  int n = 0, L = 0, m = 0;
+  bool loaded = false, initialized = false, poisoned = false;
+  uint8_t* E = nullptr;
+  size_t E_cap = 0;
+  uint64_t* Z = nullptr;
+  size_t Z_cap = 0;
+  int64_t nz_local = 0;
+  uint64_t nz_total = 0;
+  bool z_listed = false;
+  unsigned emax = 0;
+  Geometry geom;
+  // coefficient tables
+  void* d_coef = nullptr;
+  size_t d_coef_cap = 0;
+  void* h_coef = nullptr;
+  size_t h_coef_cap = 0;
+  cudaEvent_t coef_done = nullptr;
+  bool coef_pending = false;
+  // reductions
+  double* d_part = nullptr;
+  size_t d_part_cap = 0;
+  double* d_out = nullptr;   // 64 doubles
+  double* h_out = nullptr;   // pinned, 64 doubles
+  unsigned* d_counters = nullptr;  // [0] = max (unsigned), [2..3] = zero count (u64)
+  // options
+  int row_bits = 3;
+  int profile = 0;
+  int step_spanning = 1;
+  int ctas_per_sm = 1;
+  // programs
+  std::map<std::tuple<int, int, int, int>, Program> progs;
+  // stats
+  qaa_stats stats;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+  size_t ev_used = 0;
+  std::string err;
+};
+
+static qaa_status fail(qaa_ctx* c, qaa_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) {
+    c->err = buf;
+    if (st == QAA_E_CUDA || st == QAA_E_NCCL) c->poisoned = true;
+  }
+  return st;
+}
+
+#define CUDA_TRY(call)                                                                      \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(ctx, QAA_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                      \
+  } while (0)
+
+#define CHECK_CTX()                                                             \
+  do {                                                                          \
+    if (!ctx) return QAA_E_USAGE;                                               \
+    if (ctx->poisoned) return fail(ctx, QAA_E_STATE, "context poisoned: %s", ctx->err.c_str()); \
+    cudaSetDevice(ctx->device);                                                 \
+  } while (0)
+
+static qaa_status ensure_buffer(qaa_ctx* ctx, void** p, size_t* cap, size_t bytes) {
+  if (*cap >= bytes && *p) return QAA_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *p = nullptr;
+    return fail(ctx, QAA_E_CAP, "device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+  }
+  *cap = bytes;
+  return QAA_OK;
+}
+
+static qaa_status ensure_host(qaa_ctx* ctx, void** p, size_t* cap, size_t bytes) {
+  if (*cap >= bytes && *p) return QAA_OK;
+  if (*p) cudaFreeHost(*p);
+  *p = nullptr;
+  *cap = 0;
+  CUDA_TRY(cudaMallocHost(p, bytes));
+  *cap = bytes;
+  return QAA_OK;
+}
+
+extern "C" {
+
+const char* qaa_version(void) { return "qaa-b200 0.1 (sm_100a)"; }
+
+qaa_status qaa_create(const qaa_config* cfg, qaa_ctx** out) {
+  if (!cfg || !out) return QAA_E_USAGE;
+  *out = nullptr;
+  if (cfg->world != 1 && cfg->world != 2 && cfg->world != 4 && cfg->world != 8) return QAA_E_USAGE;
+  if (cfg->rank < 0 || cfg->rank >= cfg->world) return QAA_E_USAGE;
+  qaa_ctx* ctx = new (std::nothrow) qaa_ctx();
+  if (!ctx) return QAA_E_CAP;
+  *out = ctx;
+  memset(&ctx->stats, 0, sizeof ctx->stats);
+  ctx->device = cfg->device;
+  ctx->rank = cfg->rank;
+  ctx->world = cfg->world;
+  ctx->gbits = cfg->world == 1 ? 0 : (cfg->world == 2 ? 1 : (cfg->world == 4 ? 2 : 3));
+  if (ctx->world > 1)
+    return fail(ctx, QAA_E_USAGE, "world > 1 requires the NCCL build (not available in this build)");
+  CUDA_TRY(cudaSetDevice(cfg->device));
+  CUDA_TRY(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
+  if (cfg->stream) {
+    ctx->stream = (cudaStream_t)cfg->stream;
+  } else {
+    CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  if (cfg->state) {
+    if (((uintptr_t)cfg->state) % 256 != 0) return fail(ctx, QAA_E_USAGE, "state buffer must be 256-byte aligned");
+    ctx->state = (double2*)cfg->state;
+    ctx->state_cap_bytes = cfg->state_bytes;
+    ctx->own_state = false;
+  }
+  CUDA_TRY(cudaMalloc(&ctx->d_out, 64 * sizeof(double)));
+  CUDA_TRY(cudaMallocHost(&ctx->h_out, 64 * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&ctx->d_counters, 16));
+  CUDA_TRY(cudaEventCreateWithFlags(&ctx->coef_done, cudaEventDisableTiming));
+  CUDA_TRY(pass_kernel_setup());
+  return QAA_OK;
+}
+
+void qaa_destroy(qaa_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->own_state && ctx->state) cudaFree(ctx->state);
+  if (ctx->E) cudaFree(ctx->E);
+  if (ctx->Z) cudaFree(ctx->Z);
+  if (ctx->d_coef) cudaFree(ctx->d_coef);
+  if (ctx->h_coef) cudaFreeHost(ctx->h_coef);
+  if (ctx->d_part) cudaFree(ctx->d_part);
+  if (ctx->d_out) cudaFree(ctx->d_out);
+  if (ctx->h_out) cudaFreeHost(ctx->h_out);
+  if (ctx->d_counters) cudaFree(ctx->d_counters);
+  if (ctx->coef_done) cudaEventDestroy(ctx->coef_done);
+  for (auto& p : ctx->ev_pool) {
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  cudaGetLastError();
+  delete ctx;
+}
+
+const char* qaa_last_error(const qaa_ctx* ctx) {
+  if (!ctx) return "null context";
+  return ctx->err.c_str();
+}
+
+qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
+  if (!ctx) return QAA_E_USAGE;
+  switch (key) {
+    case QAA_OPT_ROW_BITS:
+      if (value < 1 || value > 5) return fail(ctx, QAA_E_USAGE, "row_bits must be in 1..5, got %lld", (long long)value);
+      ctx->row_bits = (int)value;
+      ctx->progs.clear();
+      if (ctx->loaded && ctx->L > RESIDENT_MAX_L) {
+        std::string e;
+        if (!build_geometry(ctx->L, ctx->row_bits, &ctx->geom, &e)) return fail(ctx, QAA_E_USAGE, "%s", e.c_str());
+      }
+      return QAA_OK;
+    case QAA_OPT_PROFILE:
+      ctx->profile = value != 0;
+      return QAA_OK;
+    case QAA_OPT_STEP_SPANNING:
+      ctx->step_spanning = value != 0;
+      return QAA_OK;
+    case QAA_OPT_CTAS_PER_SM:
+      if (value < 1 || value > 4) return fail(ctx, QAA_E_USAGE, "ctas_per_sm must be in 1..4");
+      ctx->ctas_per_sm = (int)value;
+      return QAA_OK;
+    default:
+      return fail(ctx, QAA_E_USAGE, "unknown option key %d", key);
+  }
+}
+
+qaa_status qaa_load_instance(qaa_ctx* ctx, int n, int m, const int32_t* lits) {
+  CHECK_CTX();
+  if (n < 1 || n > 40) return fail(ctx, QAA_E_USAGE, "n must be in 1..40, got %d", n);
+  if (m < 0) return fail(ctx, QAA_E_USAGE, "m must be >= 0, got %d", m);
+  if (m > 0 && !lits) return fail(ctx, QAA_E_USAGE, "lits is NULL with m = %d", m);
+  const int L = n - ctx->gbits;
+  if (L < 1) return fail(ctx, QAA_E_USAGE, "n = %d too small for world = %d", n, ctx->world);
+  for (int i = 0; i < 3 * m; i++)
+    if (lits[i] == 0 || lits[i] > n || lits[i] < -n)
+      return fail(ctx, QAA_E_INPUT, "literal %d of clause %d is %d, outside +-(1..%d)", i % 3, i / 3, lits[i], n);
+  if (m > 255) return fail(ctx, QAA_E_CAP, "m = %d exceeds 255 (uint8 energy table)", m);
+  // encode clauses (A1): violated iff (x & M) == V; drop tautologies.
+  std::vector<ClauseRecHost> recs;
+  for (int c = 0; c < m; c++) {
+    uint64_t M = 0, V = 0;
+    bool taut = false;
+    for (int j = 0; j < 3; j++) {
+      const int l = lits[3 * c + j];
+      const uint64_t bit = 1ull << ((l > 0 ? l : -l) - 1);
+      const uint64_t want = l > 0 ? 0 : bit;  // value of x_|l| that makes the literal false
+      if ((M & bit) && ((V & bit) != want)) taut = true;
+      M |= bit;
+      V |= want;
+    }
+    if (taut) continue;
+    ClauseRecHost r;
+    r.mhi = M & ~15ull;
+    r.vhi = V & ~15ull;
+    memset(r.spread, 0, sizeof r.spread);
+    for (int i = 0; i < 16; i++)
+      if (((uint64_t)i & M & 15ull) == (V & 15ull)) r.spread[i >> 2] |= 1u << (8 * (i & 3));
+    recs.push_back(r);
+  }
+  const int64_t N = (int64_t)1 << L;
+  const size_t state_bytes = (size_t)N * sizeof(double2);
+  // capacity
+  if (!ctx->own_state && ctx->state) {
+    if (ctx->state_cap_bytes < state_bytes)
+      return fail(ctx, QAA_E_CAP, "caller state buffer holds %zu bytes, need %zu for n = %d", ctx->state_cap_bytes,
+                  state_bytes, n);
+  } else {
+    if (ctx->state_cap_bytes < state_bytes) {
+      if (ctx->state) cudaFree(ctx->state);
+      ctx->state = nullptr;
+      ctx->state_cap_bytes = 0;
+      void* p = nullptr;
+      qaa_status st = ensure_buffer(ctx, &p, &ctx->state_cap_bytes, state_bytes);
+      if (st) return fail(ctx, QAA_E_CAP, "state of %zu bytes (n = %d) does not fit on the device", state_bytes, n);
+      ctx->state = (double2*)p;
+      ctx->own_state = true;
+    }
+  }
+  {
+    void* p = ctx->E;
+    qaa_status st = ensure_buffer(ctx, &p, &ctx->E_cap, std::max<size_t>((size_t)N, 16));
+    ctx->E = (uint8_t*)p;
+    if (st) return st;
+  }
+  ctx->loaded = false;
+  ctx->initialized = false;
+  ctx->n = n;
+  ctx->L = L;
+  ctx->m = m;
+  if (L > RESIDENT_MAX_L) {
+    std::string e;
+    if (!build_geometry(L, ctx->row_bits, &ctx->geom, &e)) return fail(ctx, QAA_E_USAGE, "%s", e.c_str());
+  } else {
+    ctx->geom = Geometry();
+  }
+  ctx->progs.clear();
+  // clause records to device (scratch: reuse the coefficient buffer)
+  const size_t rec_bytes = std::max<size_t>(recs.size(), 1) * sizeof(ClauseRecHost);
+  {
+    qaa_status st = ensure_buffer(ctx, &ctx->d_coef, &ctx->d_coef_cap, rec_bytes);
+    if (st) return st;
+  }
+  if (ctx->coef_pending) CUDA_TRY(cudaEventSynchronize(ctx->coef_done));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (!recs.empty())
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_coef, recs.data(), rec_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(ctx->d_counters, 0, 16, ctx->stream));
+  const uint64_t x_offset = (uint64_t)ctx->rank << L;
+  CUDA_TRY(launch_energy_table(ctx->E, N, x_offset, (const uint64_t*)ctx->d_coef, (int)recs.size(), ctx->d_counters,
+                               (unsigned long long*)(ctx->d_counters + 2), ctx->num_sms, ctx->stream));
+  ctx->stats.kernel_launches_total++;
+  unsigned hc[4];
+  CUDA_TRY(cudaMemcpyAsync(hc, ctx->d_counters, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  ctx->emax = hc[0];
+  uint64_t zeros;
+  memcpy(&zeros, &hc[2], 8);
+  ctx->nz_local = (int64_t)zeros;
+  ctx->nz_total = zeros;
+  ctx->z_listed = false;
+  if (ctx->nz_local > 0 && ctx->nz_local <= ZLIST_CAP) {
+    void* p = ctx->Z;
+    qaa_status st = ensure_buffer(ctx, &p, &ctx->Z_cap, (size_t)ctx->nz_local * 8);
+    ctx->Z = (uint64_t*)p;
+    if (st) return st;
+    CUDA_TRY(cudaMemsetAsync(ctx->d_counters, 0, 16, ctx->stream));
+    CUDA_TRY(launch_compact_zeros(ctx->E, N, x_offset, ctx->Z, (unsigned long long*)(ctx->d_counters + 2),
+                                  ctx->num_sms, ctx->stream));
+    ctx->stats.kernel_launches_total++;
+    std::vector<uint64_t> hz((size_t)ctx->nz_local);
+    CUDA_TRY(cudaMemcpyAsync(hz.data(), ctx->Z, hz.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    std::sort(hz.begin(), hz.end());  // fixed order => deterministic gather sum
+    CUDA_TRY(cudaMemcpyAsync(ctx->Z, hz.data(), hz.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    ctx->z_listed = true;
+  }
+  ctx->loaded = true;
+  return QAA_OK;
+}
+
+qaa_status qaa_init_uniform(qaa_ctx* ctx) {
+  CHECK_CTX();
+  if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "init_uniform before load_instance");
+  const double a = 1.0 / std::sqrt(std::ldexp(1.0, ctx->n));
+  CUDA_TRY(launch_fill(ctx->state, (int64_t)1 << ctx->L, a, 0.0, ctx->num_sms, ctx->stream));
+  ctx->stats.kernel_launches_total++;
+  ctx->initialized = true;
+  return QAA_OK;
+}
+
+qaa_status qaa_init_basis(qaa_ctx* ctx, uint64_t x) {
+  CHECK_CTX();
+  if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "init_basis before load_instance");
+  if (ctx->n < 64 && x >= (1ull << ctx->n)) return fail(ctx, QAA_E_USAGE, "basis index %llu >= 2^n", (unsigned long long)x);
+  CUDA_TRY(launch_fill(ctx->state, (int64_t)1 << ctx->L, 0.0, 0.0, ctx->num_sms, ctx->stream));
+  ctx->stats.kernel_launches_total++;
+  if ((int)(x >> ctx->L) == ctx->rank) {
+    CUDA_TRY(launch_set_one(ctx->state, (int64_t)(x & ((1ull << ctx->L) - 1)), ctx->stream));
+    ctx->stats.kernel_launches_total++;
+  }
+  ctx->initialized = true;
+  return QAA_OK;
+}
+
+// H1: per-step coefficients (host, binary64 libm; R11).
+namespace {
+struct StepCoef {
+  double coef;
+  int form;
+};
+}  // namespace
+
+static void build_step(double T, int64_t K, double s, int n, int n_phi, double2* phi_row, StepCoef* sc) {
+  const double dt = T / (double)K;
+  const double theta = dt * s;              // D: exp(-i theta E)
+  const double beta = 0.5 * dt * (1.0 - s);  // X: exp(-i beta (1 - sigma^x)) per qubit
+  const double cb = std::cos(beta), sb = std::sin(beta);
+  double mag;
+  if (std::fabs(sb) <= std::fabs(cb)) {
+    sc->form = 0;
+    sc->coef = sb / cb;  // tan beta
+    mag = cb;
+  } else {
+    sc->form = 1;
+    sc->coef = cb / sb;  // cot beta
+    mag = sb;
+  }
+  const double scale = std::pow(mag, (double)n);  // |(g cos b)^n| (or sin)
+  const double nb = (double)n * beta;             // arg of g^n = -n beta
+  for (int e = 0; e < n_phi; e++) {
+    const double ang = theta * (double)e + nb;
+    phi_row[e] = make_double2(scale * std::cos(ang), -scale * std::sin(ang));
+  }
+}
+
+static qaa_status ensure_events(qaa_ctx* ctx, size_t need) {
+  while (ctx->ev_pool.size() < need) {
+    cudaEvent_t a, b;
+    CUDA_TRY(cudaEventCreate(&a));
+    CUDA_TRY(cudaEventCreate(&b));
+    ctx->ev_pool.push_back({a, b});
+  }
+  return QAA_OK;
+}
+
+static const Program* get_program(qaa_ctx* ctx, int g, bool pre, bool d, bool post) {
+  auto key = std::make_tuple(g, (int)pre, (int)d, (int)post);
+  auto it = ctx->progs.find(key);
+  if (it != ctx->progs.end()) return &it->second;
+  const Group& gr = ctx->geom.groups[g];
+  Program p;
+  if (!build_program(pre ? gr.rot_local : 0u, d, post ? gr.rot_local : 0u, &p)) return nullptr;
+  return &(ctx->progs[key] = p);
+}
+
+qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule) {
+  CHECK_CTX();
+  if (!ctx->loaded || !ctx->initialized) return fail(ctx, QAA_E_STATE, "evolve before load_instance/init");
+  if (!(T >= 0.0) || !std::isfinite(T)) return fail(ctx, QAA_E_USAGE, "T must be finite and >= 0, got %g", T);
+  if (K < 1) return fail(ctx, QAA_E_USAGE, "steps must be >= 1, got %lld", (long long)K);
+  if (schedule)
+    for (int64_t k = 0; k < K; k++)
+      if (!(schedule[k] >= 0.0 && schedule[k] <= 1.0))
+        return fail(ctx, QAA_E_USAGE, "schedule[%lld] = %g outside [0, 1]", (long long)k, schedule[k]);
+  const int n_phi = (int)ctx->emax + 1;
+  const size_t phi_bytes = (size_t)K * n_phi * sizeof(double2);
+  const size_t coef_bytes = (size_t)K * sizeof(double);
+  const size_t form_bytes = (size_t)K * sizeof(int32_t);
+  const size_t total = phi_bytes + coef_bytes + form_bytes + 256;
+  // staging buffer may still be feeding a previous async copy
+  if (ctx->coef_pending) {
+    CUDA_TRY(cudaEventSynchronize(ctx->coef_done));
+    ctx->coef_pending = false;
+  }
+  {
+    qaa_status st = ensure_host(ctx, &ctx->h_coef, &ctx->h_coef_cap, total);
+    if (st) return st;
+  }
+  double2* hphi = (double2*)ctx->h_coef;
+  double* hcoef = (double*)((char*)ctx->h_coef + phi_bytes);
+  int32_t* hform = (int32_t*)((char*)ctx->h_coef + phi_bytes + coef_bytes);
+  std::vector<StepCoef> sc((size_t)K);
+  for (int64_t k = 0; k < K; k++) {
+    const double s = schedule ? schedule[k] : ((double)k + 0.5) / (double)K;  // R8 midpoint
+    build_step(T, K, s, ctx->n, n_phi, hphi + (size_t)k * n_phi, &sc[(size_t)k]);
+    hcoef[k] = sc[(size_t)k].coef;
+    hform[k] = sc[(size_t)k].form;
+  }
+  // the device table is read by kernels still queued from a previous evolve:
+  // growing it must not free memory under them
+  if (ctx->d_coef_cap < total) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  {
+    qaa_status st = ensure_buffer(ctx, &ctx->d_coef, &ctx->d_coef_cap, total);
+    if (st) return st;
+  }
+  CUDA_TRY(cudaMemcpyAsync(ctx->d_coef, ctx->h_coef, total - 256, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(cudaEventRecord(ctx->coef_done, ctx->stream));
+  ctx->coef_pending = true;
+  const double2* dphi = (const double2*)ctx->d_coef;
+  const double* dcoef = (const double*)((char*)ctx->d_coef + phi_bytes);
+  const int32_t* dform = (const int32_t*)((char*)ctx->d_coef + phi_bytes + coef_bytes);
+
+  ctx->stats.evolve_calls++;
+  ctx->stats.trotter_steps += K;
+  if (ctx->L <= RESIDENT_MAX_L) {
+    ResidentArgs ra;
+    ra.psi = ctx->state;
+    ra.E = ctx->E;
+    ra.L = ctx->L;
+    ra.K = K;
+    ra.phi_all = dphi;
+    ra.n_phi = n_phi;
+    ra.coef = dcoef;
+    ra.form = dform;
+    size_t ev = ctx->ev_used;
+    if (ctx->profile) {
+      qaa_status st = ensure_events(ctx, ev + 1);
+      if (st) return st;
+      CUDA_TRY(cudaEventRecord(ctx->ev_pool[ev].first, ctx->stream));
+    }
+    CUDA_TRY(launch_resident(ra, ctx->stream));
+    if (ctx->profile) {
+      CUDA_TRY(cudaEventRecord(ctx->ev_pool[ev].second, ctx->stream));
+      ctx->ev_used = ev + 1;
+    }
+    ctx->stats.pass_launches++;
+    ctx->stats.kernel_launches_total++;
+    return QAA_OK;
+  }
+  std::vector<PassPlan> plan;
+  build_pass_schedule((int)ctx->geom.groups.size(), K, ctx->step_spanning != 0, &plan);
+  const int max_grid = ctx->num_sms * ctx->ctas_per_sm;
+  if (ctx->profile) {
+    qaa_status st = ensure_events(ctx, ctx->ev_used + plan.size());
+    if (st) return st;
+  }
+  PassArgs a;
+  memset(&a, 0, sizeof a);
+  a.psi = ctx->state;
+  a.E = ctx->E;
+  a.n_phi = n_phi;
+  for (const PassPlan& pp : plan) {
+    const Group& gr = ctx->geom.groups[pp.group];
+    const Program* prog = get_program(ctx, pp.group, pp.pre_step >= 0, pp.d_step >= 0, pp.post_step >= 0);
+    if (!prog) return fail(ctx, QAA_E_USAGE, "no register program for group %d", pp.group);
+    a.phi = pp.d_step >= 0 ? dphi + (size_t)pp.d_step * n_phi : nullptr;
+    a.e_pattern = prog->e_pattern;
+    a.final_pattern = prog->final_pattern;
+    a.nops = prog->nops;
+    for (int i = 0; i < prog->nops; i++) a.ops[i] = prog->ops[i];
+    if (pp.pre_step >= 0) {
+      a.coef[0] = sc[(size_t)pp.pre_step].coef;
+      a.form[0] = sc[(size_t)pp.pre_step].form;
+    }
+    if (pp.post_step >= 0) {
+      a.coef[1] = sc[(size_t)pp.post_step].coef;
+      a.form[1] = sc[(size_t)pp.post_step].form;
+    }
+    a.ntiles = gr.ntiles;
+    for (int b = 0; b < TILE_BITS; b++) a.phys[b] = gr.phys[b];
+    a.nseg = gr.nseg;
+    for (int s = 0; s < gr.nseg; s++) {
+      a.seg_src[s] = gr.seg_src[s];
+      a.seg_dst[s] = gr.seg_dst[s];
+      a.seg_len[s] = gr.seg_len[s];
+    }
+    const int grid = (int)std::min<int64_t>(gr.ntiles, max_grid);
+    if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
+    CUDA_TRY(launch_pass(a, grid, ctx->stream));
+    if (ctx->profile) {
+      CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, ctx->stream));
+      ctx->ev_used++;
+    }
+    ctx->stats.pass_launches++;
+    ctx->stats.kernel_launches_total++;
+  }
+  return QAA_OK;
+}
+
+// ------------------------------------------------------------------ observables
+static qaa_status ensure_part(qaa_ctx* ctx, size_t doubles) {
+  void* p = ctx->d_part;
+  qaa_status st = ensure_buffer(ctx, &p, &ctx->d_part_cap, doubles * sizeof(double));
+  ctx->d_part = (double*)p;
+  return st;
+}
+
+// basic[0..2] = {norm2, <H_P>, sum_{E=0}|psi|^2}
+static qaa_status obs_basic(qaa_ctx* ctx, double* basic) {
+  const int64_t N = (int64_t)1 << ctx->L;
+  int grid = ctx->num_sms * RED_BLOCKS_PER_SM;
+  if ((int64_t)grid * 256 > N) grid = (int)std::max<int64_t>(1, (N + 255) / 256);
+  qaa_status st = ensure_part(ctx, (size_t)grid * 3);
+  if (st) return st;
+  CUDA_TRY(launch_obs_basic(ctx->state, ctx->E, N, ctx->d_part, grid, ctx->stream));
+  CUDA_TRY(launch_reduce_partials(ctx->d_part, grid, 3, 3, ctx->d_out, ctx->stream));
+  ctx->stats.kernel_launches_total += 2;
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_out, ctx->d_out, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  for (int j = 0; j < 3; j++) basic[j] = ctx->h_out[j];
+  return QAA_OK;
+}
+
+// sx[j] = <sigma^x_j> for local qubits j < L
+static qaa_status obs_sigma(qaa_ctx* ctx, double* sx) {
+  std::vector<SigmaArgs> jobs;
+  if (ctx->L <= RESIDENT_MAX_L) {
+    SigmaArgs a;
+    memset(&a, 0, sizeof a);
+    a.psi = ctx->state;
+    a.k = ctx->L;
+    a.mask = (1u << ctx->L) - 1;
+    for (int b = 0; b < TILE_BITS; b++) a.phys[b] = b < ctx->L ? b : 0;
+    a.nseg = 0;
+    a.ntiles = 1;
+    jobs.push_back(a);
+  } else {
+    for (const Group& g : ctx->geom.groups) {
+      SigmaArgs a;
+      memset(&a, 0, sizeof a);
+      a.psi = ctx->state;
+      a.k = TILE_BITS;
+      a.mask = g.rot_local;
+      for (int b = 0; b < TILE_BITS; b++) a.phys[b] = g.phys[b];
+      a.nseg = g.nseg;
+      for (int s = 0; s < g.nseg; s++) {
+        a.seg_src[s] = g.seg_src[s];
+        a.seg_dst[s] = g.seg_dst[s];
+        a.seg_len[s] = g.seg_len[s];
+      }
+      a.ntiles = g.ntiles;
+      jobs.push_back(a);
+    }
+  }
+  for (const SigmaArgs& a : jobs) {
+    const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)ctx->num_sms * 2);
+    qaa_status st = ensure_part(ctx, (size_t)grid * TILE_BITS);
+    if (st) return st;
+    CUDA_TRY(launch_obs_sigma(a, ctx->d_part, grid, ctx->stream));
+    CUDA_TRY(launch_reduce_partials(ctx->d_part, grid, TILE_BITS, TILE_BITS, ctx->d_out, ctx->stream));
+    ctx->stats.kernel_launches_total += 2;
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_out, ctx->d_out, TILE_BITS * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    for (int j = 0; j < a.k; j++)
+      if (a.mask >> j & 1) sx[a.phys[j]] = 2.0 * ctx->h_out[j];
+  }
+  return QAA_OK;
+}
+
+qaa_status qaa_success_prob(qaa_ctx* ctx, double* out) {
+  CHECK_CTX();
+  if (!out) return fail(ctx, QAA_E_USAGE, "out is NULL");
+  if (!ctx->loaded || !ctx->initialized) return fail(ctx, QAA_E_STATE, "success_prob before init");
+  if (ctx->nz_local == 0) {
+    *out = 0.0;
+    return QAA_OK;
+  }
+  if (ctx->z_listed) {
+    CUDA_TRY(launch_gather_success(ctx->state, ctx->Z, ctx->nz_local, (uint64_t)ctx->rank << ctx->L, ctx->d_out,
+                                   ctx->stream));
+    ctx->stats.kernel_launches_total++;
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_out, ctx->d_out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    *out = ctx->h_out[0];
+    return QAA_OK;
+  }
+  double b[3];
+  qaa_status st = obs_basic(ctx, b);
+  if (st) return st;
+  *out = b[2];
+  return QAA_OK;
+}
+
+qaa_status qaa_norm2(qaa_ctx* ctx, double* out) {
+  CHECK_CTX();
+  if (!out) return fail(ctx, QAA_E_USAGE, "out is NULL");
+  if (!ctx->loaded || !ctx->initialized) return fail(ctx, QAA_E_STATE, "norm2 before init");
+  double b[3];
+  qaa_status st = obs_basic(ctx, b);
+  if (st) return st;
+  *out = b[0];
+  return QAA_OK;
+}
+
+qaa_status qaa_sigma_x(qaa_ctx* ctx, double* out) {
+  CHECK_CTX();
+  if (!out) return fail(ctx, QAA_E_USAGE, "out is NULL");
+  if (!ctx->loaded || !ctx->initialized) return fail(ctx, QAA_E_STATE, "sigma_x before init");
+  return obs_sigma(ctx, out);
+}
+
+qaa_status qaa_energy(qaa_ctx* ctx, double s, double* out) {
+  CHECK_CTX();
+  if (!out) return fail(ctx, QAA_E_USAGE, "out is NULL");
+  if (!(s >= 0.0 && s <= 1.0)) return fail(ctx, QAA_E_USAGE, "s = %g outside [0, 1]", s);
+  if (!ctx->loaded || !ctx->initialized) return fail(ctx, QAA_E_STATE, "energy before init");
+  double b[3];
+  qaa_status st = obs_basic(ctx, b);
+  if (st) return st;
+  std::vector<double> sx((size_t)ctx->n, 0.0);
+  st = obs_sigma(ctx, sx.data());
+  if (st) return st;
+  double hb = 0.0;
+  for (int j = 0; j < ctx->n; j++) hb += 0.5 * (b[0] - sx[(size_t)j]);
+  *out = (1.0 - s) * hb + s * b[1];
+  return QAA_OK;
+}
+
+qaa_status qaa_num_solutions(qaa_ctx* ctx, uint64_t* out) {
+  CHECK_CTX();
+  if (!out) return fail(ctx, QAA_E_USAGE, "out is NULL");
+  if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "num_solutions before load_instance");
+  *out = ctx->nz_total;
+  return QAA_OK;
+}
+
+qaa_status qaa_max_energy(qaa_ctx* ctx, uint32_t* out) {
+  CHECK_CTX();
+  if (!out) return fail(ctx, QAA_E_USAGE, "out is NULL");
+  if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "max_energy before load_instance");
+  *out = ctx->emax;
+  return QAA_OK;
+}
+
+static bool local_range(qaa_ctx* ctx, uint64_t first, uint64_t count, uint64_t* lo, uint64_t* hi) {
+  const uint64_t own_lo = (uint64_t)ctx->rank << ctx->L, own_hi = own_lo + (1ull << ctx->L);
+  *lo = std::max(first, own_lo);
+  *hi = std::min(first + count, own_hi);
+  return *lo < *hi;
+}
+
+qaa_status qaa_copy_state(qaa_ctx* ctx, uint64_t first, uint64_t count, double* dst) {
+  CHECK_CTX();
+  if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "copy_state before load_instance");
+  if (count && !dst) return fail(ctx, QAA_E_USAGE, "dst is NULL");
+  if (first + count > (1ull << ctx->n) || first + count < first)
+    return fail(ctx, QAA_E_USAGE, "range [%llu, +%llu) outside [0, 2^%d)", (unsigned long long)first,
+                (unsigned long long)count, ctx->n);
+  uint64_t lo, hi;
+  if (local_range(ctx, first, count, &lo, &hi)) {
+    const uint64_t off = lo - ((uint64_t)ctx->rank << ctx->L);
+    CUDA_TRY(cudaMemcpyAsync(dst + 2 * (lo - first), ctx->state + off, (hi - lo) * sizeof(double2),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return QAA_OK;
+}
+
+qaa_status qaa_set_state(qaa_ctx* ctx, uint64_t first, uint64_t count, const double* src) {
+  CHECK_CTX();
+  if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "set_state before load_instance");
+  if (count && !src) return fail(ctx, QAA_E_USAGE, "src is NULL");
+  if (first + count > (1ull << ctx->n) || first + count < first)
+    return fail(ctx, QAA_E_USAGE, "range outside [0, 2^%d)", ctx->n);
+  uint64_t lo, hi;
+  if (local_range(ctx, first, count, &lo, &hi)) {
+    const uint64_t off = lo - ((uint64_t)ctx->rank << ctx->L);
+    CUDA_TRY(cudaMemcpyAsync(ctx->state + off, src + 2 * (lo - first), (hi - lo) * sizeof(double2),
+                             cudaMemcpyHostToDevice, ctx->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  ctx->initialized = true;
+  return QAA_OK;
+}
+
+qaa_status qaa_copy_energy_table(qaa_ctx* ctx, uint64_t first, uint64_t count, uint8_t* dst) {
+  CHECK_CTX();
+  if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "copy_energy_table before load_instance");
+  if (count && !dst) return fail(ctx, QAA_E_USAGE, "dst is NULL");
+  if (first + count > (1ull << ctx->n) || first + count < first)
+    return fail(ctx, QAA_E_USAGE, "range outside [0, 2^%d)", ctx->n);
+  uint64_t lo, hi;
+  if (local_range(ctx, first, count, &lo, &hi)) {
+    const uint64_t off = lo - ((uint64_t)ctx->rank << ctx->L);
+    CUDA_TRY(cudaMemcpyAsync(dst + (lo - first), ctx->E + off, hi - lo, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return QAA_OK;
+}
+
+qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps) {
+  CHECK_CTX();
+  if (!out || !amps) return fail(ctx, QAA_E_USAGE, "NULL output");
+  if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "state_ptr before load_instance");
+  *out = ctx->state;
+  *amps = 1ull << ctx->L;
+  return QAA_OK;
+}
+
+qaa_status qaa_get_stats(qaa_ctx* ctx, qaa_stats* out) {
+  CHECK_CTX();
+  if (!out) return fail(ctx, QAA_E_USAGE, "out is NULL");
+  if (ctx->ev_used) {
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    for (size_t i = 0; i < ctx->ev_used; i++) {
+      float ms = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&ms, ctx->ev_pool[i].first, ctx->ev_pool[i].second));
+      ctx->stats.pass_kernel_ms += ms;
+      ctx->stats.pass_kernels_timed++;
+    }
+    ctx->ev_used = 0;
+  }
+  qaa_stats s = ctx->stats;
+  s.n = ctx->n;
+  s.n_local = ctx->L;
+  s.amps_local = ctx->loaded ? ((int64_t)1 << ctx->L) : 0;
+  s.groups = ctx->L > RESIDENT_MAX_L ? (int)ctx->geom.groups.size() : 1;
+  s.tile_bits = ctx->L > RESIDENT_MAX_L ? TILE_BITS : ctx->L;
+  s.row_bits = ctx->row_bits;
+  const int P = s.groups;
+  s.passes_per_step_num = (ctx->step_spanning && P > 1) ? P - 1 : P;
+  s.passes_per_step_den = 1;
+  s.bytes_per_pass = s.amps_local * 32;
+  *out = s;
+  return QAA_OK;
+}
+
+qaa_status qaa_reset_stats(qaa_ctx* ctx) {
+  CHECK_CTX();
+  if (ctx->ev_used) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  ctx->ev_used = 0;
+  memset(&ctx->stats, 0, sizeof ctx->stats);
+  return QAA_OK;
+}
+
+qaa_status qaa_plan_describe(int n_local, int row_bits, int step_spanning, int64_t K, int32_t* rec, int64_t cap,
+                             int64_t* count) {
+  if (!count || n_local < 1 || n_local > 40 || K < 1 || (cap > 0 && !rec)) return QAA_E_USAGE;
+  if (n_local <= RESIDENT_MAX_L) {
+    const uint64_t mask = (n_local >= 64) ? ~0ull : ((1ull << n_local) - 1);
+    for (int64_t k = 0; k < K && k < cap; k++) {
+      int32_t* r = rec + k * QAA_PLAN_RECORD;
+      r[0] = 0;
+      r[1] = -1;
+      r[2] = (int32_t)k;
+      r[3] = (int32_t)k;
+      r[4] = 0;
+      r[5] = 0;
+      r[6] = (int32_t)(mask & 0xffffffffu);
+      r[7] = (int32_t)(mask >> 32);
+      r[8] = 0;
+      r[9] = 0;
+    }
+    *count = K;
+    return QAA_OK;
+  }
+  Geometry g;
+  std::string e;
+  if (!build_geometry(n_local, row_bits, &g, &e)) return QAA_E_USAGE;
+  std::vector<PassPlan> plan;
+  build_pass_schedule((int)g.groups.size(), K, step_spanning != 0, &plan);
+  *count = (int64_t)plan.size();
+  for (int64_t i = 0; i < (int64_t)plan.size() && i < cap; i++) {
+    const PassPlan& pp = plan[(size_t)i];
+    const Group& gr = g.groups[pp.group];
+    Program prog;
+    if (!build_program(pp.pre_step >= 0 ? gr.rot_local : 0u, pp.d_step >= 0, pp.post_step >= 0 ? gr.rot_local : 0u,
+                       &prog))
+      return QAA_E_USAGE;
+    const uint64_t pre = pp.pre_step >= 0 ? gr.rot_phys : 0, post = pp.post_step >= 0 ? gr.rot_phys : 0;
+    int32_t* r = rec + i * QAA_PLAN_RECORD;
+    r[0] = pp.group;
+    r[1] = (int32_t)pp.pre_step;
+    r[2] = (int32_t)pp.d_step;
+    r[3] = (int32_t)pp.post_step;
+    r[4] = (int32_t)(pre & 0xffffffffu);
+    r[5] = (int32_t)(pre >> 32);
+    r[6] = (int32_t)(post & 0xffffffffu);
+    r[7] = (int32_t)(post >> 32);
+    r[8] = prog.n_exch;
+    r[9] = prog.n_shfl;
+  }
+  return QAA_OK;
+}
+
+}  // extern "C"

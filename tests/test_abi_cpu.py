@@ -1,0 +1,134 @@
+"""CPU-side tests of the product library: the C-ABI loads and exports every
+symbol include/qaa.h declares, and the host pass planner (H2) is correct.
+No GPU compute calls here."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def q():
+    import paper_1103_1399_b200 as q
+    from paper_1103_1399_b200 import build
+    build.build()
+    q.lib()
+    return q
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "qaa.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(qaa_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported(q):
+    funcs = header_functions()
+    assert len(funcs) >= 20
+    L = q.lib()
+    for f in funcs:
+        assert hasattr(L, f), f"{f} declared in qaa.h but not exported"
+    assert sorted(q.qaa.EXPORTS) == funcs
+
+
+def test_exports_are_c_symbols(q):
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", q.library_path], capture_output=True, text=True).stdout
+    syms = set(re.findall(r"\bT (qaa_\w+)", out))
+    assert set(header_functions()) <= syms
+
+
+def test_library_is_sm100a(q):
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", q.library_path],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_create_without_gpu_fails_cleanly(q):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(q.QaaError) as ei:
+        q.qaa_create(0)
+    assert ei.value.status == 5  # QAA_E_CUDA, no crash
+
+
+def test_usage_errors_without_gpu(q):
+    with pytest.raises(q.QaaError):
+        q.qaa_create(world=3)
+    with pytest.raises(q.QaaError):
+        q.qaa_create(rank=2, world=2)
+
+
+def simulate(rec, L, K):
+    """Replays a pass plan symbolically: checks D_0..D_{K-1} appear once each, in
+    order, and that between D_k and D_{k+1} (and after D_{K-1}) every qubit is
+    rotated exactly once, for step k."""
+    rot = {}  # (step, qubit) -> count
+    d_seen = []
+    cur = None  # the step whose D was applied last
+    for r in rec:
+        g, pre, d, post = int(r[0]), int(r[1]), int(r[2]), int(r[3])
+        pre_mask = (int(r[4]) & 0xffffffff) | ((int(r[5]) & 0xffffffff) << 32)
+        post_mask = (int(r[6]) & 0xffffffff) | ((int(r[7]) & 0xffffffff) << 32)
+        if pre >= 0:
+            assert pre == cur, "rotation for a step other than the current one"
+            for j in range(L):
+                if pre_mask >> j & 1:
+                    rot[(pre, j)] = rot.get((pre, j), 0) + 1
+        if d >= 0:
+            if cur is not None:  # step cur must be complete before D_{cur+1}
+                assert all(rot.get((cur, j), 0) == 1 for j in range(L)), (cur, rot)
+            assert d == (0 if cur is None else cur + 1)
+            d_seen.append(d)
+            cur = d
+        if post >= 0:
+            assert post == cur
+            for j in range(L):
+                if post_mask >> j & 1:
+                    rot[(post, j)] = rot.get((post, j), 0) + 1
+    assert d_seen == list(range(K))
+    for k in range(K):
+        for j in range(L):
+            assert rot.get((k, j), 0) == 1, (k, j)
+
+
+@pytest.mark.parametrize("L", [1, 5, 12, 13, 14, 16, 20, 21, 22, 24, 27, 30, 31, 33])
+@pytest.mark.parametrize("c", [3, 4])
+@pytest.mark.parametrize("span", [0, 1])
+def test_plan_covers_every_qubit_once_per_step(q, L, c, span):
+    for K in (1, 2, 3, 7):
+        rec = q.qaa_plan_describe(L, c, span, K)
+        simulate(rec, L, K)
+
+
+@pytest.mark.parametrize("L,c,P", [(13, 3, 2), (21, 3, 2), (22, 3, 3), (30, 3, 3), (31, 3, 4), (30, 4, 4),
+                                   (24, 3, 3), (16, 4, 2)])
+def test_plan_pass_counts(q, L, c, P):
+    """P tile groups: K*(P-1)+1 passes with step spanning, K*P without."""
+    K = 10
+    rec = q.qaa_plan_describe(L, c, 1, K)
+    assert len(set(int(g) for g in rec[:, 0])) == P
+    assert len(rec) == (K * (P - 1) + 1 if P > 1 else K)
+    assert len(q.qaa_plan_describe(L, c, 0, K)) == K * P
+
+
+def test_plan_register_programs_cost(q):
+    """Exchange/shuffle counts of the n = 30, c = 3 plan (DESIGN.md §4 table)."""
+    rec = q.qaa_plan_describe(30, 3, 1, 4)
+    costs = {(int(r[0]), int(r[2]) >= 0, int(r[1]) >= 0): (int(r[8]), int(r[9])) for r in rec}
+    assert costs[(0, True, False)] == (2, 0)   # first pass: D0 then 12 rotations
+    assert costs[(1, False, True)] == (1, 1)   # 9 rotations: regs + one exchange + one lane shuffle
+    assert costs[(2, True, True)] == (2, 2)    # D pass on a 9-qubit group
+    assert costs[(0, True, True)] == (4, 0)    # D pass on the 12-qubit group
+
+
+def test_plan_rejects_bad_args(q):
+    with pytest.raises(q.QaaError):
+        q.qaa_plan_describe(0, 3, 1, 1)
+    with pytest.raises(q.QaaError):
+        q.qaa_plan_describe(20, 9, 1, 1)

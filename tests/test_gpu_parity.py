@@ -1,0 +1,333 @@
+"""GPU parity: libqaa (through its C-ABI) against the CPU oracle, element by
+element on the same seeded inputs (DESIGN.md §6 tolerances).
+
+Tolerance (BASELINE north_star): |psi_gpu - psi_oracle| <= 1e-10 absolute per
+amplitude. Because amplitudes shrink like 2^{-n/2}, we also bound the relative
+l2 error ||d|| / ||psi|| <= RTOL_L2 = 1e-11, derived from the rounding budget
+K * (n + 4) * eps with K <= 1000, n <= 24.
+"""
+import numpy as np
+import pytest
+
+from inputs import cnf
+
+pytestmark = pytest.mark.gpu
+
+ATOL = 1e-10
+RTOL_L2 = 1e-11
+
+
+@pytest.fixture(scope="module")
+def q():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1103_1399_b200 as q
+    return q
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle import oracle
+    oracle.build()
+    return oracle
+
+
+@pytest.fixture()
+def ctx(q):
+    c = q.Context(0)
+    yield c
+    c.close()
+
+
+def assert_close(got, want, atol=ATOL, rtol_l2=RTOL_L2):
+    d = np.abs(got - want)
+    assert np.max(d) <= atol, f"max abs err {np.max(d):.3e}"
+    rel = np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-300)
+    assert rel <= rtol_l2, f"relative l2 err {rel:.3e}"
+
+
+def instance(n, seed=None):
+    if n in (8, 10, 12, 13, 14, 16, 20, 24, 30):
+        return cnf.load_instance(n)[0]
+    return cnf.random_instance(n, max(1, int(round(4.3 * n))), seed if seed is not None else 1000 + n)
+
+
+# ------------------------------------------------------------------ K1 / K2
+@pytest.mark.parametrize("n", [3, 4, 6, 8, 11, 12, 13, 16, 20, 24])
+def test_energy_table_exact(ctx, orc, n):
+    cl = instance(n)
+    ctx.load_instance(n, cl)
+    Eg = ctx.energy_table()
+    Eo = orc.energy_table(n, cl)
+    assert np.array_equal(Eg.astype(np.uint16), Eo)
+    assert ctx.num_solutions() == int((Eo == 0).sum())
+    assert ctx.max_energy() == int(Eo.max())
+
+
+def test_energy_table_paper_instances(ctx, orc):
+    for corrected, sol in ((False, 10), (True, 11)):
+        n, cl = cnf.paper_instance(corrected)
+        ctx.load_instance(n, cl)
+        Eg = ctx.energy_table()
+        assert np.array_equal(Eg.astype(np.uint16), orc.energy_table(n, cl))
+        assert list(np.flatnonzero(Eg == 0)) == [sol]
+
+
+def test_energy_table_degenerate(ctx, orc):
+    n = 5
+    cl = [(1, -1, 2), (2, 2, 3), (2, 2, 3), (-5, -5, -5), (1, 2, 3)]
+    ctx.load_instance(n, cl)
+    assert np.array_equal(ctx.energy_table().astype(np.uint16), orc.energy_table(n, cl))
+    ctx.load_instance(n, [])
+    assert np.all(ctx.energy_table() == 0) and ctx.num_solutions() == 32
+
+
+def test_energy_table_n30_sampled(ctx, orc):
+    n = 30
+    cl, sol = cnf.load_instance(30)
+    ctx.load_instance(n, cl)
+    assert ctx.num_solutions() == 1
+    rng = np.random.default_rng(5)
+    xs = np.unique(np.concatenate([rng.integers(0, 1 << n, 4000, dtype=np.uint64),
+                                   np.arange(0, 2048, dtype=np.uint64),
+                                   np.array([sol, (1 << n) - 1], dtype=np.uint64)]))
+    want = orc.energy_at(n, cl, xs)
+    got = np.array([ctx.energy_table(int(x), 1)[0] for x in xs[:300]], dtype=np.uint16)
+    assert np.array_equal(got, want[:300])
+    blk = ctx.energy_table(0, 2048)
+    assert np.array_equal(blk.astype(np.uint16), orc.energy_at(n, cl, np.arange(2048, dtype=np.uint64)))
+    assert ctx.energy_table(sol, 1)[0] == 0
+
+
+# ------------------------------------------------------------------ evolution parity
+def run_both(q, ctx, orc, n, cl, T, K, schedule=None, psi0=None, row_bits=None, span=None):
+    if row_bits is not None:
+        ctx.set_option(q.OPT_ROW_BITS, row_bits)
+    if span is not None:
+        ctx.set_option(q.OPT_STEP_SPANNING, span)
+    ctx.load_instance(n, cl)
+    E = orc.energy_table(n, cl)
+    if psi0 is None:
+        ctx.init_uniform()
+        psi0 = orc.init_uniform(n)
+    else:
+        ctx.set_state(psi0)
+    ctx.evolve(T, K, schedule)
+    got = ctx.state()
+    want = orc.evolve(n, E, psi0, T, K, schedule)
+    return got, want, E
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 11, 12])
+def test_resident_parity(q, ctx, orc, n):
+    cl = instance(n) if n >= 3 else [(1, 1, -n)]
+    psi0 = cnf.random_state(n, n)
+    got, want, _ = run_both(q, ctx, orc, n, cl, 3.0, 17, psi0=psi0)
+    assert_close(got, want)
+
+
+@pytest.mark.parametrize("n", [13, 14, 15, 16, 18, 21, 22, 23])
+@pytest.mark.parametrize("span", [1, 0])
+def test_pass_parity_small(q, ctx, orc, n, span):
+    cl = instance(n)
+    psi0 = cnf.random_state(n, 100 + n)
+    sched = np.random.default_rng(n).uniform(0, 1, 5)
+    got, want, _ = run_both(q, ctx, orc, n, cl, 2.5, 5, schedule=sched, psi0=psi0, span=span)
+    assert_close(got, want)
+
+
+@pytest.mark.parametrize("c", [3, 4, 5])
+def test_pass_parity_row_bits(q, ctx, orc, c):
+    n = 22
+    cl = instance(n)
+    psi0 = cnf.random_state(n, 7)
+    got, want, _ = run_both(q, ctx, orc, n, cl, 1.7, 4, psi0=psi0, row_bits=c)
+    assert_close(got, want)
+    ctx.set_option(q.OPT_ROW_BITS, 3)
+
+
+def test_cot_form_large_beta(q, ctx, orc):
+    """|beta| > pi/4 selects the cot form (u psi0 + i psi1) on both kernels."""
+    for n in (10, 17):
+        cl = instance(n)
+        psi0 = cnf.random_state(n, 3)
+        sched = np.array([0.0, 0.1, 0.5, 0.95, 0.0])
+        got, want, _ = run_both(q, ctx, orc, n, cl, 2.0 * 5 * 1.3, 5, schedule=sched, psi0=psi0)  # beta up to 1.3
+        assert_close(got, want)
+
+
+def test_config1_n8_full(q, ctx, orc):
+    """BASELINE configs[0]: n = 8 unique-solution instance, T = 10, 100 steps."""
+    cl, sol = cnf.load_instance(8)
+    got, want, E = run_both(q, ctx, orc, 8, cl, 10.0, 100)
+    assert_close(got, want)
+    ps = ctx.success_prob()
+    assert abs(ps - abs(want[sol]) ** 2) < 1e-13
+
+
+def test_config2_n16_full(q, ctx, orc):
+    """BASELINE configs[1]: n = 16, T = 50, 1000 steps (full oracle run)."""
+    cl, sol = cnf.load_instance(16)
+    got, want, E = run_both(q, ctx, orc, 16, cl, 50.0, 1000)
+    assert_close(got, want)
+    assert abs(ctx.success_prob() - abs(want[sol]) ** 2) < 1e-12
+
+
+def test_config3_n24_first_steps(q, ctx, orc):
+    """BASELINE configs[2]: n = 24, T = 100, K = 5000: the first 10 steps of that
+    schedule (dt = 0.02) against the oracle, element by element."""
+    cl, sol = cnf.load_instance(24)
+    K, Kp = 5000, 10
+    sched = (np.arange(Kp) + 0.5) / K
+    got, want, E = run_both(q, ctx, orc, 24, cl, 100.0 / K * Kp, Kp, schedule=sched)
+    assert_close(got, want)
+
+
+# ------------------------------------------------------------------ n = 30 (full size) closed forms
+@pytest.fixture(scope="module")
+def ctx30(q):
+    c = q.Context(0)
+    cl, sol = cnf.load_instance(30)
+    c.load_instance(30, cl)
+    yield c, cl, sol
+    c.close()
+
+
+def test_n30_s_one_closed_form(ctx30, orc):
+    """s = 1: psi_K(x) = 2^{-15} e^{-i T E(x)} (sampled x, E from the oracle)."""
+    c, cl, sol = ctx30
+    c.init_uniform()
+    T, K = 0.37, 6
+    c.evolve(T, K, np.ones(K))
+    rng = np.random.default_rng(1)
+    starts = rng.integers(0, (1 << 30) - 64, 40)
+    for s0 in starts:
+        xs = np.arange(s0, s0 + 64, dtype=np.uint64)
+        want = 2.0 ** -15 * np.exp(-1j * T * orc.energy_at(30, cl, xs).astype(float))
+        assert_close(c.state(int(s0), 64), want, atol=1e-15, rtol_l2=1e-12)
+
+
+def test_n30_s_zero_basis_closed_form(ctx30):
+    """s = 0 from |x0>: product closed form with Theta = T/2, sampled."""
+    c, cl, sol = ctx30
+    x0 = 0x2A5A5A5A
+    c.init_basis(x0)
+    T, K = 1.1, 4
+    c.evolve(T, K, np.zeros(K))
+    th = T / 2
+    same = np.exp(-1j * th) * np.cos(th)
+    diff = 1j * np.exp(-1j * th) * np.sin(th)
+    rng = np.random.default_rng(2)
+    for s0 in list(rng.integers(0, (1 << 30) - 32, 30)) + [x0 - 8]:
+        ys = np.arange(s0, s0 + 32, dtype=np.int64)
+        flips = np.array([bin(int(y) ^ x0).count("1") for y in ys])
+        want = same ** (30 - flips) * diff ** flips
+        assert_close(c.state(int(s0), 32), want, atol=1e-15, rtol_l2=1e-12)
+
+
+def test_n30_uniform_observables_and_norm(ctx30, q):
+    """t = 0 closed forms at full size: ||psi||^2 = 1, <H_P> = m/8, <H_B> = 0,
+    P_succ = 2^-30; then 8 Trotter steps conserve the norm to 1e-12."""
+    c, cl, sol = ctx30
+    c.init_uniform()
+    m = len(cl)
+    assert abs(c.norm2() - 1) < 1e-12
+    assert abs(c.energy(1.0) - m / 8) < 1e-10
+    assert abs(c.energy(0.0)) < 1e-10
+    assert abs(c.success_prob() - 2.0 ** -30) < 1e-20
+    c.evolve(0.16, 8, (np.arange(8) + 0.5) / 10000)
+    assert abs(c.norm2() - 1) < 1e-12
+
+
+def test_n30_determinism(ctx30):
+    c, cl, sol = ctx30
+    outs = []
+    for _ in range(2):
+        c.init_uniform()
+        c.evolve(0.1, 5)
+        outs.append(np.concatenate([c.state(0, 4096), c.state(sol - 100, 200), c.state((1 << 30) - 4096, 4096)]))
+    assert np.array_equal(outs[0], outs[1])
+
+
+# ------------------------------------------------------------------ observables
+@pytest.mark.parametrize("n", [6, 10, 16, 21])
+def test_observables_parity(q, ctx, orc, n):
+    cl = instance(n)
+    psi0 = cnf.random_state(n, 11)
+    got, want, E = run_both(q, ctx, orc, n, cl, 1.3, 3, psi0=psi0)
+    ob = orc.observables(n, E, want)
+    assert abs(ctx.norm2() - ob["norm2"]) < 1e-12 * max(1, ob["norm2"])
+    assert np.allclose(ctx.sigma_x(), ob["sigma_x"], atol=1e-12, rtol=0)
+    for s in (0.0, 0.4, 1.0):
+        assert abs(ctx.energy(s) - orc.energy(n, E, want, s)) < 1e-11
+    assert abs(ctx.success_prob() - ob["success"]) < 1e-13
+
+
+def test_success_prob_full_pass_path(q, ctx, orc):
+    """Many solutions (|Z| > list cap) -> the full-pass reduction path."""
+    n = 18
+    cl = [(1, 2, 3)]
+    psi0 = cnf.random_state(n, 4)
+    got, want, E = run_both(q, ctx, orc, n, cl, 0.5, 2, psi0=psi0)
+    assert ctx.num_solutions() == (1 << 18) - (1 << 15)
+    assert abs(ctx.success_prob() - orc.observables(n, E, want)["success"]) < 1e-12
+
+
+def test_unsat_success_zero(q, ctx):
+    unsat = [(a * 1, b * 2, c * 3) for a in (1, -1) for b in (1, -1) for c in (1, -1)]
+    ctx.load_instance(3, unsat)
+    ctx.init_uniform()
+    ctx.evolve(5.0, 50)
+    assert ctx.success_prob() == 0.0
+
+
+def test_T_zero_identity(q, ctx):
+    for n in (9, 20):
+        ctx.load_instance(n, instance(n))
+        psi0 = cnf.random_state(n, 1)
+        ctx.set_state(psi0)
+        ctx.evolve(0.0, 3)
+        assert np.array_equal(ctx.state(), psi0)
+
+
+# ------------------------------------------------------------------ error behaviour
+def test_error_codes(q, ctx):
+    with pytest.raises(q.QaaError) as e:
+        ctx.init_uniform()
+    assert e.value.status == 4
+    with pytest.raises(q.QaaError) as e:
+        ctx.load_instance(4, [(1, 2, 5)])
+    assert e.value.status == 2
+    with pytest.raises(q.QaaError) as e:
+        ctx.load_instance(4, [(1, 2, 3)] * 256)
+    assert e.value.status == 3
+    ctx.load_instance(4, [(1, 2, 3)])
+    with pytest.raises(q.QaaError) as e:
+        ctx.evolve(1.0, 3)
+    assert e.value.status == 4
+    ctx.init_uniform()
+    for args in ((-1.0, 3), (float("nan"), 3), (1.0, 0)):
+        with pytest.raises(q.QaaError) as e:
+            ctx.evolve(*args)
+        assert e.value.status == 1
+    with pytest.raises(q.QaaError) as e:
+        ctx.evolve(1.0, 2, [0.5, 1.5])
+    assert e.value.status == 1
+    with pytest.raises(q.QaaError) as e:
+        ctx.energy(1.2)
+    assert e.value.status == 1
+    assert "outside" in q.qaa_last_error(ctx.ctx)
+
+
+def test_torch_owned_state(q, orc):
+    import torch
+    c = q.Context(0, n_max=14, torch_state=True)
+    cl = instance(14)
+    c.load_instance(14, cl)
+    c.init_uniform()
+    c.evolve(1.0, 4)
+    t = c.state_tensor()
+    torch.cuda.synchronize()
+    want = orc.evolve(14, orc.energy_table(14, cl), orc.init_uniform(14), 1.0, 4)
+    assert_close(t.cpu().numpy()[: 1 << 14], want)
+    c.close()
