@@ -30,8 +30,39 @@ struct PassArgs {
 
 constexpr size_t PASS_SMEM_BYTES = sizeof(double2) * TILE + sizeof(double2) * 256;
 
+// Generic (interpreted) pass: any register program, tangent or cot form per
+// slot. Used only when a pass needs the cot form (|tan beta| > 1e4) or an
+// uncommon program; the specialised kernels below handle the common passes.
 cudaError_t launch_pass(const PassArgs& a, int grid, cudaStream_t st);
 cudaError_t pass_kernel_setup();  // opt-in shared memory size
+
+// Specialised fused passes (pass_fast.cu): the register program is compiled
+// in, rotations are tangent form with a per-tile-bit coefficient (0 = the
+// bit is not rotated by this group, an exact identity), shared-memory
+// exchanges use the additive padded layout l + (l >> 4).
+enum FastProg : int {
+  FP_G0_DPOST = 0,       // group 0: D, then rotate all 12 tile bits      (first pass)
+  FP_G0_PRE = 1,         // group 0: rotate all 12 tile bits
+  FP_G0_PRE_D_POST = 2,  // group 0: rotate (step k), D_{k+1}, rotate (step k+1)
+  FP_GK_PRE = 3,         // group k>0: rotate tile bits 3..11
+  FP_GK_PRE_D_POST = 4,  // group k>0: rotate, D, rotate
+  FP_COUNT = 5
+};
+struct FastArgs {
+  double2* psi;
+  const uint8_t* E;
+  const double2* phi;
+  int n_phi;
+  double t[2][TILE_BITS];  // [slot][tile-local bit]: tan beta, or 0 if not rotated
+  int64_t ntiles;
+  int phys[TILE_BITS];
+  int nseg;
+  int seg_src[MAX_SEGS], seg_dst[MAX_SEGS], seg_len[MAX_SEGS];
+};
+constexpr int FAST_XBUF = TILE + TILE / 16;  // padded exchange buffer (amplitudes)
+constexpr size_t FAST_SMEM_BYTES = sizeof(double2) * (FAST_XBUF + 256);
+cudaError_t pass_fast_setup();
+cudaError_t launch_pass_fast(const FastArgs& a, int prog, bool lane3, bool prefetch, int grid, cudaStream_t st);
 
 // Whole-evolution kernel for L <= 12 local qubits: one CTA keeps the state in
 // shared memory for all K steps (SURVEY §7 hard part 5; latency-bound sizes).

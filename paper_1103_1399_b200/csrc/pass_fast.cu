@@ -1,0 +1,292 @@
+// pass_fast.cu -- specialised fused Trotter pass kernels (K4).
+//
+// One CTA (256 threads, 8 warps) owns a 2^12-amplitude tile at a time; each
+// thread holds 16 amplitudes in registers. A register "pattern" says which
+// tile-local bits are register bits (rotated in-thread), lane bits (rotated
+// with shuffles) and warp bits; between patterns the tile is transposed
+// through shared memory (plan.hpp). Each kernel below is one fixed program:
+//
+//   G0_DPOST         D | PA:r8-11 | ->PC r0-3 | ->PB r4-7 | store PB
+//   G0_PRE           PA:r8-11 | ->PC r0-3 | ->PB r4-7 | store PB
+//   G0_PRE_D_POST    PA | ->PC | ->PB (step k) | D_{k+1} | PB | ->PC | ->PA (step k+1) | store PA
+//   GK_PRE           PA:r8-11 | ->PB r4-7 + lane bit 3 | store PB
+//   GK_PRE_D_POST    PA | ->PB (+lane 3) | D | PB (+lane 3) | ->PA | store PA
+//
+// Rotations are exp(-i beta (1 - sigma^x)) = g cos(beta) (I + i t sigma^x),
+// t = tan(beta), with the scalar (g cos beta)^n folded into the step's Phi
+// table: one DFMA per real component. A tile bit the group
+// does not rotate gets t = 0 (exact identity).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace qaa {
+namespace {
+
+#define FULLM 0xffffffffu
+
+__device__ __forceinline__ constexpr int padA(int l) { return l + (l >> 4); }
+
+template <int P>
+__device__ __forceinline__ int pat_tl(int lane, int warp) {
+  if (P == PA) return lane | (warp << 5);
+  if (P == PB) return (lane & 15) | ((lane >> 4) << 8) | (warp << 9);
+  return (lane << 4) | (warp << 9);
+}
+template <int P>
+__device__ __forceinline__ constexpr int reg_shift() {
+  return P == PA ? 8 : (P == PB ? 4 : 0);
+}
+template <int P>
+__device__ __forceinline__ constexpr int lane_local(int i) {
+  return P == PA ? i : (P == PB ? (i < 4 ? i : 8) : 4 + i);
+}
+
+struct Off {
+  int64_t thr;
+  int64_t s[4];
+};
+
+template <int P>
+__device__ __forceinline__ Off make_off(const FastArgs& a, int lane, int warp) {
+  Off o;
+  const int tl = pat_tl<P>(lane, warp);
+  int64_t t = 0;
+#pragma unroll
+  for (int b = 0; b < TILE_BITS; b++)
+    if ((tl >> b) & 1) t += (int64_t)1 << a.phys[b];
+  o.thr = t;
+#pragma unroll
+  for (int i = 0; i < 4; i++) o.s[i] = (int64_t)1 << a.phys[reg_shift<P>() + i];
+  return o;
+}
+
+__device__ __forceinline__ int64_t roff(const Off& o, int r) {
+  int64_t x = o.thr;
+  if (r & 1) x += o.s[0];
+  if (r & 2) x += o.s[1];
+  if (r & 4) x += o.s[2];
+  if (r & 8) x += o.s[3];
+  return x;
+}
+
+__device__ __forceinline__ int64_t tbase(const FastArgs& a, int64_t T) {
+  int64_t b = 0;
+#pragma unroll
+  for (int s = 0; s < MAX_SEGS; s++)
+    if (s < a.nseg) b += ((T >> a.seg_src[s]) & (((int64_t)1 << a.seg_len[s]) - 1)) << a.seg_dst[s];
+  return b;
+}
+
+// (x, y) <- (x + i t y, y + i t x)
+__device__ __forceinline__ void rot2(double2& x, double2& y, double t) {
+  const double2 nx = make_double2(fma(-t, y.y, x.x), fma(t, y.x, x.y));
+  const double2 ny = make_double2(fma(-t, x.y, y.x), fma(t, x.x, y.y));
+  x = nx;
+  y = ny;
+}
+
+// rotate the 4 register bits of pattern P with per-local-bit coefficients t[slot][.]
+template <int P>
+__device__ __forceinline__ void rot_regs(double2 (&v)[RPT], const double (&t)[TILE_BITS]) {
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const double c = t[reg_shift<P>() + i];
+#pragma unroll
+    for (int r = 0; r < RPT; r++)
+      if (!(r & (1 << i))) rot2(v[r], v[r | (1 << i)], c);
+  }
+}
+
+__device__ __forceinline__ void rot_lane(double2 (&v)[RPT], int lanebit, double t) {
+#pragma unroll
+  for (int r = 0; r < RPT; r++) {
+    const double px = __shfl_xor_sync(FULLM, v[r].x, 1 << lanebit);
+    const double py = __shfl_xor_sync(FULLM, v[r].y, 1 << lanebit);
+    v[r] = make_double2(fma(-t, py, v[r].x), fma(t, px, v[r].y));
+  }
+}
+
+template <int FROM, int TO>
+__device__ __forceinline__ void xchg(double2* xb, double2 (&v)[RPT], int lane, int warp) {
+  const int bs = padA(pat_tl<FROM>(lane, warp));
+#pragma unroll
+  for (int r = 0; r < RPT; r++) xb[bs + padA(r << reg_shift<FROM>())] = v[r];
+  __syncthreads();
+  const int bl = padA(pat_tl<TO>(lane, warp));
+#pragma unroll
+  for (int r = 0; r < RPT; r++) v[r] = xb[bl + padA(r << reg_shift<TO>())];
+  __syncthreads();
+}
+
+__device__ __forceinline__ void diag(double2 (&v)[RPT], const uint32_t (&ep)[4], const double2* phis) {
+#pragma unroll
+  for (int r = 0; r < RPT; r++) {
+    const int e = (ep[r >> 2] >> ((r & 3) * 8)) & 0xff;
+    const double2 f = phis[e];
+    const double2 x = v[r];
+    v[r] = make_double2(fma(f.x, x.x, -f.y * x.y), fma(f.x, x.y, f.y * x.x));
+  }
+}
+
+template <int PROG>
+struct ProgInfo {
+  static constexpr bool has_d = PROG == FP_G0_DPOST || PROG == FP_G0_PRE_D_POST || PROG == FP_GK_PRE_D_POST;
+  static constexpr int e_pat = PROG == FP_G0_DPOST ? PA : PB;
+  static constexpr int store_pat = (PROG == FP_G0_PRE_D_POST || PROG == FP_GK_PRE_D_POST) ? PA : PB;
+};
+
+template <int PROG, bool LANE3>
+__device__ __forceinline__ void program(const FastArgs& a, double2 (&v)[RPT], const uint32_t (&ep)[4], double2* xb,
+                                        const double2* phis, int lane, int warp) {
+  const double(&t0)[TILE_BITS] = a.t[0];
+  const double(&t1)[TILE_BITS] = a.t[1];
+  if (PROG == FP_G0_DPOST) {
+    diag(v, ep, phis);
+    rot_regs<PA>(v, t1);
+    xchg<PA, PC>(xb, v, lane, warp);
+    rot_regs<PC>(v, t1);
+    xchg<PC, PB>(xb, v, lane, warp);
+    rot_regs<PB>(v, t1);
+  } else if (PROG == FP_G0_PRE) {
+    rot_regs<PA>(v, t0);
+    xchg<PA, PC>(xb, v, lane, warp);
+    rot_regs<PC>(v, t0);
+    xchg<PC, PB>(xb, v, lane, warp);
+    rot_regs<PB>(v, t0);
+  } else if (PROG == FP_G0_PRE_D_POST) {
+    rot_regs<PA>(v, t0);
+    xchg<PA, PC>(xb, v, lane, warp);
+    rot_regs<PC>(v, t0);
+    xchg<PC, PB>(xb, v, lane, warp);
+    rot_regs<PB>(v, t0);
+    diag(v, ep, phis);
+    rot_regs<PB>(v, t1);
+    xchg<PB, PC>(xb, v, lane, warp);
+    rot_regs<PC>(v, t1);
+    xchg<PC, PA>(xb, v, lane, warp);
+    rot_regs<PA>(v, t1);
+  } else if (PROG == FP_GK_PRE) {
+    rot_regs<PA>(v, t0);
+    xchg<PA, PB>(xb, v, lane, warp);
+    rot_regs<PB>(v, t0);
+    if (LANE3) rot_lane(v, 3, t0[3]);
+  } else if (PROG == FP_GK_PRE_D_POST) {
+    rot_regs<PA>(v, t0);
+    xchg<PA, PB>(xb, v, lane, warp);
+    rot_regs<PB>(v, t0);
+    if (LANE3) rot_lane(v, 3, t0[3]);
+    diag(v, ep, phis);
+    rot_regs<PB>(v, t1);
+    if (LANE3) rot_lane(v, 3, t1[3]);
+    xchg<PB, PA>(xb, v, lane, warp);
+    rot_regs<PA>(v, t1);
+  }
+}
+
+template <bool HAS_D>
+__device__ __forceinline__ void load(const FastArgs& a, const Off& pa, const Off& pe, int64_t T, double2 (&v)[RPT],
+                                     uint32_t (&ep)[4]) {
+  const int64_t base = tbase(a, T);
+  const double2* src = a.psi + base;
+#pragma unroll
+  for (int r = 0; r < RPT; r++) v[r] = src[roff(pa, r)];
+  if (HAS_D) {
+    const uint8_t* eb = a.E + base;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      uint32_t w = 0;
+#pragma unroll
+      for (int j = 0; j < 4; j++) w |= (uint32_t)eb[roff(pe, q * 4 + j)] << (8 * j);
+      ep[q] = w;
+    }
+  }
+}
+
+__device__ __forceinline__ void store(const FastArgs& a, const Off& ps, int64_t T, const double2 (&v)[RPT]) {
+  double2* dst = a.psi + tbase(a, T);
+#pragma unroll
+  for (int r = 0; r < RPT; r++) dst[roff(ps, r)] = v[r];
+}
+
+template <int PROG, bool LANE3, bool PREFETCH>
+__global__ void __launch_bounds__(NTHREADS, PREFETCH ? 1 : 2) qaa_pass_fast(const FastArgs a) {
+  extern __shared__ double2 smem[];
+  double2* xb = smem;
+  double2* phis = smem + FAST_XBUF;
+  using PI = ProgInfo<PROG>;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (PI::has_d)
+    for (int e = tid; e < a.n_phi; e += NTHREADS) phis[e] = a.phi[e];
+  __syncthreads();
+  const Off pa = make_off<PA>(a, lane, warp);
+  const Off pe = make_off<PI::e_pat>(a, lane, warp);
+  const Off ps = make_off<PI::store_pat>(a, lane, warp);
+  double2 va[RPT];
+  uint32_t ea[4] = {0, 0, 0, 0};
+  const int64_t stride = gridDim.x;
+  int64_t T = blockIdx.x;
+  if (!PREFETCH) {
+    for (; T < a.ntiles; T += stride) {
+      load<PI::has_d>(a, pa, pe, T, va, ea);
+      program<PROG, LANE3>(a, va, ea, xb, phis, lane, warp);
+      store(a, ps, T, va);
+    }
+    return;
+  }
+  double2 vb[RPT];
+  uint32_t eb[4] = {0, 0, 0, 0};
+  if (T < a.ntiles) load<PI::has_d>(a, pa, pe, T, va, ea);
+  while (T < a.ntiles) {
+    int64_t Tn = T + stride;
+    if (Tn < a.ntiles) load<PI::has_d>(a, pa, pe, Tn, vb, eb);
+    program<PROG, LANE3>(a, va, ea, xb, phis, lane, warp);
+    store(a, ps, T, va);
+    T = Tn;
+    if (T >= a.ntiles) break;
+    Tn = T + stride;
+    if (Tn < a.ntiles) load<PI::has_d>(a, pa, pe, Tn, va, ea);
+    program<PROG, LANE3>(a, vb, eb, xb, phis, lane, warp);
+    store(a, ps, T, vb);
+    T = Tn;
+  }
+}
+
+typedef void (*FastKernel)(const FastArgs);
+
+template <bool PF>
+FastKernel pick(int prog, bool lane3) {
+  switch (prog) {
+    case FP_G0_DPOST: return qaa_pass_fast<FP_G0_DPOST, false, PF>;
+    case FP_G0_PRE: return qaa_pass_fast<FP_G0_PRE, false, PF>;
+    case FP_G0_PRE_D_POST: return qaa_pass_fast<FP_G0_PRE_D_POST, false, PF>;
+    case FP_GK_PRE: return lane3 ? qaa_pass_fast<FP_GK_PRE, true, PF> : qaa_pass_fast<FP_GK_PRE, false, PF>;
+    case FP_GK_PRE_D_POST:
+      return lane3 ? qaa_pass_fast<FP_GK_PRE_D_POST, true, PF> : qaa_pass_fast<FP_GK_PRE_D_POST, false, PF>;
+    default: return nullptr;
+  }
+}
+
+}  // namespace
+
+cudaError_t pass_fast_setup() {
+  for (int p = 0; p < FP_COUNT; p++)
+    for (int l = 0; l < 2; l++)
+      for (int pf = 0; pf < 2; pf++) {
+        FastKernel k = pf ? pick<true>(p, l) : pick<false>(p, l);
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FAST_SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+      }
+  return cudaSuccess;
+}
+
+cudaError_t launch_pass_fast(const FastArgs& a, int prog, bool lane3, bool prefetch, int grid, cudaStream_t st) {
+  FastKernel k = prefetch ? pick<true>(prog, lane3) : pick<false>(prog, lane3);
+  if (!k) return cudaErrorInvalidValue;
+  k<<<grid, NTHREADS, FAST_SMEM_BYTES, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace qaa

@@ -170,6 +170,7 @@ qaa_status qaa_create(const qaa_config* cfg, qaa_ctx** out) {
   CUDA_TRY(cudaMalloc(&ctx->d_counters, 16));
   CUDA_TRY(cudaEventCreateWithFlags(&ctx->coef_done, cudaEventDisableTiming));
   CUDA_TRY(pass_kernel_setup());
+  CUDA_TRY(pass_fast_setup());
   return QAA_OK;
 }
 
@@ -381,7 +382,10 @@ static void build_step(double T, int64_t K, double s, int n, int n_phi, double2*
   const double beta = 0.5 * dt * (1.0 - s);  // X: exp(-i beta (1 - sigma^x)) per qubit
   const double cb = std::cos(beta), sb = std::sin(beta);
   double mag;
-  if (std::fabs(sb) <= std::fabs(cb)) {
+  // tangent form (I + i t sigma^x), t = tan beta, whenever |t| <= 1e4: it is a
+  // scaled unitary, so rounding stays relative to |psi| for any such t; only
+  // beta within ~1e-4 of pi/2 (mod pi) switches to the cot form.
+  if (std::fabs(sb) <= 1e4 * std::fabs(cb)) {
     sc->form = 0;
     sc->coef = sb / cb;  // tan beta
     mag = cb;
@@ -504,8 +508,52 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
   a.psi = ctx->state;
   a.E = ctx->E;
   a.n_phi = n_phi;
+  FastArgs fa;
+  memset(&fa, 0, sizeof fa);
+  fa.psi = ctx->state;
+  fa.E = ctx->E;
+  fa.n_phi = n_phi;
+  const bool prefetch = ctx->ctas_per_sm == 1;
+  const int fast_grid_cap = ctx->num_sms * (prefetch ? 1 : 2);
   for (const PassPlan& pp : plan) {
     const Group& gr = ctx->geom.groups[pp.group];
+    const bool pre = pp.pre_step >= 0, d = pp.d_step >= 0, post = pp.post_step >= 0;
+    int fp = -1;
+    if (pp.group == 0) {
+      if (!pre && d && post) fp = FP_G0_DPOST;
+      else if (pre && !d && !post) fp = FP_G0_PRE;
+      else if (pre && d && post) fp = FP_G0_PRE_D_POST;
+    } else if ((gr.rot_local & ~0xFF8u) == 0) {
+      if (pre && !d && !post) fp = FP_GK_PRE;
+      else if (pre && d && post) fp = FP_GK_PRE_D_POST;
+    }
+    if ((pre && sc[(size_t)pp.pre_step].form != 0) || (post && sc[(size_t)pp.post_step].form != 0)) fp = -1;
+    if (fp >= 0) {
+      fa.phi = d ? dphi + (size_t)pp.d_step * n_phi : nullptr;
+      for (int b = 0; b < TILE_BITS; b++) {
+        const bool rb = (gr.rot_local >> b) & 1;
+        fa.t[0][b] = (pre && rb) ? sc[(size_t)pp.pre_step].coef : 0.0;
+        fa.t[1][b] = (post && rb) ? sc[(size_t)pp.post_step].coef : 0.0;
+        fa.phys[b] = gr.phys[b];
+      }
+      fa.ntiles = gr.ntiles;
+      fa.nseg = gr.nseg;
+      for (int s = 0; s < gr.nseg; s++) {
+        fa.seg_src[s] = gr.seg_src[s];
+        fa.seg_dst[s] = gr.seg_dst[s];
+        fa.seg_len[s] = gr.seg_len[s];
+      }
+      const int grid = (int)std::min<int64_t>(gr.ntiles, fast_grid_cap);
+      if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
+      CUDA_TRY(launch_pass_fast(fa, fp, (gr.rot_local >> 3) & 1, prefetch, grid, ctx->stream));
+      if (ctx->profile) {
+        CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, ctx->stream));
+        ctx->ev_used++;
+      }
+      ctx->stats.pass_launches++;
+      ctx->stats.kernel_launches_total++;
+      continue;
+    }
     const Program* prog = get_program(ctx, pp.group, pp.pre_step >= 0, pp.d_step >= 0, pp.post_step >= 0);
     if (!prog) return fail(ctx, QAA_E_USAGE, "no register program for group %d", pp.group);
     a.phi = pp.d_step >= 0 ? dphi + (size_t)pp.d_step * n_phi : nullptr;
