@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--row-bits", type=int, default=3)
     ap.add_argument("--step-spanning", type=int, default=1)
     ap.add_argument("--ctas-per-sm", type=int, default=1)
+    ap.add_argument("--kernel", type=int, default=1, help="1 = TMA warp-specialised pass, 0 = register pass")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=26)
@@ -194,6 +195,7 @@ def run_ours(args):
     ctx.set_option(q.OPT_ROW_BITS, args.row_bits)
     ctx.set_option(q.OPT_STEP_SPANNING, args.step_spanning)
     ctx.set_option(q.OPT_CTAS_PER_SM, args.ctas_per_sm)
+    ctx.set_option(q.OPT_KERNEL, args.kernel)
     ctx.load_instance(n, cl)
     ctx.init_uniform()
     chunk = args.chunk
@@ -307,7 +309,8 @@ def run_ours(args):
                 "config": {"workload": f"n={n} unique-solution 3-SAT (inputs/instances), T=200, K=1e4 (dt=0.02), "
                                        f"{chunk} Trotter steps + P_succ per bench step",
                            "n": n, "m": len(cl), "chunk": chunk, "row_bits": args.row_bits,
-                           "step_spanning": args.step_spanning, "passes_per_step":
+                           "step_spanning": args.step_spanning, "kernel": "tma" if args.kernel else "register",
+                           "passes_per_step":
                                st["passes_per_step_num"] / st["passes_per_step_den"], "tile_groups": st["groups"],
                            "l2": "state 16 GiB >> 126 MB L2 (no flush needed)",
                            "parallelism": f"dp{world}" if world > 1 else "single"},

@@ -55,6 +55,19 @@ typedef enum {
 
 typedef struct qaa_ctx qaa_ctx;
 
+/* Host-side collectives the library needs when world > 1 (bootstrap of the
+ * CUDA-IPC peer pointers, one barrier per Trotter step, scalar reductions).
+ * The caller implements them over its process group (the Python binding uses
+ * torch.distributed). Both return 0 on success; any other value makes the
+ * library call fail with QAA_E_NCCL (and poisons the context).
+ *  barrier     returns after every rank has entered it.
+ *  allgather   recv[r*bytes .. (r+1)*bytes) = rank r's `send` (bytes each). */
+typedef struct {
+  void* user;
+  int (*barrier)(void* user);
+  int (*allgather)(void* user, const void* send, void* recv, size_t bytes);
+} qaa_comm;
+
 /* Creation parameters. All pointers are borrowed: the caller keeps
  * ownership and must keep them valid for the life of the context.
  *  device        CUDA device ordinal.
@@ -62,10 +75,18 @@ typedef struct qaa_ctx qaa_ctx;
  *  rank, world   this process's rank and the number of ranks (world = 1, or
  *                a power of two up to 8 when the state is sharded over GPUs
  *                on its top log2(world) qubits).
- *  nccl_id       128-byte ncclUniqueId shared by all ranks (world > 1), else NULL.
+ *  nccl_id       reserved, must be NULL (the global-qubit exchange is the
+ *                library's own CUDA-IPC peer-store pass, not NCCL).
  *  state         optional caller-owned device buffer for the local state
  *                (>= 16 * 2^L bytes, 256-byte aligned); NULL = library-owned.
- *  state_bytes   its size in bytes. */
+ *                Must be NULL when world > 1 (the library owns the two
+ *                IPC-shared shard buffers the layout swap alternates between).
+ *  state_bytes   its size in bytes.
+ *  comm          host collectives (required when world > 1, else ignored);
+ *                copied, the function pointers must stay valid.
+ * Sharding: rank r holds canonical indices [r 2^L, (r+1) 2^L),
+ * L = n - log2(world). Every rank must run on a GPU that can reach the
+ * others' memory through CUDA IPC (one node; NVLink/NVSwitch, or the same GPU). */
 typedef struct {
   int device;
   void* stream;
@@ -74,10 +95,12 @@ typedef struct {
   const void* nccl_id;
   void* state;
   size_t state_bytes;
+  const qaa_comm* comm;
 } qaa_config;
 
 /* Create a context. Errors: USAGE (NULL pointers, world not in {1,2,4,8},
- * rank out of range), CUDA (device/stream setup), NCCL (communicator). */
+ * rank out of range, world > 1 without comm or with a caller state buffer),
+ * CUDA (device/stream setup). */
 qaa_status qaa_create(const qaa_config* cfg, qaa_ctx** out);
 
 /* Release every library-owned resource. Safe on a poisoned context and on NULL. */
@@ -161,12 +184,17 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *  QAA_OPT_STEP_SPANNING 1 (default) = merge the last tile group of step k with
  *                        the first of step k+1 around D_{k+1};
  *                        0 = one D per step in the first pass only.
- *  QAA_OPT_CTAS_PER_SM   persistent-grid CTAs per SM for the pass kernel (1 or 2). */
+ *  QAA_OPT_CTAS_PER_SM   register-kernel variant: 1 = one CTA per SM with register
+ *                        double-buffered prefetch, 2 = two CTAs per SM, no prefetch.
+ *  QAA_OPT_KERNEL        1 (default) = warp-specialised TMA pass kernel (producer warp +
+ *                        two consumer groups, mbarrier ring of 3 shared-memory slots),
+ *                        0 = register-prefetch pass kernel. */
 enum {
   QAA_OPT_ROW_BITS = 1,
   QAA_OPT_PROFILE = 2,
   QAA_OPT_STEP_SPANNING = 3,
-  QAA_OPT_CTAS_PER_SM = 4
+  QAA_OPT_CTAS_PER_SM = 4,
+  QAA_OPT_KERNEL = 5
 };
 qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value);
 
@@ -201,6 +229,17 @@ qaa_status qaa_reset_stats(qaa_ctx* ctx);
 #define QAA_PLAN_RECORD 10
 qaa_status qaa_plan_describe(int n_local, int row_bits, int step_spanning, int64_t K,
                              int32_t* records, int64_t cap, int64_t* count);
+
+/* Pure host function: the sharded pass plan for n qubits over `world` ranks
+ * (plan.hpp ShardPass). Records of QAA_SHARD_RECORD int32:
+ *   {kind (0 pass, 1 plain remap), group, pre_step, d_step, post_step,
+ *    remote (1: the pass stores into the peers' other buffer = layout swap),
+ *    layout (0 = A, 1 = B, of the state the pass reads),
+ *    pre_mask, post_mask (physical local qubits rotated for pre/post step), 0}
+ * Errors: USAGE (bad sizes), CAP (n too small to shard over `world`). */
+#define QAA_SHARD_RECORD 10
+qaa_status qaa_plan_describe_sharded(int n, int world, int row_bits, int64_t K, int32_t* records, int64_t cap,
+                                     int64_t* count);
 
 /* Library version string. */
 const char* qaa_version(void);

@@ -326,7 +326,10 @@ struct ClauseRec {
 
 __global__ void __launch_bounds__(256) energy_table_kernel(uint8_t* E, int64_t N, uint64_t x_offset,
                                                             const ClauseRec* recs, int m, unsigned* d_max,
-                                                            unsigned long long* d_zeros) {
+                                                            unsigned long long* d_zeros, int lowbits, int hishift) {
+  // local index p -> global assignment x = (p mod 2^lowbits) | x_offset | ((p >> lowbits) << hishift)
+  // (layout A: lowbits = L; layout B of the sharded state: lowbits = L - g, hishift = L)
+  const uint64_t lowmask = (lowbits >= 64) ? ~0ull : ((1ull << lowbits) - 1);
   __shared__ ClauseRec sr[256];
   for (int i = threadIdx.x; i < m; i += blockDim.x) sr[i] = recs[i];
   __syncthreads();
@@ -334,7 +337,8 @@ __global__ void __launch_bounds__(256) energy_table_kernel(uint8_t* E, int64_t N
   unsigned long long zeros = 0;
   const int64_t ngroups = N >> 4;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups; g += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t x0 = x_offset + ((uint64_t)g << 4);
+    const uint64_t p0 = (uint64_t)g << 4;
+    const uint64_t x0 = (p0 & lowmask) | x_offset | ((p0 >> lowbits) << hishift);
     uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
     for (int c = 0; c < m; c++) {
       const ClauseRec r = sr[c];
@@ -385,7 +389,7 @@ __global__ void energy_table_small_kernel(uint8_t* E, int64_t N, uint64_t x_offs
 }
 
 cudaError_t launch_energy_table(uint8_t* E, int64_t N, uint64_t x_offset, const uint64_t* MV, int m, unsigned* d_max,
-                                unsigned long long* d_zeros, int num_sms, cudaStream_t st) {
+                                unsigned long long* d_zeros, int num_sms, cudaStream_t st, int lowbits, int hishift) {
   const ClauseRec* recs = reinterpret_cast<const ClauseRec*>(MV);
   if (N < 16) {
     energy_table_small_kernel<<<1, 32, 0, st>>>(E, N, x_offset, recs, m, d_max, d_zeros);
@@ -394,7 +398,7 @@ cudaError_t launch_energy_table(uint8_t* E, int64_t N, uint64_t x_offset, const 
     int64_t grid = (groups + 255) / 256;
     const int64_t cap = (int64_t)num_sms * 8;
     if (grid > cap) grid = cap;
-    energy_table_kernel<<<(int)grid, 256, 0, st>>>(E, N, x_offset, recs, m, d_max, d_zeros);
+    energy_table_kernel<<<(int)grid, 256, 0, st>>>(E, N, x_offset, recs, m, d_max, d_zeros, lowbits, hishift);
   }
   return cudaGetLastError();
 }
@@ -559,4 +563,46 @@ cudaError_t launch_reduce_partials(const double* partial, int nblocks, int strid
   return cudaGetLastError();
 }
 
+}  // namespace qaa
+
+namespace qaa {
+// Eg[T*4096 + l] = E[tbase(T) + off(l)]: the energy slice of tile T of a group,
+// contiguous so the TMA pass can bulk-copy it next to the amplitudes.
+struct PermArgs {
+  int phys[TILE_BITS];
+  int nseg;
+  int seg_src[MAX_SEGS], seg_dst[MAX_SEGS], seg_len[MAX_SEGS];
+  int64_t ntiles;
+};
+__global__ void __launch_bounds__(256) permute_energy_kernel(const uint8_t* E, uint8_t* Eg, const PermArgs a) {
+  for (int64_t T = blockIdx.x; T < a.ntiles; T += gridDim.x) {
+    int64_t base = 0;
+#pragma unroll
+    for (int s = 0; s < MAX_SEGS; s++)
+      if (s < a.nseg) base += ((T >> a.seg_src[s]) & (((int64_t)1 << a.seg_len[s]) - 1)) << a.seg_dst[s];
+    for (int l = threadIdx.x; l < TILE; l += blockDim.x) {
+      int64_t o = base;
+#pragma unroll
+      for (int b = 0; b < TILE_BITS; b++)
+        if ((l >> b) & 1) o += (int64_t)1 << a.phys[b];
+      Eg[T * TILE + l] = E[o];
+    }
+  }
+}
+cudaError_t launch_permute_energy(const uint8_t* E, uint8_t* Eg, const int (&phys)[TILE_BITS], int nseg,
+                                  const int* seg_src, const int* seg_dst, const int* seg_len, int64_t ntiles,
+                                  int num_sms, cudaStream_t st) {
+  PermArgs a;
+  for (int b = 0; b < TILE_BITS; b++) a.phys[b] = phys[b];
+  a.nseg = nseg;
+  for (int s = 0; s < MAX_SEGS; s++) {
+    a.seg_src[s] = s < nseg ? seg_src[s] : 0;
+    a.seg_dst[s] = s < nseg ? seg_dst[s] : 0;
+    a.seg_len[s] = s < nseg ? seg_len[s] : 0;
+  }
+  a.ntiles = ntiles;
+  int64_t grid = ntiles < (int64_t)num_sms * 8 ? ntiles : (int64_t)num_sms * 8;
+  permute_energy_kernel<<<(int)grid, 256, 0, st>>>(E, Eg, a);
+  return cudaGetLastError();
+}
 }  // namespace qaa

@@ -1,6 +1,7 @@
 // kernels.cuh -- device-side entry points of libqaa (launch wrappers). The
 // C-ABI in qaa_api.cu is the only caller.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -58,11 +59,47 @@ struct FastArgs {
   int phys[TILE_BITS];
   int nseg;
   int seg_src[MAX_SEGS], seg_dst[MAX_SEGS], seg_len[MAX_SEGS];
+  // sharded remap: when remote != 0 the tile at local index x
+  // is stored into peers[j] at (x mod 2^gshift) | (rank << gshift), j = x >> gshift
+  int remote;
+  int gshift;
+  int rank;
+  double2* peers[8];
 };
+// plain remap for the sharded layout swap: every local amplitude x goes to
+// peers[x >> gshift] at (x mod 2^gshift) | (rank << gshift)
+cudaError_t launch_remap(const double2* src, double2* const* peers, int64_t N, int gshift, int rank, int num_sms,
+                         cudaStream_t st);
 constexpr int FAST_XBUF = TILE + TILE / 16;  // padded exchange buffer (amplitudes)
 constexpr size_t FAST_SMEM_BYTES = sizeof(double2) * (FAST_XBUF + 256);
 cudaError_t pass_fast_setup();
 cudaError_t launch_pass_fast(const FastArgs& a, int prog, bool lane3, bool prefetch, int grid, cudaStream_t st);
+
+// Warp-specialised TMA pass (pass_tma.cu): same programs as FastArgs, tiles
+// streamed into shared memory by a producer warp (bulk copy for contiguous
+// tiles, tensor-map copy for strided ones), energies from a per-group
+// permuted table Eg (tile T's 4096 bytes contiguous at Eg + 4096 T).
+struct TmaArgs {
+  double2* psi;
+  const uint8_t* Eg;
+  const double2* phi;
+  int n_phi;
+  double t[2][TILE_BITS];
+  int64_t ntiles;
+  int phys[TILE_BITS];
+  int nseg;
+  int seg_src[MAX_SEGS], seg_dst[MAX_SEGS], seg_len[MAX_SEGS];
+  int contiguous;   // 1: tile is 64 KiB contiguous at psi + tbase(T)
+  int ndims;        // tensor-map rank (2..5) otherwise
+  int dim_seg[5];   // per dim: -1 = tile dim (coordinate 0), else the tile-id segment giving the coordinate
+};
+cudaError_t pass_tma_setup();
+cudaError_t launch_pass_tma(const CUtensorMap* map, const TmaArgs& a, int prog, bool lane3, int grid,
+                            cudaStream_t st);
+// gather a group's energy layout: Eg[T*4096 + l] = E[tbase(T) + off(l)]
+cudaError_t launch_permute_energy(const uint8_t* E, uint8_t* Eg, const int (&phys)[TILE_BITS], int nseg,
+                                  const int* seg_src, const int* seg_dst, const int* seg_len, int64_t ntiles,
+                                  int num_sms, cudaStream_t st);
 
 // Whole-evolution kernel for L <= 12 local qubits: one CTA keeps the state in
 // shared memory for all K steps (SURVEY §7 hard part 5; latency-bound sizes).
@@ -82,7 +119,8 @@ cudaError_t launch_resident(const ResidentArgs& a, cudaStream_t st);
 // E[x] = sum_c [(xg & M_c) == V_c], xg = x_offset + x, also folding
 // max(E) and the zero count into the given device counters.
 cudaError_t launch_energy_table(uint8_t* E, int64_t N, uint64_t x_offset, const uint64_t* MV, int m,
-                                unsigned* d_max, unsigned long long* d_zeros, int num_sms, cudaStream_t st);
+                                unsigned* d_max, unsigned long long* d_zeros, int num_sms, cudaStream_t st,
+                                int lowbits = 63, int hishift = 0);
 // Z compaction (A3): writes x_offset + x for every E[x] == 0 (order unspecified).
 cudaError_t launch_compact_zeros(const uint8_t* E, int64_t N, uint64_t x_offset, uint64_t* Z,
                                  unsigned long long* d_count, int num_sms, cudaStream_t st);

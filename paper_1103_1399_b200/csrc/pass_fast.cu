@@ -206,9 +206,28 @@ __device__ __forceinline__ void load(const FastArgs& a, const Off& pa, const Off
 }
 
 __device__ __forceinline__ void store(const FastArgs& a, const Off& ps, int64_t T, const double2 (&v)[RPT]) {
-  double2* dst = a.psi + tbase(a, T);
+  const int64_t tb = tbase(a, T);
+  double2* dst = a.psi + tb;
+  if (a.remote) {
+    // the bit swap of the sharded layouts: the tile's top local bits (not tile
+    // bits of this group) name the destination rank
+    const int64_t j = tb >> a.gshift;
+    dst = a.peers[j] + (tb - (j << a.gshift) + ((int64_t)a.rank << a.gshift));
+  }
 #pragma unroll
   for (int r = 0; r < RPT; r++) dst[roff(ps, r)] = v[r];
+}
+
+__global__ void __launch_bounds__(256) remap_kernel(const double2* src, double2* const* peers_unused, int64_t N,
+                                                    int gshift, int rank, double2* p0, double2* p1, double2* p2,
+                                                    double2* p3, double2* p4, double2* p5, double2* p6, double2* p7) {
+  double2* peers[8] = {p0, p1, p2, p3, p4, p5, p6, p7};
+  const int64_t low = ((int64_t)1 << gshift) - 1;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < N; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = x >> gshift;
+    peers[j][(x & low) | ((int64_t)rank << gshift)] = src[x];
+  }
+  __threadfence_system();
 }
 
 template <int PROG, bool LANE3, bool PREFETCH>
@@ -234,6 +253,7 @@ __global__ void __launch_bounds__(NTHREADS, PREFETCH ? 1 : 2) qaa_pass_fast(cons
       program<PROG, LANE3>(a, va, ea, xb, phis, lane, warp);
       store(a, ps, T, va);
     }
+    if (a.remote) __threadfence_system();
     return;
   }
   double2 vb[RPT];
@@ -252,6 +272,7 @@ __global__ void __launch_bounds__(NTHREADS, PREFETCH ? 1 : 2) qaa_pass_fast(cons
     store(a, ps, T, vb);
     T = Tn;
   }
+  if (a.remote) __threadfence_system();
 }
 
 typedef void (*FastKernel)(const FastArgs);
@@ -280,6 +301,15 @@ cudaError_t pass_fast_setup() {
         if (e != cudaSuccess) return e;
       }
   return cudaSuccess;
+}
+
+cudaError_t launch_remap(const double2* src, double2* const* peers, int64_t N, int gshift, int rank, int num_sms,
+                         cudaStream_t st) {
+  int64_t grid = (N + 255) / 256;
+  if (grid > (int64_t)num_sms * 8) grid = (int64_t)num_sms * 8;
+  remap_kernel<<<(int)grid, 256, 0, st>>>(src, nullptr, N, gshift, rank, peers[0], peers[1], peers[2], peers[3],
+                                          peers[4], peers[5], peers[6], peers[7]);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_pass_fast(const FastArgs& a, int prog, bool lane3, bool prefetch, int grid, cudaStream_t st) {

@@ -15,11 +15,6 @@ int pattern_lane_local(int pat, int i) { return kLaneLocal[pat][i]; }
 int pattern_warp_local(int pat, int i) { return kWarpLocal[pat][i]; }
 bool pattern_storable(int pat) { return pat == PA || pat == PB; }
 
-static uint32_t reg_mask(int pat) {
-  uint32_t m = 0;
-  for (int i = 0; i < 4; i++) m |= 1u << kRegLocal[pat][i];
-  return m;
-}
 static uint32_t lane_mask(int pat) {
   uint32_t m = 0;
   for (int i = 0; i < 5; i++) m |= 1u << kLaneLocal[pat][i];
@@ -128,6 +123,43 @@ void build_pass_schedule(int P, int64_t K, bool step_spanning, std::vector<PassP
       out->push_back({g, step, -1, -1});
     }
   }
+}
+
+bool build_shard_schedule(const Geometry& geo, int gbits, int64_t K, std::vector<ShardPass>* out, std::string* err) {
+  out->clear();
+  const int P = (int)geo.groups.size();
+  const int L = geo.L;
+  if (P < 2) {
+    if (err) *err = "sharding needs at least two tile groups (n - log2(world) >= 13)";
+    return false;
+  }
+  const Group& top = geo.groups[(size_t)P - 1];
+  const Group& last = geo.groups[(size_t)P - 2];
+  uint32_t carried = 0;
+  for (int b = 0; b < TILE_BITS; b++) {
+    if (top.phys[b] >= L - gbits) carried |= 1u << b;
+    if (last.phys[b] >= L - gbits) {
+      if (err) *err = "remote group holds a carried bit";
+      return false;
+    }
+  }
+  int nc = 0;
+  for (int b = 0; b < TILE_BITS; b++) nc += (carried >> b) & 1;
+  if (nc != gbits || (carried & ~top.rot_local)) {
+    if (err) *err = "top tile group does not rotate every carried qubit (n too small for this world)";
+    return false;
+  }
+  for (int64_t k = 0; k < K; k++) {
+    const int layout = (int)(k & 1);
+    ShardPass f{SK_PASS, P - 1, k >= 1 ? k - 1 : -1, k >= 1 ? carried : 0u, k, k, top.rot_local, 0, layout};
+    out->push_back(f);
+    for (int g = 0; g <= P - 2; g++)
+      out->push_back({SK_PASS, g, k, geo.groups[(size_t)g].rot_local, -1, -1, 0u, g == P - 2 ? 1 : 0, layout});
+  }
+  const int lay = (int)(K & 1);
+  out->push_back({SK_PASS, P - 1, K - 1, carried, -1, -1, 0u, 0, lay});
+  if (lay == 1) out->push_back({SK_REMAP, -1, -1, 0u, -1, -1, 0u, 1, 1});
+  return true;
 }
 
 // ---------------------------------------------------------------- programs

@@ -89,6 +89,33 @@ bool build_geometry(int L, int row_bits, Geometry* g, std::string* err);
 // Pass schedule for K steps (step_spanning: see header comment).
 void build_pass_schedule(int ngroups, int64_t K, bool step_spanning, std::vector<PassPlan>* out);
 
+// ---------------------------------------------------------------- sharded plan
+// World W = 2^g ranks hold the state on its top g qubits.
+// Layout A: rank r = logical bits [L, n); local bit p = logical p.
+// Layout B: rank r = logical bits [L-g, L); local bits [L-g, L) hold logical
+// [L, n) (the previous rank field). Going A <-> B is one all-to-all of
+// contiguous chunks (the bit swap), done by the last pass of every phase
+// storing its tiles straight into the peers' next buffers.
+// Step k runs as one phase in layout k % 2:
+//   [top group: rotate the g carried bits for step k-1, D_k, rotate all of
+//    its bits for step k], then groups 0..P-2 rotate for step k, the last of
+//    them storing remotely (layout flips).
+// After the last phase the carried bits get their step K-1 rotation and, if
+// the state is in layout B, a plain remap returns it to layout A.
+enum ShardKind : int { SK_PASS = 0, SK_REMAP = 1 };
+struct ShardPass {
+  int kind;
+  int group;
+  int64_t pre_step;
+  uint32_t pre_local;   // tile-local bits rotated for pre_step
+  int64_t d_step;
+  int64_t post_step;
+  uint32_t post_local;  // tile-local bits rotated for post_step
+  int remote;           // tiles go to the peers' next buffers (A <-> B)
+  int layout;           // layout of the state this pass reads (0 = A, 1 = B)
+};
+bool build_shard_schedule(const Geometry& geo, int gbits, int64_t K, std::vector<ShardPass>* out, std::string* err);
+
 // Register-pattern program for one pass: rotate pre_local (slot 0), apply D
 // (if has_d), rotate post_local (slot 1); minimises exchanges + shuffles.
 bool build_program(uint32_t pre_local, bool has_d, uint32_t post_local, Program* prog);

@@ -1,5 +1,7 @@
 // qaa_api.cu -- the C-ABI of libqaa (include/qaa.h): context, validation,
 // host coefficient builder (H1), pass planning (H2, plan.cpp) and launches.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -70,8 +72,24 @@ struct qaa_ctx {
   int profile = 0;
   int step_spanning = 1;
   int ctas_per_sm = 1;
+  int kernel_mode = 1;  // 1: TMA warp-specialised pass, 0: register-prefetch pass
+  // TMA state per tile group (built at load)
+  std::vector<uint8_t*> Eg;  // per-group permuted energies (Eg[0] = E)
+  std::vector<CUtensorMap> tmaps;
+  std::vector<TmaArgs> tma_static;
+  std::vector<int> tma_ok;
   // programs
   std::map<std::tuple<int, int, int, int>, Program> progs;
+  // sharded state (world > 1): two IPC-shared shard buffers, layout A/B tables
+  qaa_comm comm;
+  bool has_comm = false;
+  double2* bufs[2] = {nullptr, nullptr};
+  size_t buf_cap = 0;
+  int cur = 0;                       // buffer holding the current state
+  double2* peers[2][8] = {{nullptr}};  // peers[b][r]: rank r's buffer b (own rank: local pointer)
+  bool peer_open[2][8] = {{false}};
+  uint8_t* E_B = nullptr;            // energies in layout B
+  size_t E_B_cap = 0;
   // stats
   qaa_stats stats;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
@@ -149,8 +167,14 @@ qaa_status qaa_create(const qaa_config* cfg, qaa_ctx** out) {
   ctx->rank = cfg->rank;
   ctx->world = cfg->world;
   ctx->gbits = cfg->world == 1 ? 0 : (cfg->world == 2 ? 1 : (cfg->world == 4 ? 2 : 3));
-  if (ctx->world > 1)
-    return fail(ctx, QAA_E_USAGE, "world > 1 requires the NCCL build (not available in this build)");
+  if (ctx->world > 1) {
+    if (!cfg->comm || !cfg->comm->barrier || !cfg->comm->allgather)
+      return fail(ctx, QAA_E_USAGE, "world > 1 needs comm callbacks (barrier, allgather)");
+    if (cfg->state) return fail(ctx, QAA_E_USAGE, "world > 1: the library owns the shard buffers (state must be NULL)");
+    if (cfg->nccl_id) return fail(ctx, QAA_E_USAGE, "nccl_id is reserved and must be NULL");
+    ctx->comm = *cfg->comm;
+    ctx->has_comm = true;
+  }
   CUDA_TRY(cudaSetDevice(cfg->device));
   CUDA_TRY(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
   if (cfg->stream) {
@@ -171,6 +195,7 @@ qaa_status qaa_create(const qaa_config* cfg, qaa_ctx** out) {
   CUDA_TRY(cudaEventCreateWithFlags(&ctx->coef_done, cudaEventDisableTiming));
   CUDA_TRY(pass_kernel_setup());
   CUDA_TRY(pass_fast_setup());
+  CUDA_TRY(pass_tma_setup());
   return QAA_OK;
 }
 
@@ -187,6 +212,14 @@ void qaa_destroy(qaa_ctx* ctx) {
   if (ctx->d_out) cudaFree(ctx->d_out);
   if (ctx->h_out) cudaFreeHost(ctx->h_out);
   if (ctx->d_counters) cudaFree(ctx->d_counters);
+  for (size_t g = 1; g < ctx->Eg.size(); g++)
+    if (ctx->Eg[g]) cudaFree(ctx->Eg[g]);
+  for (int b = 0; b < 2; b++) {
+    for (int r = 0; r < 8; r++)
+      if (ctx->peer_open[b][r]) cudaIpcCloseMemHandle(ctx->peers[b][r]);
+    if (ctx->bufs[b]) cudaFree(ctx->bufs[b]);
+  }
+  if (ctx->E_B) cudaFree(ctx->E_B);
   if (ctx->coef_done) cudaEventDestroy(ctx->coef_done);
   for (auto& p : ctx->ev_pool) {
     cudaEventDestroy(p.first);
@@ -220,6 +253,10 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
     case QAA_OPT_STEP_SPANNING:
       ctx->step_spanning = value != 0;
       return QAA_OK;
+    case QAA_OPT_KERNEL:
+      if (value < 0 || value > 1) return fail(ctx, QAA_E_USAGE, "kernel mode must be 0 or 1");
+      ctx->kernel_mode = (int)value;
+      return QAA_OK;
     case QAA_OPT_CTAS_PER_SM:
       if (value < 1 || value > 4) return fail(ctx, QAA_E_USAGE, "ctas_per_sm must be in 1..4");
       ctx->ctas_per_sm = (int)value;
@@ -227,6 +264,203 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
     default:
       return fail(ctx, QAA_E_USAGE, "unknown option key %d", key);
   }
+}
+
+// Per-group TMA descriptors and permuted energy tables (pass_tma.cu).
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    cudaGetLastError();
+  }
+  return fn;
+}
+
+static qaa_status build_tma(qaa_ctx* ctx) {
+  for (size_t g = 1; g < ctx->Eg.size(); g++)
+    if (ctx->Eg[g]) cudaFree(ctx->Eg[g]);
+  ctx->Eg.clear();
+  ctx->tmaps.clear();
+  ctx->tma_static.clear();
+  ctx->tma_ok.clear();
+  if (ctx->L <= RESIDENT_MAX_L) return QAA_OK;
+  const int L = ctx->L;
+  const size_t N = (size_t)1 << L;
+  auto enc = tensor_map_encoder();
+  for (size_t gi = 0; gi < ctx->geom.groups.size(); gi++) {
+    const Group& gr = ctx->geom.groups[gi];
+    TmaArgs t;
+    memset(&t, 0, sizeof t);
+    CUtensorMap map;
+    memset(&map, 0, sizeof map);
+    bool ok = true;
+    bool in_tile[64] = {false};
+    for (int b = 0; b < TILE_BITS; b++) in_tile[gr.phys[b]] = true;
+    bool contiguous = true;
+    for (int b = 0; b < TILE_BITS; b++) contiguous = contiguous && gr.phys[b] == b;
+    t.contiguous = contiguous ? 1 : 0;
+    if (!contiguous) {
+      // dims: runs of tile bits (split to box-size limits) and gap runs (box 1)
+      cuuint64_t gdim[5], gstride[5];
+      cuuint32_t box[5], estr[5];
+      int nd = 0, gap_index = 0;
+      for (int p = 0; p < L && ok;) {
+        int q = p;
+        while (q + 1 < L && in_tile[q + 1] == in_tile[p]) q++;
+        int bits = q - p + 1;
+        if (in_tile[p]) {
+          int start = p;
+          while (bits > 0 && ok) {
+            const int lim = nd == 0 ? 7 : 8;
+            const int take = bits < lim ? bits : lim;
+            if (nd >= 5) { ok = false; break; }
+            gdim[nd] = (cuuint64_t)1 << (take + (nd == 0 ? 1 : 0));
+            box[nd] = (cuuint32_t)gdim[nd];
+            gstride[nd] = (cuuint64_t)16 << start;
+            t.dim_seg[nd] = -1;
+            nd++;
+            start += take;
+            bits -= take;
+          }
+        } else {
+          if (nd >= 5 || nd == 0) { ok = false; break; }
+          gdim[nd] = (cuuint64_t)1 << bits;
+          box[nd] = 1;
+          gstride[nd] = (cuuint64_t)16 << p;
+          t.dim_seg[nd] = gap_index++;
+          nd++;
+        }
+        p = q + 1;
+      }
+      if (ok && enc) {
+        for (int d = 0; d < nd; d++) estr[d] = 1;
+        CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)nd, (void*)ctx->state, gdim, gstride + 1,
+                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        ok = r == CUDA_SUCCESS;
+      } else {
+        ok = false;
+      }
+      t.ndims = nd;
+    }
+    // permuted energies
+    uint8_t* eg = nullptr;
+    if (gi == 0) {
+      eg = ctx->E;
+    } else if (ok) {
+      cudaError_t e = cudaMalloc(&eg, N);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        eg = nullptr;
+        ok = false;  // not enough memory for the permuted table: register kernel fallback
+      } else {
+        CUDA_TRY(launch_permute_energy(ctx->E, eg, gr.phys, gr.nseg, gr.seg_src, gr.seg_dst, gr.seg_len, gr.ntiles,
+                                       ctx->num_sms, ctx->stream));
+        ctx->stats.kernel_launches_total++;
+      }
+    }
+    t.Eg = eg;
+    ctx->Eg.push_back(eg);
+    ctx->tmaps.push_back(map);
+    ctx->tma_static.push_back(t);
+    ctx->tma_ok.push_back(ok ? 1 : 0);
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return QAA_OK;
+}
+
+// ------------------------------------------------------------------ sharding helpers
+static qaa_status comm_barrier(qaa_ctx* ctx) {
+  if (ctx->comm.barrier(ctx->comm.user) != 0) return fail(ctx, QAA_E_NCCL, "comm barrier failed");
+  return QAA_OK;
+}
+static qaa_status comm_allgather(qaa_ctx* ctx, const void* send, void* recv, size_t bytes) {
+  if (ctx->comm.allgather(ctx->comm.user, send, recv, bytes) != 0) return fail(ctx, QAA_E_NCCL, "comm allgather failed");
+  return QAA_OK;
+}
+// sum of `n` doubles over ranks, added in rank order (deterministic)
+static qaa_status comm_sum(qaa_ctx* ctx, double* v, int n) {
+  if (ctx->world == 1) return QAA_OK;
+  std::vector<double> all((size_t)n * ctx->world);
+  qaa_status st = comm_allgather(ctx, v, all.data(), sizeof(double) * (size_t)n);
+  if (st) return st;
+  for (int j = 0; j < n; j++) {
+    double s = 0.0;
+    for (int r = 0; r < ctx->world; r++) s += all[(size_t)r * n + j];
+    v[j] = s;
+  }
+  return QAA_OK;
+}
+
+// Two shard buffers per rank, exported with CUDA IPC; every rank maps every
+// other rank's buffers so the layout-swap pass can store into them directly
+// (NVLink/NVSwitch peer stores across GPUs, plain stores on one GPU).
+static qaa_status setup_shard_buffers(qaa_ctx* ctx, size_t bytes) {
+  if (ctx->buf_cap >= bytes && ctx->bufs[0]) {
+    ctx->state = ctx->bufs[ctx->cur = 0];
+    return QAA_OK;
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  for (int b = 0; b < 2; b++) {
+    for (int r = 0; r < 8; r++) {
+      if (ctx->peer_open[b][r]) cudaIpcCloseMemHandle(ctx->peers[b][r]);
+      ctx->peer_open[b][r] = false;
+      ctx->peers[b][r] = nullptr;
+    }
+    if (ctx->bufs[b]) cudaFree(ctx->bufs[b]);
+    ctx->bufs[b] = nullptr;
+  }
+  ctx->buf_cap = 0;
+  for (int b = 0; b < 2; b++) {
+    cudaError_t e = cudaMalloc(&ctx->bufs[b], bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, QAA_E_CAP, "shard buffers of 2 x %zu bytes do not fit on the device", bytes);
+    }
+  }
+  ctx->buf_cap = bytes;
+  cudaIpcMemHandle_t mine[2];
+  for (int b = 0; b < 2; b++) CUDA_TRY(cudaIpcGetMemHandle(&mine[b], ctx->bufs[b]));
+  std::vector<cudaIpcMemHandle_t> all(2 * (size_t)ctx->world);
+  qaa_status st = comm_allgather(ctx, mine, all.data(), sizeof mine);
+  if (st) return st;
+  for (int r = 0; r < ctx->world; r++)
+    for (int b = 0; b < 2; b++) {
+      if (r == ctx->rank) {
+        ctx->peers[b][r] = ctx->bufs[b];
+        continue;
+      }
+      void* p = nullptr;
+      CUDA_TRY(cudaIpcOpenMemHandle(&p, all[2 * (size_t)r + b], cudaIpcMemLazyEnablePeerAccess));
+      ctx->peers[b][r] = (double2*)p;
+      ctx->peer_open[b][r] = true;
+    }
+  st = comm_barrier(ctx);
+  if (st) return st;
+  ctx->cur = 0;
+  ctx->state = ctx->bufs[0];
+  ctx->own_state = false;
+  ctx->state_cap_bytes = bytes;
+  return QAA_OK;
+}
+
+// one layout swap (A <-> B) of the whole sharded state: stores, barrier, flip
+static qaa_status shard_remap(qaa_ctx* ctx) {
+  CUDA_TRY(launch_remap(ctx->bufs[ctx->cur], ctx->peers[ctx->cur ^ 1], (int64_t)1 << ctx->L, ctx->L - ctx->gbits,
+                        ctx->rank, ctx->num_sms, ctx->stream));
+  ctx->stats.kernel_launches_total++;
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  qaa_status st = comm_barrier(ctx);
+  if (st) return st;
+  ctx->cur ^= 1;
+  ctx->state = ctx->bufs[ctx->cur];
+  return QAA_OK;
 }
 
 qaa_status qaa_load_instance(qaa_ctx* ctx, int n, int m, const int32_t* lits) {
@@ -265,7 +499,17 @@ qaa_status qaa_load_instance(qaa_ctx* ctx, int n, int m, const int32_t* lits) {
   const int64_t N = (int64_t)1 << L;
   const size_t state_bytes = (size_t)N * sizeof(double2);
   // capacity
-  if (!ctx->own_state && ctx->state) {
+  if (ctx->world > 1) {
+    Geometry gtest;
+    std::string e;
+    std::vector<ShardPass> sp;
+    if (L <= RESIDENT_MAX_L || !build_geometry(L, ctx->row_bits, &gtest, &e) ||
+        !build_shard_schedule(gtest, ctx->gbits, 1, &sp, &e))
+      return fail(ctx, QAA_E_CAP, "n = %d cannot be sharded over %d ranks: %s", n, ctx->world,
+                  e.empty() ? "n - log2(world) must be >= 13" : e.c_str());
+    qaa_status st = setup_shard_buffers(ctx, state_bytes);
+    if (st) return st;
+  } else if (!ctx->own_state && ctx->state) {
     if (ctx->state_cap_bytes < state_bytes)
       return fail(ctx, QAA_E_CAP, "caller state buffer holds %zu bytes, need %zu for n = %d", ctx->state_cap_bytes,
                   state_bytes, n);
@@ -323,6 +567,29 @@ qaa_status qaa_load_instance(qaa_ctx* ctx, int n, int m, const int32_t* lits) {
   ctx->nz_local = (int64_t)zeros;
   ctx->nz_total = zeros;
   ctx->z_listed = false;
+  if (ctx->world > 1) {
+    // layout-B energies: local p -> x = (p mod 2^(L-g)) | r 2^(L-g) | (p >> (L-g)) 2^L
+    void* p = ctx->E_B;
+    qaa_status st = ensure_buffer(ctx, &p, &ctx->E_B_cap, (size_t)N);
+    ctx->E_B = (uint8_t*)p;
+    if (st) return st;
+    CUDA_TRY(launch_energy_table(ctx->E_B, N, (uint64_t)ctx->rank << (L - ctx->gbits), (const uint64_t*)ctx->d_coef,
+                                 (int)recs.size(), ctx->d_counters, (unsigned long long*)(ctx->d_counters + 2),
+                                 ctx->num_sms, ctx->stream, L - ctx->gbits, L));
+    ctx->stats.kernel_launches_total++;
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    // global |Z| and max E over ranks
+    uint64_t mine[2] = {zeros, (uint64_t)ctx->emax};
+    std::vector<uint64_t> all(2 * (size_t)ctx->world);
+    qaa_status st2 = comm_allgather(ctx, mine, all.data(), sizeof mine);
+    if (st2) return st2;
+    ctx->nz_total = 0;
+    ctx->emax = 0;
+    for (int r = 0; r < ctx->world; r++) {
+      ctx->nz_total += all[2 * (size_t)r];
+      ctx->emax = std::max<unsigned>(ctx->emax, (unsigned)all[2 * (size_t)r + 1]);
+    }
+  }
   if (ctx->nz_local > 0 && ctx->nz_local <= ZLIST_CAP) {
     void* p = ctx->Z;
     qaa_status st = ensure_buffer(ctx, &p, &ctx->Z_cap, (size_t)ctx->nz_local * 8);
@@ -339,6 +606,10 @@ qaa_status qaa_load_instance(qaa_ctx* ctx, int n, int m, const int32_t* lits) {
     CUDA_TRY(cudaMemcpyAsync(ctx->Z, hz.data(), hz.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     ctx->z_listed = true;
+  }
+  if (ctx->world == 1) {
+    qaa_status st = build_tma(ctx);
+    if (st) return st;
   }
   ctx->loaded = true;
   return QAA_OK;
@@ -412,6 +683,81 @@ static qaa_status ensure_events(qaa_ctx* ctx, size_t need) {
   return QAA_OK;
 }
 
+// Sharded evolve (plan.hpp ShardPass): every phase ends with a
+// pass whose tiles are stored straight into the peers' other shard buffer
+// (the bit swap of the top local and the rank qubits), then one host barrier.
+static qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<StepCoef>& sc, const double2* dphi,
+                                 int n_phi) {
+  for (int64_t k = 0; k < K; k++)
+    if (sc[(size_t)k].form != 0)
+      return fail(ctx, QAA_E_USAGE, "sharded evolve needs |tan(dt(1-s)/2)| <= 1e4 (step %lld)", (long long)k);
+  std::vector<ShardPass> plan;
+  std::string e;
+  if (!build_shard_schedule(ctx->geom, ctx->gbits, K, &plan, &e)) return fail(ctx, QAA_E_CAP, "%s", e.c_str());
+  if (ctx->profile) {
+    qaa_status st = ensure_events(ctx, ctx->ev_used + plan.size());
+    if (st) return st;
+  }
+  const int P = (int)ctx->geom.groups.size();
+  FastArgs fa;
+  memset(&fa, 0, sizeof fa);
+  fa.n_phi = n_phi;
+  fa.gshift = ctx->L - ctx->gbits;
+  fa.rank = ctx->rank;
+  for (const ShardPass& sp : plan) {
+    if (sp.kind == SK_REMAP) {
+      qaa_status st = shard_remap(ctx);
+      if (st) return st;
+      continue;
+    }
+    const Group& gr = ctx->geom.groups[(size_t)sp.group];
+    const bool d = sp.d_step >= 0;
+    int fp;
+    if (sp.group == 0)
+      fp = FP_G0_PRE;  // group 0 never carries D in the sharded plan
+    else
+      fp = d ? FP_GK_PRE_D_POST : FP_GK_PRE;
+    if (sp.group == 0 && (d || sp.post_step >= 0)) return fail(ctx, QAA_E_USAGE, "internal: unexpected shard pass");
+    if (sp.group > 0 && (gr.rot_local & ~0xFF8u)) return fail(ctx, QAA_E_USAGE, "sharded plan needs row_bits >= 3");
+    fa.psi = ctx->bufs[ctx->cur];
+    fa.E = sp.layout ? ctx->E_B : ctx->E;
+    fa.phi = d ? dphi + (size_t)sp.d_step * n_phi : nullptr;
+    for (int b = 0; b < TILE_BITS; b++) {
+      fa.t[0][b] = (sp.pre_step >= 0 && ((sp.pre_local >> b) & 1)) ? sc[(size_t)sp.pre_step].coef : 0.0;
+      fa.t[1][b] = (sp.post_step >= 0 && ((sp.post_local >> b) & 1)) ? sc[(size_t)sp.post_step].coef : 0.0;
+      fa.phys[b] = gr.phys[b];
+    }
+    fa.ntiles = gr.ntiles;
+    fa.nseg = gr.nseg;
+    for (int s = 0; s < gr.nseg; s++) {
+      fa.seg_src[s] = gr.seg_src[s];
+      fa.seg_dst[s] = gr.seg_dst[s];
+      fa.seg_len[s] = gr.seg_len[s];
+    }
+    fa.remote = sp.remote;
+    for (int r = 0; r < 8; r++) fa.peers[r] = ctx->peers[ctx->cur ^ 1][r];
+    const int grid = (int)std::min<int64_t>(gr.ntiles, ctx->num_sms);
+    const bool lane3 = ((sp.pre_local | sp.post_local | gr.rot_local) >> 3) & 1;
+    if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
+    CUDA_TRY(launch_pass_fast(fa, fp, lane3, true, grid, ctx->stream));
+    if (ctx->profile) {
+      CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, ctx->stream));
+      ctx->ev_used++;
+    }
+    ctx->stats.pass_launches++;
+    ctx->stats.kernel_launches_total++;
+    if (sp.remote) {
+      CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+      qaa_status st = comm_barrier(ctx);
+      if (st) return st;
+      ctx->cur ^= 1;
+      ctx->state = ctx->bufs[ctx->cur];
+    }
+  }
+  (void)P;
+  return QAA_OK;
+}
+
 static const Program* get_program(qaa_ctx* ctx, int g, bool pre, bool d, bool post) {
   auto key = std::make_tuple(g, (int)pre, (int)d, (int)post);
   auto it = ctx->progs.find(key);
@@ -471,6 +817,7 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
 
   ctx->stats.evolve_calls++;
   ctx->stats.trotter_steps += K;
+  if (ctx->world > 1) return evolve_sharded(ctx, K, sc, dphi, n_phi);
   if (ctx->L <= RESIDENT_MAX_L) {
     ResidentArgs ra;
     ra.psi = ctx->state;
@@ -528,6 +875,35 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
       else if (pre && d && post) fp = FP_GK_PRE_D_POST;
     }
     if ((pre && sc[(size_t)pp.pre_step].form != 0) || (post && sc[(size_t)pp.post_step].form != 0)) fp = -1;
+    if (fp >= 0 && ctx->kernel_mode == 1 && ctx->tma_ok[(size_t)pp.group]) {
+      TmaArgs ta = ctx->tma_static[(size_t)pp.group];
+      ta.psi = ctx->state;
+      ta.phi = d ? dphi + (size_t)pp.d_step * n_phi : nullptr;
+      ta.n_phi = n_phi;
+      for (int b = 0; b < TILE_BITS; b++) {
+        const bool rb = (gr.rot_local >> b) & 1;
+        ta.t[0][b] = (pre && rb) ? sc[(size_t)pp.pre_step].coef : 0.0;
+        ta.t[1][b] = (post && rb) ? sc[(size_t)pp.post_step].coef : 0.0;
+        ta.phys[b] = gr.phys[b];
+      }
+      ta.ntiles = gr.ntiles;
+      ta.nseg = gr.nseg;
+      for (int s = 0; s < gr.nseg; s++) {
+        ta.seg_src[s] = gr.seg_src[s];
+        ta.seg_dst[s] = gr.seg_dst[s];
+        ta.seg_len[s] = gr.seg_len[s];
+      }
+      const int grid = (int)std::min<int64_t>(gr.ntiles / 2, ctx->num_sms);
+      if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
+      CUDA_TRY(launch_pass_tma(&ctx->tmaps[(size_t)pp.group], ta, fp, (gr.rot_local >> 3) & 1, grid, ctx->stream));
+      if (ctx->profile) {
+        CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, ctx->stream));
+        ctx->ev_used++;
+      }
+      ctx->stats.pass_launches++;
+      ctx->stats.kernel_launches_total++;
+      continue;
+    }
     if (fp >= 0) {
       fa.phi = d ? dphi + (size_t)pp.d_step * n_phi : nullptr;
       for (int b = 0; b < TILE_BITS; b++) {
@@ -611,11 +987,33 @@ static qaa_status obs_basic(qaa_ctx* ctx, double* basic) {
   CUDA_TRY(cudaMemcpyAsync(ctx->h_out, ctx->d_out, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   for (int j = 0; j < 3; j++) basic[j] = ctx->h_out[j];
+  return comm_sum(ctx, basic, 3);
+}
+
+// sx[phys + phys_offset] = local pair sums of sigma^x on the rotated bits of
+// every group (only_top: the top group's bits >= L - g, after a swap to layout B)
+static qaa_status obs_sigma_local(qaa_ctx* ctx, double* sx, bool only_top);
+
+// sx[j] = <sigma^x_j> for all n qubits (collective when sharded: the global
+// qubits are measured in layout B, between two layout swaps)
+static qaa_status obs_sigma(qaa_ctx* ctx, double* sx) {
+  for (int j = 0; j < ctx->n; j++) sx[j] = 0.0;
+  qaa_status st = obs_sigma_local(ctx, sx, false);
+  if (st) return st;
+  if (ctx->world > 1) {
+    st = shard_remap(ctx);
+    if (st) return st;
+    st = obs_sigma_local(ctx, sx, true);
+    if (st) return st;
+    st = shard_remap(ctx);
+    if (st) return st;
+    st = comm_sum(ctx, sx, ctx->n);
+    if (st) return st;
+  }
   return QAA_OK;
 }
 
-// sx[j] = <sigma^x_j> for local qubits j < L
-static qaa_status obs_sigma(qaa_ctx* ctx, double* sx) {
+static qaa_status obs_sigma_local(qaa_ctx* ctx, double* sx, bool only_top) {
   std::vector<SigmaArgs> jobs;
   if (ctx->L <= RESIDENT_MAX_L) {
     SigmaArgs a;
@@ -628,12 +1026,19 @@ static qaa_status obs_sigma(qaa_ctx* ctx, double* sx) {
     a.ntiles = 1;
     jobs.push_back(a);
   } else {
-    for (const Group& g : ctx->geom.groups) {
+    for (size_t gi = 0; gi < ctx->geom.groups.size(); gi++) {
+      const Group& g = ctx->geom.groups[gi];
+      if (only_top && gi + 1 != ctx->geom.groups.size()) continue;
       SigmaArgs a;
       memset(&a, 0, sizeof a);
       a.psi = ctx->state;
       a.k = TILE_BITS;
       a.mask = g.rot_local;
+      if (only_top) {
+        a.mask = 0;
+        for (int b = 0; b < TILE_BITS; b++)
+          if (g.phys[b] >= ctx->L - ctx->gbits) a.mask |= 1u << b;
+      }
       for (int b = 0; b < TILE_BITS; b++) a.phys[b] = g.phys[b];
       a.nseg = g.nseg;
       for (int s = 0; s < g.nseg; s++) {
@@ -654,8 +1059,10 @@ static qaa_status obs_sigma(qaa_ctx* ctx, double* sx) {
     ctx->stats.kernel_launches_total += 2;
     CUDA_TRY(cudaMemcpyAsync(ctx->h_out, ctx->d_out, TILE_BITS * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    // layout B keeps the rank qubits of layout A (logical L..n-1) at local L-g..L-1
+    const int off = only_top ? ctx->gbits : 0;
     for (int j = 0; j < a.k; j++)
-      if (a.mask >> j & 1) sx[a.phys[j]] = 2.0 * ctx->h_out[j];
+      if (a.mask >> j & 1) sx[a.phys[j] + off] = 2.0 * ctx->h_out[j];
   }
   return QAA_OK;
 }
@@ -664,23 +1071,29 @@ qaa_status qaa_success_prob(qaa_ctx* ctx, double* out) {
   CHECK_CTX();
   if (!out) return fail(ctx, QAA_E_USAGE, "out is NULL");
   if (!ctx->loaded || !ctx->initialized) return fail(ctx, QAA_E_STATE, "success_prob before init");
-  if (ctx->nz_local == 0) {
+  if (ctx->nz_total == 0) {
     *out = 0.0;
     return QAA_OK;
   }
-  if (ctx->z_listed) {
+  if (ctx->nz_total > (uint64_t)ZLIST_CAP) {  // same decision on every rank (collectives must match)
+    double b[3];
+    qaa_status st = obs_basic(ctx, b);  // collective
+    if (st) return st;
+    *out = b[2];
+    return QAA_OK;
+  }
+  double v = 0.0;
+  if (ctx->nz_local > 0) {
     CUDA_TRY(launch_gather_success(ctx->state, ctx->Z, ctx->nz_local, (uint64_t)ctx->rank << ctx->L, ctx->d_out,
                                    ctx->stream));
     ctx->stats.kernel_launches_total++;
     CUDA_TRY(cudaMemcpyAsync(ctx->h_out, ctx->d_out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    *out = ctx->h_out[0];
-    return QAA_OK;
+    v = ctx->h_out[0];
   }
-  double b[3];
-  qaa_status st = obs_basic(ctx, b);
+  qaa_status st = comm_sum(ctx, &v, 1);
   if (st) return st;
-  *out = b[2];
+  *out = v;
   return QAA_OK;
 }
 
@@ -887,3 +1300,41 @@ qaa_status qaa_plan_describe(int n_local, int row_bits, int step_spanning, int64
 }
 
 }  // extern "C"
+
+extern "C" qaa_status qaa_plan_describe_sharded(int n, int world, int row_bits, int64_t K, int32_t* rec, int64_t cap,
+                                                int64_t* count) {
+  if (!count || K < 1 || (cap > 0 && !rec)) return QAA_E_USAGE;
+  if (world != 2 && world != 4 && world != 8) return QAA_E_USAGE;
+  const int g = world == 2 ? 1 : (world == 4 ? 2 : 3);
+  const int L = n - g;
+  if (n < 1 || n > 40 || L <= RESIDENT_MAX_L) return QAA_E_CAP;
+  Geometry geo;
+  std::string e;
+  if (!build_geometry(L, row_bits, &geo, &e)) return QAA_E_USAGE;
+  std::vector<ShardPass> plan;
+  if (!build_shard_schedule(geo, g, K, &plan, &e)) return QAA_E_CAP;
+  *count = (int64_t)plan.size();
+  for (int64_t i = 0; i < (int64_t)plan.size() && i < cap; i++) {
+    const ShardPass& sp = plan[(size_t)i];
+    int32_t* r = rec + i * QAA_SHARD_RECORD;
+    uint32_t pre = 0, post = 0;
+    if (sp.kind == SK_PASS) {
+      const Group& gr = geo.groups[(size_t)sp.group];
+      for (int b = 0; b < TILE_BITS; b++) {
+        if ((sp.pre_local >> b) & 1) pre |= 1u << gr.phys[b];
+        if ((sp.post_local >> b) & 1) post |= 1u << gr.phys[b];
+      }
+    }
+    r[0] = sp.kind;
+    r[1] = sp.group;
+    r[2] = (int32_t)sp.pre_step;
+    r[3] = (int32_t)sp.d_step;
+    r[4] = (int32_t)sp.post_step;
+    r[5] = sp.remote;
+    r[6] = sp.layout;
+    r[7] = (int32_t)pre;
+    r[8] = (int32_t)post;
+    r[9] = 0;
+  }
+  return QAA_OK;
+}

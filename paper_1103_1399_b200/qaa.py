@@ -19,7 +19,8 @@ __all__ = [
     "qaa_init_basis", "qaa_evolve", "qaa_success_prob", "qaa_energy", "qaa_norm2", "qaa_sigma_x",
     "qaa_num_solutions", "qaa_max_energy", "qaa_copy_state", "qaa_set_state", "qaa_copy_energy_table",
     "qaa_state_ptr", "qaa_set_option", "qaa_get_stats", "qaa_reset_stats", "qaa_plan_describe",
-    "qaa_version", "OPT_ROW_BITS", "OPT_PROFILE", "OPT_STEP_SPANNING", "OPT_CTAS_PER_SM", "PLAN_RECORD",
+    "qaa_version", "OPT_ROW_BITS", "OPT_PROFILE", "OPT_STEP_SPANNING", "OPT_CTAS_PER_SM", "OPT_KERNEL",
+    "PLAN_RECORD", "SHARD_RECORD", "TorchComm", "qaa_plan_describe_sharded",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -27,8 +28,9 @@ library_path = os.path.join(_HERE, "libqaa.so")
 
 STATUS = {0: "QAA_OK", 1: "QAA_E_USAGE", 2: "QAA_E_INPUT", 3: "QAA_E_CAP", 4: "QAA_E_STATE",
           5: "QAA_E_CUDA", 6: "QAA_E_NCCL"}
-OPT_ROW_BITS, OPT_PROFILE, OPT_STEP_SPANNING, OPT_CTAS_PER_SM = 1, 2, 3, 4
+OPT_ROW_BITS, OPT_PROFILE, OPT_STEP_SPANNING, OPT_CTAS_PER_SM, OPT_KERNEL = 1, 2, 3, 4, 5
 PLAN_RECORD = 10
+SHARD_RECORD = 10
 
 # symbol list mirrors include/qaa.h (tests check the export table against the header)
 EXPORTS = [
@@ -36,6 +38,7 @@ EXPORTS = [
     "qaa_init_basis", "qaa_evolve", "qaa_success_prob", "qaa_energy", "qaa_norm2", "qaa_sigma_x",
     "qaa_num_solutions", "qaa_max_energy", "qaa_copy_state", "qaa_set_state", "qaa_copy_energy_table",
     "qaa_state_ptr", "qaa_set_option", "qaa_get_stats", "qaa_reset_stats", "qaa_plan_describe", "qaa_version",
+    "qaa_plan_describe_sharded",
 ]
 
 
@@ -45,10 +48,52 @@ class QaaError(RuntimeError):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
 
 
+BARRIER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t)
+
+
+class qaa_comm(ctypes.Structure):
+    _fields_ = [("user", ctypes.c_void_p), ("barrier", BARRIER_FN), ("allgather", ALLGATHER_FN)]
+
+
 class qaa_config(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int),
                 ("world", ctypes.c_int), ("nccl_id", ctypes.c_void_p), ("state", ctypes.c_void_p),
-                ("state_bytes", ctypes.c_size_t)]
+                ("state_bytes", ctypes.c_size_t), ("comm", ctypes.POINTER(qaa_comm))]
+
+
+class TorchComm:
+    """qaa_comm over a torch.distributed process group (gloo for host bytes).
+    Keeps the ctypes callback objects alive for the life of the context."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self._b = BARRIER_FN(self._barrier)
+        self._a = ALLGATHER_FN(self._allgather)
+        self.struct = qaa_comm(None, self._b, self._a)
+
+    def _barrier(self, user):
+        try:
+            self.dist.barrier(group=self.group)
+            return 0
+        except Exception:  # pragma: no cover
+            return 1
+
+    def _allgather(self, user, send, recv, nbytes):
+        try:
+            import torch
+            mine = torch.frombuffer(bytearray(ctypes.string_at(send, nbytes)), dtype=torch.uint8) if nbytes else \
+                torch.zeros(0, dtype=torch.uint8)
+            outs = [torch.zeros(nbytes, dtype=torch.uint8) for _ in range(self.world)]
+            self.dist.all_gather(outs, mine, group=self.group)
+            blob = b"".join(bytes(o.numpy().tobytes()) for o in outs)
+            ctypes.memmove(recv, blob, len(blob))
+            return 0
+        except Exception:  # pragma: no cover
+            return 1
 
 
 class qaa_stats(ctypes.Structure):
@@ -100,6 +145,7 @@ def lib():
             "qaa_get_stats": ([P, ctypes.POINTER(qaa_stats)], I),
             "qaa_reset_stats": ([P], I),
             "qaa_plan_describe": ([I, I, I, I64, P, I64, ctypes.POINTER(I64)], I),
+            "qaa_plan_describe_sharded": ([I, I, I, I64, P, I64, ctypes.POINTER(I64)], I),
             "qaa_version": ([], ctypes.c_char_p),
         }
         for name, (args, res) in sig.items():
@@ -123,8 +169,9 @@ def _dptr(a: np.ndarray):
 
 # ----------------------------------------------------------------- C-named functions
 def qaa_create(device: int = 0, stream: int = 0, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
-               state_ptr: int = 0, state_bytes: int = 0):
-    cfg = qaa_config(device, stream or None, rank, world, None, state_ptr or None, state_bytes)
+               state_ptr: int = 0, state_bytes: int = 0, comm: Optional["TorchComm"] = None):
+    cfg = qaa_config(device, stream or None, rank, world, None, state_ptr or None, state_bytes,
+                     ctypes.pointer(comm.struct) if comm is not None else None)
     idbuf = None
     if nccl_id is not None:
         idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
@@ -269,6 +316,20 @@ def qaa_plan_describe(n_local: int, row_bits: int = 3, step_spanning: int = 1, K
     return rec[: min(cap, cnt.value)]
 
 
+def qaa_plan_describe_sharded(n: int, world: int, row_bits: int = 3, K: int = 1):
+    """Host-only sharded pass plan: array of shape (passes, SHARD_RECORD) int32."""
+    cnt = ctypes.c_int64()
+    st = lib().qaa_plan_describe_sharded(int(n), int(world), int(row_bits), int(K), None, 0, ctypes.byref(cnt))
+    if st != 0:
+        raise QaaError(st, "plan_describe_sharded")
+    rec = np.zeros((cnt.value, SHARD_RECORD), dtype=np.int32)
+    st = lib().qaa_plan_describe_sharded(int(n), int(world), int(row_bits), int(K), _dptr(rec), cnt.value,
+                                         ctypes.byref(cnt))
+    if st != 0:
+        raise QaaError(st, "plan_describe_sharded")
+    return rec
+
+
 def qaa_version() -> str:
     return lib().qaa_version().decode()
 
@@ -279,8 +340,10 @@ class Context:
     is a torch tensor (allocated lazily for 2^n_max amplitudes)."""
 
     def __init__(self, device: int = 0, stream: Optional[int] = None, rank: int = 0, world: int = 1,
-                 nccl_id: Optional[bytes] = None, n_max: Optional[int] = None, torch_state: bool = False):
+                 nccl_id: Optional[bytes] = None, n_max: Optional[int] = None, torch_state: bool = False,
+                 comm: Optional[TorchComm] = None):
         self._tensor = None
+        self._comm = comm
         state_ptr, state_bytes = 0, 0
         if torch_state:
             import torch
@@ -291,7 +354,8 @@ class Context:
             state_ptr, state_bytes = self._tensor.data_ptr(), self._tensor.numel() * 16
             if stream is None:
                 stream = torch.cuda.current_stream(device).cuda_stream
-        self.ctx = qaa_create(device, stream or 0, rank, world, nccl_id, state_ptr, state_bytes)
+        self.ctx = qaa_create(device, stream or 0, rank, world, nccl_id, state_ptr, state_bytes, comm)
+        self.rank, self.world = rank, world
         self.n = None
 
     def close(self):

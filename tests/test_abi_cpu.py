@@ -132,3 +132,59 @@ def test_plan_rejects_bad_args(q):
         q.qaa_plan_describe(0, 3, 1, 1)
     with pytest.raises(q.QaaError):
         q.qaa_plan_describe(20, 9, 1, 1)
+
+
+def replay_sharded(rec, n, world, K):
+    """Replays a sharded plan tracking logical qubits through layouts A/B
+    (plan.hpp): every step gets D once and each of the n logical qubits is
+    rotated exactly once between D_k and D_{k+1}; the plan ends in layout A."""
+    g = world.bit_length() - 1
+    L = n - g
+    layout = 0
+    rot = {}
+    cur = None
+    for r in rec:
+        kind, grp, pre, d, post, remote, lay, pre_m, post_m = (int(x) for x in r[:9])
+        assert lay == layout, "record layout does not match the replayed layout"
+
+        def logical(p):
+            if layout == 0 or p < L - g:
+                return p
+            return p + g  # layout B keeps logical L..n-1 at local L-g..L-1
+        if kind == 0:
+            if pre >= 0:
+                assert pre == cur
+                for p in range(L):
+                    if (pre_m >> p) & 1:
+                        rot[(pre, logical(p))] = rot.get((pre, logical(p)), 0) + 1
+            if d >= 0:
+                if cur is not None:
+                    assert all(rot.get((cur, j), 0) == 1 for j in range(n)), (cur, sorted(rot))
+                assert d == (0 if cur is None else cur + 1)
+                cur = d
+            if post >= 0:
+                assert post == cur
+                for p in range(L):
+                    if (post_m >> p) & 1:
+                        rot[(post, logical(p))] = rot.get((post, logical(p)), 0) + 1
+        if remote:
+            layout ^= 1
+    assert cur == K - 1
+    for k in range(K):
+        for j in range(n):
+            assert rot.get((k, j), 0) == 1, (k, j)
+    assert layout == 0
+
+
+@pytest.mark.parametrize("n,world", [(14, 2), (16, 2), (17, 4), (18, 8), (24, 2), (26, 4), (31, 2), (34, 8), (33, 8)])
+def test_sharded_plan_replay(q, n, world):
+    for K in (1, 2, 3, 6):
+        rec = q.qaa_plan_describe_sharded(n, world, 3, K)
+        replay_sharded(rec, n, world, K)
+        # exactly one remote (layout-swap) pass per step, plus one final remap when K is odd
+        assert int(sum(rec[:, 5])) == K + (K % 2)
+
+
+def test_sharded_plan_rejects_small(q):
+    with pytest.raises(q.QaaError):
+        q.qaa_plan_describe_sharded(13, 2, 3, 1)  # L = 12: single tile group

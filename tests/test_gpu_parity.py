@@ -128,9 +128,10 @@ def test_resident_parity(q, ctx, orc, n):
 
 @pytest.mark.parametrize("n", [13, 14, 15, 16, 18, 21, 22, 23])
 @pytest.mark.parametrize("span", [1, 0])
-@pytest.mark.parametrize("ctas", [1, 2])
-def test_pass_parity_small(q, ctx, orc, n, span, ctas):
-    ctx.set_option(q.OPT_CTAS_PER_SM, ctas)
+@pytest.mark.parametrize("variant", ["tma", "reg1", "reg2"])
+def test_pass_parity_small(q, ctx, orc, n, span, variant):
+    ctx.set_option(q.OPT_KERNEL, 1 if variant == "tma" else 0)
+    ctx.set_option(q.OPT_CTAS_PER_SM, 2 if variant == "reg2" else 1)
     cl = instance(n)
     psi0 = cnf.random_state(n, 100 + n)
     sched = np.random.default_rng(n).uniform(0, 1, 5)

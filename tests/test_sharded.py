@@ -1,0 +1,76 @@
+"""Sharded (multi-rank) path: host plumbing on CPU with gloo (world 2), and
+the full sharded evolution with 2/4/8 ranks sharing one GPU (CUDA IPC peer
+stores between processes), compared with the single-process oracle."""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from inputs import cnf
+
+import qaa_shard_worker as W
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_torchcomm_callbacks_gloo_world2():
+    world = 2
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(W.comm_worker, args=(world, free_port(), d), nprocs=world, join=True)
+        for r in range(world):
+            got = np.load(os.path.join(d, f"comm{r}.npy"))
+            assert list(got) == [0, 1, 2, 3, 4, 10, 11, 12, 13, 14]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,world,K", [(16, 2, 5), (17, 4, 4), (18, 8, 3), (22, 2, 4), (24, 4, 3)])
+def test_sharded_evolution_parity(n, world, K):
+    from oracle import oracle
+    cl = cnf.load_instance(n)[0] if os.path.exists(cnf.instance_path(n)) else cnf.random_instance(n, 4 * n, n)
+    T = 1.9
+    sched = np.random.default_rng(n).uniform(0, 1, K)
+    psi0 = cnf.random_state(n, 5)
+    s_values = [0.0, 0.3, 1.0]
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(W.shard_worker, args=(world, free_port(), d, n, cl, T, K, sched, psi0, s_values),
+                 nprocs=world, join=True)
+        res = [np.load(os.path.join(d, f"rank{r}.npy"), allow_pickle=True).item() for r in range(world)]
+    got = np.concatenate([r["state"] for r in res])
+    E = oracle.energy_table(n, cl)
+    want = oracle.evolve(n, E, psi0, T, K, sched)
+    assert np.max(np.abs(got - want)) < 1e-10
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-11
+    assert np.array_equal(np.concatenate([r["E"] for r in res]).astype(np.uint16), E)
+    ob = oracle.observables(n, E, want)
+    for r in res:  # every rank reports the global values
+        assert abs(r["norm2"] - ob["norm2"]) < 1e-12 * ob["norm2"]
+        assert abs(r["success"] - ob["success"]) < 1e-13
+        assert np.allclose(r["sigma_x"], ob["sigma_x"], atol=1e-12, rtol=0)
+        for s, e in zip(s_values, r["energy"]):
+            assert abs(e - oracle.energy(n, E, want, s)) < 1e-11
+        assert r["nsol"] == int((E == 0).sum()) and r["emax"] == int(E.max())
+
+
+@pytest.mark.gpu
+def test_sharded_uniform_start_paper_config():
+    """configs[0]-like run sharded over 2 ranks: n = 16 instance, uniform start."""
+    from oracle import oracle
+    n, world, K, T = 16, 2, 40, 5.0
+    cl, sol = cnf.load_instance(n)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(W.shard_worker, args=(world, free_port(), d, n, cl, T, K, None, None, [1.0]),
+                 nprocs=world, join=True)
+        res = [np.load(os.path.join(d, f"rank{r}.npy"), allow_pickle=True).item() for r in range(world)]
+    got = np.concatenate([r["state"] for r in res])
+    want = oracle.evolve(n, oracle.energy_table(n, cl), oracle.init_uniform(n), T, K)
+    assert np.max(np.abs(got - want)) < 1e-10
+    assert abs(res[0]["success"] - abs(want[sol]) ** 2) < 1e-13
