@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--step-spanning", type=int, default=1)
     ap.add_argument("--ctas-per-sm", type=int, default=1)
     ap.add_argument("--kernel", type=int, default=1, help="1 = TMA warp-specialised pass, 0 = register pass")
+    ap.add_argument("--tma-groups", type=int, default=0, help="0 = auto, 1 or 2 consumer groups per TMA CTA")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=26)
@@ -178,24 +179,30 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        world = args.gpus if world == 1 else world
+    if world > 1 and world != args.gpus:
+        raise SystemExit(f"WORLD_SIZE={world} but --gpus {args.gpus}")
     torch.cuda.set_device(local)
-    if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = None
+    if world > 1:
+        if not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # host collectives of libqaa (IPC bootstrap, one barrier per step) over gloo
+        comm_group = dist.new_group(backend="gloo")
     import paper_1103_1399_b200 as q
 
+    # weak scaling: 2^30 amplitudes (16 GiB) per GPU, n = 30 + log2(N)
     n = args.n or (N_DEFAULT + (world.bit_length() - 1))
     if world > 1:
-        raise SystemExit("sharded multi-GPU evolve is not built in this round (DESIGN.md §7)")
+        comm = q.TorchComm(comm_group)
     cl, sol = cnf.load_instance(n) if os.path.exists(cnf.instance_path(n)) else (
         cnf.random_instance(n, int(round(4.5 * n)), 1000 + n), None)
     stream = torch.cuda.current_stream(local)
-    ctx = q.Context(local, stream=stream.cuda_stream)
+    ctx = q.Context(local, stream=stream.cuda_stream, rank=rank, world=world, comm=comm)
     ctx.set_option(q.OPT_ROW_BITS, args.row_bits)
     ctx.set_option(q.OPT_STEP_SPANNING, args.step_spanning)
     ctx.set_option(q.OPT_CTAS_PER_SM, args.ctas_per_sm)
     ctx.set_option(q.OPT_KERNEL, args.kernel)
+    ctx.set_option(q.OPT_TMA_GROUPS, args.tma_groups)
     ctx.load_instance(n, cl)
     ctx.init_uniform()
     chunk = args.chunk
@@ -249,18 +256,20 @@ def run_ours(args):
         traffic = tr["bytes_per_launch"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "kernel": "qaa_pass_kernel", "launches": npass,
+                "kernel": "qaa_pass_tma" if (args.kernel == 1 and world == 1) else "qaa_pass_fast",
+                "launches": npass,
                 "avg_launch_ms": kernel_ms / max(npass, 1),
                 "alg_bytes_per_launch": alg_bytes / max(npass, 1),
                 "kernel_share_of_step": kernel_ms / ms if ms > 0 else None,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback B200_PROFILING.md"}
     clocks = clk.summary()
     gpu_launches = st["kernel_launches_total"]
+    ctx.close()  # free the shard buffers before the e2e context allocates its own
 
     # ---------------------------------------------------------------- e2e
     e2e = None
     if not args.no_e2e:
-        ctx2 = q.Context(local, stream=stream.cuda_stream)
+        ctx2 = q.Context(local, stream=stream.cuda_stream, rank=rank, world=world, comm=comm)
         ctx2.set_option(q.OPT_ROW_BITS, args.row_bits)
         ctx2.set_option(q.OPT_STEP_SPANNING, args.step_spanning)
         lits = np.ascontiguousarray(np.asarray(cl, dtype=np.int32).reshape(-1))
@@ -300,7 +309,6 @@ def run_ours(args):
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": f"failed: {e}"}
-    ctx.close()
     if rank == 0:
         line = {"metric": "trotter_steps_per_s", "value": value, "unit": "steps/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,

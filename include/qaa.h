@@ -188,13 +188,17 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        double-buffered prefetch, 2 = two CTAs per SM, no prefetch.
  *  QAA_OPT_KERNEL        1 (default) = warp-specialised TMA pass kernel (producer warp +
  *                        two consumer groups, mbarrier ring of 3 shared-memory slots),
- *                        0 = register-prefetch pass kernel. */
+ *                        0 = register-prefetch pass kernel.
+ *  QAA_OPT_TMA_GROUPS    consumer groups (8 warps each) per TMA CTA: 0 = auto (1 for
+ *                        passes without D: two tiles in flight; 2 for D passes: two
+ *                        groups overlap their transposes and FMAs), or force 1 / 2. */
 enum {
   QAA_OPT_ROW_BITS = 1,
   QAA_OPT_PROFILE = 2,
   QAA_OPT_STEP_SPANNING = 3,
   QAA_OPT_CTAS_PER_SM = 4,
-  QAA_OPT_KERNEL = 5
+  QAA_OPT_KERNEL = 5,
+  QAA_OPT_TMA_GROUPS = 6
 };
 qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value);
 

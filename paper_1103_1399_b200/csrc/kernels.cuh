@@ -94,7 +94,7 @@ struct TmaArgs {
   int dim_seg[5];   // per dim: -1 = tile dim (coordinate 0), else the tile-id segment giving the coordinate
 };
 cudaError_t pass_tma_setup();
-cudaError_t launch_pass_tma(const CUtensorMap* map, const TmaArgs& a, int prog, bool lane3, int grid,
+cudaError_t launch_pass_tma(const CUtensorMap* map, const TmaArgs& a, int prog, bool lane3, int ngroups, int grid,
                             cudaStream_t st);
 // gather a group's energy layout: Eg[T*4096 + l] = E[tbase(T) + off(l)]
 cudaError_t launch_permute_energy(const uint8_t* E, uint8_t* Eg, const int (&phys)[TILE_BITS], int nseg,

@@ -24,7 +24,7 @@ namespace {
 #define FULLM 0xffffffffu
 constexpr int TMA_SLOTS = 3;
 constexpr int SLOT_BYTES = FAST_XBUF * 16;  // 69632: padded exchange layout
-constexpr int TMA_THREADS = 2 * NTHREADS;
+constexpr int TMA_MAX_GROUPS = 2;
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -243,13 +243,13 @@ __device__ __forceinline__ int64_t tile_of(int64_t j) {
   return 2 * (blockIdx.x + (j >> 1) * (int64_t)gridDim.x) + (j & 1);
 }
 
-template <int PROG>
+template <int PROG, int NG>
 __device__ __forceinline__ void issue_tile(const CUtensorMap* tmap, const TmaArgs& a, int64_t j, double2* slots,
                                            uint8_t* eslots, uint64_t* full) {
   using I = Info<PROG>;
   const int s = (int)(j % TMA_SLOTS);
   const int64_t T = tile_of(j);
-  uint64_t* fb = &full[2 * s + (int)(j & 1)];
+  uint64_t* fb = &full[NG * s + (int)(j % NG)];
   mbar_expect_tx(fb, TILE * 16u + (I::has_d ? (uint32_t)TILE : 0u));
   double2* dst = slots + (size_t)s * FAST_XBUF;
   if (a.contiguous) {
@@ -266,39 +266,40 @@ __device__ __forceinline__ void issue_tile(const CUtensorMap* tmap, const TmaArg
   if (I::has_d) bulk_g2s(eslots + (size_t)s * TILE, a.Eg + T * TILE, TILE, fb);
 }
 
-template <int PROG, bool LANE3>
-__global__ void __launch_bounds__(TMA_THREADS, 1) qaa_pass_tma(const __grid_constant__ CUtensorMap tmap,
-                                                              const TmaArgs a) {
+template <int PROG, bool LANE3, int NG>
+__global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_pass_tma(const __grid_constant__ CUtensorMap tmap,
+                                                                const TmaArgs a) {
   extern __shared__ __align__(128) unsigned char sm[];
   double2* slots = reinterpret_cast<double2*>(sm);
   uint8_t* eslots = sm + TMA_SLOTS * SLOT_BYTES;
   double2* phis = reinterpret_cast<double2*>(eslots + TMA_SLOTS * TILE);
-  // full[2*s + g]: slot s landed for consumer group g. Tile j uses slot j % 3
-  // and group j % 2, so each (slot, group) barrier is used by every 6th tile,
-  // always by the same group, and a parity wait can never see a stale phase.
+  // full[NG*s + g]: slot s landed for consumer group g. Tile j uses slot j % 3
+  // and group j % NG, so each (slot, group) barrier is used by every (3 NG)-th
+  // tile, always by the same group, and a parity wait can never see a stale phase.
   uint64_t* full = reinterpret_cast<uint64_t*>(phis + 256);
   using I = Info<PROG>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // tiles of this CTA: pairs (2m, 2m+1), m = blockIdx.x + i gridDim.x (ntiles is even)
   const int64_t nt = 2 * ((a.ntiles / 2 - blockIdx.x + gridDim.x - 1) / gridDim.x);
   if (tid == 0) {
-    for (int s = 0; s < 2 * TMA_SLOTS; s++) mbar_init(&full[s], 1);
+    for (int s = 0; s < NG * TMA_SLOTS; s++) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int64_t j = 0; j < TMA_SLOTS && j < nt; j++) issue_tile<PROG>(&tmap, a, j, slots, eslots, full);
+    for (int64_t j = 0; j < TMA_SLOTS && j < nt; j++) issue_tile<PROG, NG>(&tmap, a, j, slots, eslots, full);
   }
   if (I::has_d)
-    for (int e = tid; e < a.n_phi; e += TMA_THREADS) phis[e] = a.phi[e];
+    for (int e = tid; e < a.n_phi; e += NG * NTHREADS) phis[e] = a.phi[e];
   __syncthreads();
-  // two consumer groups of 8 warps; the group that frees a slot refills it
-  // with tile j + 3 (the other group's next-but-one tile) -- no producer warp,
-  // so 16 warps x 128 registers fit the register file
+  // NG consumer groups of 8 warps; the group that frees a slot refills it with
+  // tile j + 3 -- no producer warp, so 16 warps x 128 registers fit the
+  // register file. NG = 1 keeps two slots in flight (latency-bound passes),
+  // NG = 2 overlaps two groups' transposes and FMAs (compute-heavy passes).
   const int g = warp >> 3, lw = warp & 7;
   const Off ps = make_off<I::store_pat>(a, lane, lw);
   const int tlA = pat_tl<PA>(lane, lw);
   double2 v[RPT];
-  for (int64_t j = g; j < nt; j += 2) {
+  for (int64_t j = g; j < nt; j += NG) {
     const int s = (int)(j % TMA_SLOTS);
-    mbar_wait(&full[2 * s + g], (uint32_t)((j / (2 * TMA_SLOTS)) & 1));
+    mbar_wait(&full[NG * s + g], (uint32_t)((j / (NG * TMA_SLOTS)) & 1));
     double2* xb = slots + (size_t)s * FAST_XBUF;
     const uint8_t* es = eslots + (size_t)s * TILE;
 #pragma unroll
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) qaa_pass_tma(const __grid_cons
     fence_async_shared();
     group_bar(g);
     if ((tid & (NTHREADS - 1)) == 0 && j + TMA_SLOTS < nt)
-      issue_tile<PROG>(&tmap, a, j + TMA_SLOTS, slots, eslots, full);
+      issue_tile<PROG, NG>(&tmap, a, j + TMA_SLOTS, slots, eslots, full);
     const int64_t T = tile_of(j);
     double2* dst = a.psi + tbase(a, T);
 #pragma unroll
@@ -320,36 +321,41 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) qaa_pass_tma(const __grid_cons
 
 typedef void (*TmaKernel)(const CUtensorMap, const TmaArgs);
 
-TmaKernel pick(int prog, bool lane3) {
+template <int NG>
+TmaKernel pick_ng(int prog, bool lane3) {
   switch (prog) {
-    case FP_G0_DPOST: return qaa_pass_tma<FP_G0_DPOST, false>;
-    case FP_G0_PRE: return qaa_pass_tma<FP_G0_PRE, false>;
-    case FP_G0_PRE_D_POST: return qaa_pass_tma<FP_G0_PRE_D_POST, false>;
-    case FP_GK_PRE: return lane3 ? qaa_pass_tma<FP_GK_PRE, true> : qaa_pass_tma<FP_GK_PRE, false>;
-    case FP_GK_PRE_D_POST: return lane3 ? qaa_pass_tma<FP_GK_PRE_D_POST, true> : qaa_pass_tma<FP_GK_PRE_D_POST, false>;
+    case FP_G0_DPOST: return qaa_pass_tma<FP_G0_DPOST, false, NG>;
+    case FP_G0_PRE: return qaa_pass_tma<FP_G0_PRE, false, NG>;
+    case FP_G0_PRE_D_POST: return qaa_pass_tma<FP_G0_PRE_D_POST, false, NG>;
+    case FP_GK_PRE: return lane3 ? qaa_pass_tma<FP_GK_PRE, true, NG> : qaa_pass_tma<FP_GK_PRE, false, NG>;
+    case FP_GK_PRE_D_POST:
+      return lane3 ? qaa_pass_tma<FP_GK_PRE_D_POST, true, NG> : qaa_pass_tma<FP_GK_PRE_D_POST, false, NG>;
     default: return nullptr;
   }
 }
+TmaKernel pick(int prog, bool lane3, int ng) { return ng == 1 ? pick_ng<1>(prog, lane3) : pick_ng<2>(prog, lane3); }
 
 }  // namespace
 
 constexpr size_t TMA_SMEM_BYTES =
-    (size_t)TMA_SLOTS * SLOT_BYTES + (size_t)TMA_SLOTS * TILE + 256 * 16 + 2 * TMA_SLOTS * 8;
+    (size_t)TMA_SLOTS * SLOT_BYTES + (size_t)TMA_SLOTS * TILE + 256 * 16 + TMA_MAX_GROUPS * TMA_SLOTS * 8;
 
 cudaError_t pass_tma_setup() {
   for (int p = 0; p < FP_COUNT; p++)
-    for (int l = 0; l < 2; l++) {
-      cudaError_t e = cudaFuncSetAttribute(pick(p, l), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM_BYTES);
-      if (e != cudaSuccess) return e;
-    }
+    for (int l = 0; l < 2; l++)
+      for (int ng = 1; ng <= 2; ng++) {
+        cudaError_t e =
+            cudaFuncSetAttribute(pick(p, l, ng), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+      }
   return cudaSuccess;
 }
 
-cudaError_t launch_pass_tma(const CUtensorMap* map, const TmaArgs& a, int prog, bool lane3, int grid,
+cudaError_t launch_pass_tma(const CUtensorMap* map, const TmaArgs& a, int prog, bool lane3, int ngroups, int grid,
                             cudaStream_t st) {
-  TmaKernel k = pick(prog, lane3);
+  TmaKernel k = pick(prog, lane3, ngroups);
   if (!k) return cudaErrorInvalidValue;
-  k<<<grid, TMA_THREADS, TMA_SMEM_BYTES, st>>>(*map, a);
+  k<<<grid, ngroups * NTHREADS, TMA_SMEM_BYTES, st>>>(*map, a);
   return cudaGetLastError();
 }
 

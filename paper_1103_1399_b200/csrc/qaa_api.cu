@@ -73,6 +73,7 @@ struct qaa_ctx {
   int step_spanning = 1;
   int ctas_per_sm = 1;
   int kernel_mode = 1;  // 1: TMA warp-specialised pass, 0: register-prefetch pass
+  int tma_groups = 0;   // consumer groups per TMA CTA: 0 = auto (1 without D, 2 with D)
   // TMA state per tile group (built at load)
   std::vector<uint8_t*> Eg;  // per-group permuted energies (Eg[0] = E)
   std::vector<CUtensorMap> tmaps;
@@ -252,6 +253,10 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       return QAA_OK;
     case QAA_OPT_STEP_SPANNING:
       ctx->step_spanning = value != 0;
+      return QAA_OK;
+    case QAA_OPT_TMA_GROUPS:
+      if (value < 0 || value > 2) return fail(ctx, QAA_E_USAGE, "tma groups must be 0 (auto), 1 or 2");
+      ctx->tma_groups = (int)value;
       return QAA_OK;
     case QAA_OPT_KERNEL:
       if (value < 0 || value > 1) return fail(ctx, QAA_E_USAGE, "kernel mode must be 0 or 1");
@@ -895,7 +900,8 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
       }
       const int grid = (int)std::min<int64_t>(gr.ntiles / 2, ctx->num_sms);
       if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
-      CUDA_TRY(launch_pass_tma(&ctx->tmaps[(size_t)pp.group], ta, fp, (gr.rot_local >> 3) & 1, grid, ctx->stream));
+      const int ng = ctx->tma_groups ? ctx->tma_groups : (d ? 2 : 1);
+      CUDA_TRY(launch_pass_tma(&ctx->tmaps[(size_t)pp.group], ta, fp, (gr.rot_local >> 3) & 1, ng, grid, ctx->stream));
       if (ctx->profile) {
         CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, ctx->stream));
         ctx->ev_used++;
