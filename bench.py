@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--ctas-per-sm", type=int, default=1)
     ap.add_argument("--kernel", type=int, default=1, help="1 = TMA warp-specialised pass, 0 = register pass")
     ap.add_argument("--tma-groups", type=int, default=0, help="0 = auto, 1 or 2 consumer groups per TMA CTA")
+    ap.add_argument("--super", type=int, default=0, help="QAA_OPT_SUPER bits (1 = L2-blocked D passes, experimental)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=26)
@@ -203,6 +204,7 @@ def run_ours(args):
     ctx.set_option(q.OPT_CTAS_PER_SM, args.ctas_per_sm)
     ctx.set_option(q.OPT_KERNEL, args.kernel)
     ctx.set_option(q.OPT_TMA_GROUPS, args.tma_groups)
+    ctx.set_option(q.OPT_SUPER, args.super)
     ctx.load_instance(n, cl)
     ctx.init_uniform()
     chunk = args.chunk

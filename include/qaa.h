@@ -191,14 +191,21 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        0 = register-prefetch pass kernel.
  *  QAA_OPT_TMA_GROUPS    consumer groups (8 warps each) per TMA CTA: 0 = auto (1 for
  *                        passes without D: two tiles in flight; 2 for D passes: two
- *                        groups overlap their transposes and FMAs), or force 1 / 2. */
+ *                        groups overlap their transposes and FMAs), or force 1 / 2.
+ *  QAA_OPT_SUPER         bit 0 (default 0, experimental): L2-blocked D passes when the plan
+ *                        has three tile groups (22 <= n <= 30 on one GPU): each Trotter step
+ *                        is one HBM round trip (group k and group 0 processed chunk by chunk
+ *                        in L2; parity-tested, but slower than the default two-pass plan in
+ *                        round 1); bit 1: two consumer groups (known to stall); bit 2: no
+ *                        L2 prefetch. */
 enum {
   QAA_OPT_ROW_BITS = 1,
   QAA_OPT_PROFILE = 2,
   QAA_OPT_STEP_SPANNING = 3,
   QAA_OPT_CTAS_PER_SM = 4,
   QAA_OPT_KERNEL = 5,
-  QAA_OPT_TMA_GROUPS = 6
+  QAA_OPT_TMA_GROUPS = 6,
+  QAA_OPT_SUPER = 7
 };
 qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value);
 

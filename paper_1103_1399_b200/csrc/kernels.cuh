@@ -94,6 +94,21 @@ struct TmaArgs {
   int dim_seg[5];   // per dim: -1 = tile dim (coordinate 0), else the tile-id segment giving the coordinate
 };
 cudaError_t pass_tma_setup();
+// L2-blocked D pass (pass_tma.cu qaa_superpass): group k rotate/D/rotate and
+// group 0 rotate over the same L2-resident chunk; see the comment there.
+struct SuperArgs {
+  TmaArgs gk;          // group k: t[0] = step j, t[1] = step j+1; phi/n_phi = D_{j+1}; Eg = its energy slices
+  TmaArgs g0;          // group 0 (contiguous tiles): t[0] = step j+1
+  int64_t nchunks;
+  int tpc_bits;        // tiles per chunk per sub-pass = 2^tpc_bits
+  uint32_t k_imask, k_cmask;  // group-k tile id = pdep(i, k_imask) | pdep(c, k_cmask)
+  uint32_t z_imask, z_cmask;  // group-0 tile id
+  int prefetch;        // bulk-prefetch each chunk's group-0 tiles into L2 first
+  unsigned* done;      // [nchunks] group-k tiles stored per chunk (zeroed before launch)
+  unsigned long long* queue;  // global work counter (zeroed before launch)
+};
+cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, int ngroups, int grid,
+                             cudaStream_t st);
 cudaError_t launch_pass_tma(const CUtensorMap* map, const TmaArgs& a, int prog, bool lane3, int ngroups, int grid,
                             cudaStream_t st);
 // gather a group's energy layout: Eg[T*4096 + l] = E[tbase(T) + off(l)]

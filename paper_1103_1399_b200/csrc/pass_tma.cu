@@ -319,6 +319,254 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_pass_tma(const __grid_co
   }
 }
 
+// ============================================================================
+// L2-blocked D pass ("super-pass"): group k (rotate step j, D_{j+1}, rotate
+// step j+1) and group 0 (rotate step j+1) over the same data, chunk by chunk.
+// A chunk fixes every physical bit outside (group 0 u group k) tile bits, so
+// its 2^(tpc_bits) group-k tiles and 2^(tpc_bits) group-0 tiles cover the same
+// 2^(12+tpc_bits) amplitudes (32 MiB at n = 30): the group-0 tiles of a chunk
+// are bulk-prefetched into L2 (contiguous 64 KiB reads), the group-k sub-pass
+// runs out of L2, then the group-0 sub-pass, whose dirty lines leave L2 as
+// contiguous write-backs. One HBM round trip per Trotter step instead of two.
+//
+// Work is a global queue, per chunk c: P(c) prefetch items, G(c) group-k
+// tiles, then Z(c-1) group-0 tiles of the previous chunk, so a group-0 tile of
+// chunk c is fetched >= 2^tpc_bits items after the last group-k tile of c.
+// Dependency: a group-0 tile of chunk c needs every group-k tile of c stored
+// (done[c] == 2^tpc_bits). The issuing thread never waits: if the dependency is
+// not met yet, the slot is marked "deferred" and the owning group -- which by
+// queue order holds no item that c still needs -- waits and loads it itself.
+// ============================================================================
+__device__ __forceinline__ uint32_t pdep32(uint32_t x, uint32_t mask) {
+  uint32_t r = 0;
+  for (uint32_t m = mask; m; m &= m - 1) {
+    if (x & 1u) r |= m & (~m + 1u);
+    x >>= 1;
+  }
+  return r;
+}
+
+enum SuperKind : int { SK_END = 0, SK_GK = 1, SK_G0 = 2, SK_G0_DEFERRED = 3 };
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// bounded wait: a lost arrival becomes a trap (launch error) instead of a hang
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* b, uint32_t parity) {
+  for (uint32_t it = 0;; it++) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(sa(b)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (it > (1u << 26)) __trap();
+  }
+}
+__device__ __forceinline__ void mbar_arrive_notx(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(b)) : "memory");
+}
+
+// queue position q -> (kind, chunk, intra index); returns false past the end
+__device__ __forceinline__ bool decode_item(const SuperArgs& a, unsigned long long q, int* kind, int64_t* c,
+                                            uint32_t* i) {
+  const unsigned long long tpc = 1ull << a.tpc_bits;
+  const unsigned long long per = (a.prefetch ? 3ull : 2ull) * tpc;  // items per chunk segment
+  const unsigned long long total = (unsigned long long)a.nchunks * per + tpc;
+  if (q >= total) return false;
+  const unsigned long long seg = q / per, r = q % per;
+  // segment seg: [P(seg)] G(seg) Z(seg - 1); the last segment holds only Z(nchunks-1)
+  if ((int64_t)seg >= a.nchunks) {
+    *kind = SK_G0;
+    *c = a.nchunks - 1;
+    *i = (uint32_t)r;
+    return true;
+  }
+  unsigned long long rr = r;
+  if (a.prefetch) {
+    if (rr < tpc) {
+      *kind = -1;  // prefetch
+      *c = (int64_t)seg;
+      *i = (uint32_t)rr;
+      return true;
+    }
+    rr -= tpc;
+  }
+  if (rr < tpc) {
+    *kind = SK_GK;
+    *c = (int64_t)seg;
+    *i = (uint32_t)rr;
+    return true;
+  }
+  rr -= tpc;
+  if (seg == 0) {  // no Z(-1): treat as a prefetch-like no-op
+    *kind = -2;
+    *c = 0;
+    *i = 0;
+    return true;
+  }
+  *kind = SK_G0;
+  *c = (int64_t)seg - 1;
+  *i = (uint32_t)rr;
+  return true;
+}
+
+struct SlotMeta {
+  int kind;
+  int c;
+  uint32_t T;
+  int pad;
+};
+
+// fetch the next work item for slot s (tile J of this CTA) and start its load
+template <int NG>
+__device__ void super_issue(const CUtensorMap* kmap, const SuperArgs& a, int64_t J, double2* slots, uint8_t* eslots,
+                            uint64_t* full, SlotMeta* meta) {
+  const int s = (int)(J % TMA_SLOTS);
+  uint64_t* fb = &full[NG * s + (int)(J % NG)];
+  int kind;
+  int64_t c;
+  uint32_t i;
+  while (true) {
+    const unsigned long long q = atomicAdd(a.queue, 1ull);
+    if (!decode_item(a, q, &kind, &c, &i)) {
+      meta[s] = SlotMeta{SK_END, 0, 0, 0};
+      mbar_arrive_notx(fb);
+      return;
+    }
+    if (kind == -1) {  // L2 prefetch of a group-0 tile of chunk c (contiguous 64 KiB)
+      const uint32_t T0 = pdep32(i, a.z_imask) | pdep32((uint32_t)c, a.z_cmask);
+      prefetch_l2(a.g0.psi + tbase(a.g0, T0), TILE * 16u);
+      continue;
+    }
+    if (kind == -2) continue;
+    break;
+  }
+  if (kind == SK_GK) {
+    const uint32_t T = pdep32(i, a.k_imask) | pdep32((uint32_t)c, a.k_cmask);
+    meta[s] = SlotMeta{SK_GK, (int)c, T, 0};
+    mbar_expect_tx(fb, TILE * 16u + (uint32_t)TILE);
+    int cc[5];
+#pragma unroll
+    for (int d = 0; d < 5; d++) {
+      const int sg = a.gk.dim_seg[d];
+      cc[d] = sg < 0 ? 0 : (int)((T >> a.gk.seg_src[sg]) & ((1u << a.gk.seg_len[sg]) - 1));
+    }
+    double2* dst = slots + (size_t)s * FAST_XBUF;
+    if (a.gk.contiguous)
+      bulk_g2s(dst, a.gk.psi + tbase(a.gk, T), TILE * 16u, fb);
+    else
+      tma_load(dst, kmap, cc, a.gk.ndims, fb);
+    bulk_g2s(eslots + (size_t)s * TILE, a.gk.Eg + (int64_t)T * TILE, TILE, fb);
+    return;
+  }
+  const uint32_t T0 = pdep32(i, a.z_imask) | pdep32((uint32_t)c, a.z_cmask);
+  if (ld_acquire(&a.done[c]) >= (1u << a.tpc_bits)) {
+    fence_async_global();
+    meta[s] = SlotMeta{SK_G0, (int)c, T0, 0};
+    mbar_expect_tx(fb, TILE * 16u);
+    bulk_g2s(slots + (size_t)s * FAST_XBUF, a.g0.psi + tbase(a.g0, T0), TILE * 16u, fb);
+  } else {
+    meta[s] = SlotMeta{SK_G0_DEFERRED, (int)c, T0, 0};
+    mbar_arrive_notx(fb);
+  }
+}
+
+template <bool LANE3, int NG>
+__global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_constant__ CUtensorMap kmap,
+                                                                 const SuperArgs a) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  double2* slots = reinterpret_cast<double2*>(sm);
+  uint8_t* eslots = sm + TMA_SLOTS * SLOT_BYTES;
+  double2* phis = reinterpret_cast<double2*>(eslots + TMA_SLOTS * TILE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(phis + 256);
+  uint64_t* late = full + NG * TMA_SLOTS;  // per group: deferred group-0 loads
+  SlotMeta* meta = reinterpret_cast<SlotMeta*>(late + NG);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < NG * TMA_SLOTS; s++) mbar_init(&full[s], 1);
+    for (int g = 0; g < NG; g++) mbar_init(&late[g], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int64_t J = 0; J < TMA_SLOTS; J++) super_issue<NG>(&kmap, a, J, slots, eslots, full, meta);
+  }
+  for (int e = tid; e < a.gk.n_phi; e += NG * NTHREADS) phis[e] = a.gk.phi[e];
+  __syncthreads();
+  const int g = warp >> 3, lw = warp & 7, gtid = tid & (NTHREADS - 1);
+  const Off psk = make_off<PA>(a.gk, lane, lw);  // GK_PRE_D_POST stores in pattern PA
+  const Off ps0 = make_off<PB>(a.g0, lane, lw);  // G0_PRE stores in pattern PB
+  const int tlA = pat_tl<PA>(lane, lw);
+  uint32_t late_phase = 0;
+  double2 v[RPT];
+  for (int64_t J = g;; J += NG) {
+    const int s = (int)(J % TMA_SLOTS);
+    mbar_wait_bounded(&full[NG * s + g], (uint32_t)((J / (NG * TMA_SLOTS)) & 1));
+    const SlotMeta m = meta[s];
+    if (m.kind == SK_END) {
+      // tile J+3 belongs to the other group and is only ever issued by the
+      // finisher of J: pass the end marker on before leaving
+      group_bar(g);
+      if (gtid == 0) super_issue<NG>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta);
+      break;
+    }
+    double2* xb = slots + (size_t)s * FAST_XBUF;
+    if (m.kind == SK_G0_DEFERRED) {
+      if (gtid == 0) {
+        for (uint32_t it = 0; ld_acquire(&a.done[m.c]) < (1u << a.tpc_bits); it++) {
+          __nanosleep(64);
+          if (it > (1u << 26)) __trap();
+        }
+        fence_async_global();
+        mbar_expect_tx(&late[g], TILE * 16u);
+        bulk_g2s(xb, a.g0.psi + tbase(a.g0, m.T), TILE * 16u, &late[g]);
+      }
+      mbar_wait_bounded(&late[g], late_phase & 1);
+      late_phase++;
+    }
+    const bool isk = m.kind == SK_GK;
+#pragma unroll
+    for (int r = 0; r < RPT; r++) v[r] = xb[tlA | (r << 8)];
+    group_bar(g);
+    if (isk)
+      program<FP_GK_PRE_D_POST, LANE3>(a.gk, v, xb, eslots + (size_t)s * TILE, phis, lane, lw, g);
+    else
+      program<FP_G0_PRE, false>(a.g0, v, xb, nullptr, phis, lane, lw, g);
+    fence_async_shared();
+    group_bar(g);
+    if (gtid == 0) super_issue<NG>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta);
+    if (isk) {
+      double2* dst = a.gk.psi + tbase(a.gk, m.T);
+#pragma unroll
+      for (int r = 0; r < RPT; r++) dst[roff(psk, r)] = v[r];
+      // publish: this group-k tile is stored (release for the group-0 tiles of chunk c)
+      __threadfence();
+      group_bar(g);
+      if (gtid == 0) {
+        __threadfence();  // cumulative: every store this group made before the barrier
+        atomicAdd(&a.done[m.c], 1u);
+      }
+    } else {
+      double2* dst = a.g0.psi + tbase(a.g0, m.T);
+#pragma unroll
+      for (int r = 0; r < RPT; r++) dst[roff(ps0, r)] = v[r];
+    }
+  }
+}
+
+typedef void (*SuperKernel)(const CUtensorMap, const SuperArgs);
+SuperKernel pick_super(bool lane3, int ng) {
+  if (ng == 1) return lane3 ? qaa_superpass<true, 1> : qaa_superpass<false, 1>;
+  return lane3 ? qaa_superpass<true, 2> : qaa_superpass<false, 2>;
+}
+
 typedef void (*TmaKernel)(const CUtensorMap, const TmaArgs);
 
 template <int NG>
@@ -337,8 +585,17 @@ TmaKernel pick(int prog, bool lane3, int ng) { return ng == 1 ? pick_ng<1>(prog,
 
 }  // namespace
 
-constexpr size_t TMA_SMEM_BYTES =
-    (size_t)TMA_SLOTS * SLOT_BYTES + (size_t)TMA_SLOTS * TILE + 256 * 16 + TMA_MAX_GROUPS * TMA_SLOTS * 8;
+constexpr size_t TMA_SMEM_BYTES = (size_t)TMA_SLOTS * SLOT_BYTES + (size_t)TMA_SLOTS * TILE + 256 * 16 +
+                                   TMA_MAX_GROUPS * TMA_SLOTS * 8 + TMA_MAX_GROUPS * 8 + TMA_SLOTS * 16;
+
+cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, int ngroups, int grid,
+                             cudaStream_t st) {
+  SuperKernel k = pick_super(lane3, ngroups);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  k<<<grid, ngroups * NTHREADS, TMA_SMEM_BYTES, st>>>(*kmap, a);
+  return cudaGetLastError();
+}
 
 cudaError_t pass_tma_setup() {
   for (int p = 0; p < FP_COUNT; p++)

@@ -74,6 +74,13 @@ struct qaa_ctx {
   int ctas_per_sm = 1;
   int kernel_mode = 1;  // 1: TMA warp-specialised pass, 0: register-prefetch pass
   int tma_groups = 0;   // consumer groups per TMA CTA: 0 = auto (1 without D, 2 with D)
+  int super_mode = 0;   // L2-blocked D passes (qaa_superpass) when the plan has 3 tile groups
+  int super_groups = 1;
+  int super_prefetch = 1;
+  SuperArgs super_static[4];
+  bool super_ok[4] = {false, false, false, false};
+  void* d_super = nullptr;  // done[] counters + queue
+  size_t d_super_cap = 0;
   // TMA state per tile group (built at load)
   std::vector<uint8_t*> Eg;  // per-group permuted energies (Eg[0] = E)
   std::vector<CUtensorMap> tmaps;
@@ -213,6 +220,7 @@ void qaa_destroy(qaa_ctx* ctx) {
   if (ctx->d_out) cudaFree(ctx->d_out);
   if (ctx->h_out) cudaFreeHost(ctx->h_out);
   if (ctx->d_counters) cudaFree(ctx->d_counters);
+  if (ctx->d_super) cudaFree(ctx->d_super);
   for (size_t g = 1; g < ctx->Eg.size(); g++)
     if (ctx->Eg[g]) cudaFree(ctx->Eg[g]);
   for (int b = 0; b < 2; b++) {
@@ -253,6 +261,14 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       return QAA_OK;
     case QAA_OPT_STEP_SPANNING:
       ctx->step_spanning = value != 0;
+      return QAA_OK;
+    case QAA_OPT_SUPER:
+      if (value < 0 || value > 7) return fail(ctx, QAA_E_USAGE, "super option must be in 0..7");
+      // bit 0: enable L2-blocked D passes; bit 1: two consumer groups (experimental:
+      // known to stall at the end of the work queue); bit 2: no L2 prefetch
+      ctx->super_mode = (int)(value & 1);
+      ctx->super_groups = (value & 2) ? 2 : 1;
+      ctx->super_prefetch = (value & 4) ? 0 : 1;
       return QAA_OK;
     case QAA_OPT_TMA_GROUPS:
       if (value < 0 || value > 2) return fail(ctx, QAA_E_USAGE, "tma groups must be 0 (auto), 1 or 2");
@@ -375,6 +391,49 @@ static qaa_status build_tma(qaa_ctx* ctx) {
     ctx->tmaps.push_back(map);
     ctx->tma_static.push_back(t);
     ctx->tma_ok.push_back(ok ? 1 : 0);
+  }
+  // L2-blocked D passes pair group 0 with group k (k = 1, 2) on chunks that fix
+  // every physical bit outside their tile bits (pass_tma.cu qaa_superpass)
+  for (int k = 0; k < 4; k++) ctx->super_ok[k] = false;
+  const int P = (int)ctx->geom.groups.size();
+  if (P == 3 && ctx->tma_ok[0]) {
+    const Group& g0 = ctx->geom.groups[0];
+    for (int k = 1; k < P; k++) {
+      if (!ctx->tma_ok[(size_t)k]) continue;
+      const Group& gk = ctx->geom.groups[(size_t)k];
+      if (gk.rot_local & ~0xFF8u) continue;
+      bool in0[64] = {false}, ink[64] = {false};
+      for (int b = 0; b < TILE_BITS; b++) {
+        in0[g0.phys[b]] = true;
+        ink[gk.phys[b]] = true;
+      }
+      SuperArgs sa;
+      memset(&sa, 0, sizeof sa);
+      // group-k tile-id bits = its non-tile bits in ascending physical order
+      int bit = 0;
+      for (int p = 0; p < L; p++) {
+        if (ink[p]) continue;
+        if (in0[p]) sa.k_imask |= 1u << bit;
+        else sa.k_cmask |= 1u << bit;
+        bit++;
+      }
+      bit = 0;
+      for (int p = 0; p < L; p++) {
+        if (in0[p]) continue;
+        if (ink[p]) sa.z_imask |= 1u << bit;
+        else sa.z_cmask |= 1u << bit;
+        bit++;
+      }
+      const int ik = __builtin_popcount(sa.k_imask), iz = __builtin_popcount(sa.z_imask);
+      const int cb = __builtin_popcount(sa.k_cmask);
+      if (ik != iz || cb != __builtin_popcount(sa.z_cmask)) continue;
+      sa.tpc_bits = ik;
+      sa.nchunks = (int64_t)1 << cb;
+      sa.gk = ctx->tma_static[(size_t)k];
+      sa.g0 = ctx->tma_static[0];
+      ctx->super_static[k] = sa;
+      ctx->super_ok[k] = true;
+    }
   }
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return QAA_OK;
@@ -763,6 +822,110 @@ static qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<Step
   return QAA_OK;
 }
 
+// Single-GPU evolve with L2-blocked D passes (3 tile groups, pass_tma.cu
+// qaa_superpass): every Trotter step is ONE HBM round trip.
+//   pass 0:        group 1: D_0, rotate step 0          | group 0: rotate step 0
+//   pass j (odd):  group 2: rotate j-1, D_j, rotate j   | group 0: rotate j
+//   pass j (even): group 1: rotate j-1, D_j, rotate j   | group 0: rotate j
+//   final:         the other group: rotate K-1 (plain TMA pass)
+// Each step rotates group 0 once (with its D), group k as "post" of its pass
+// and the other group as "pre" of the next pass.
+static bool super_usable(qaa_ctx* ctx) {
+  return ctx->super_mode && ctx->world == 1 && ctx->kernel_mode == 1 && ctx->geom.groups.size() == 3 &&
+         ctx->super_ok[1] && ctx->super_ok[2];
+}
+
+static qaa_status evolve_super(qaa_ctx* ctx, int64_t K, const std::vector<StepCoef>& sc, const double2* dphi,
+                               int n_phi) {
+  const int64_t nch = std::max(ctx->super_static[1].nchunks, ctx->super_static[2].nchunks);
+  const size_t need = (size_t)nch * sizeof(unsigned) + 256;
+  if (ctx->d_super_cap < need) {
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    qaa_status st = ensure_buffer(ctx, &ctx->d_super, &ctx->d_super_cap, need);
+    if (st) return st;
+  }
+  if (ctx->profile) {
+    qaa_status st = ensure_events(ctx, ctx->ev_used + (size_t)K + 1);
+    if (st) return st;
+  }
+  unsigned long long* dq = (unsigned long long*)ctx->d_super;
+  unsigned* done = (unsigned*)((char*)ctx->d_super + 256);
+  auto coef = [&](int64_t step) { return sc[(size_t)step].coef; };
+  for (int64_t j = 0; j < K; j++) {
+    const int k = (j % 2 == 0) ? 1 : 2;
+    SuperArgs a = ctx->super_static[k];
+    const Group& gk = ctx->geom.groups[(size_t)k];
+    const Group& g0 = ctx->geom.groups[0];
+    a.gk.psi = ctx->state;
+    a.g0.psi = ctx->state;
+    a.gk.phi = dphi + (size_t)j * n_phi;
+    a.gk.n_phi = n_phi;
+    for (int b = 0; b < TILE_BITS; b++) {
+      const bool rk = (gk.rot_local >> b) & 1;
+      a.gk.t[0][b] = (j >= 1 && rk) ? coef(j - 1) : 0.0;
+      a.gk.t[1][b] = rk ? coef(j) : 0.0;
+      a.gk.phys[b] = gk.phys[b];
+      a.g0.t[0][b] = ((g0.rot_local >> b) & 1) ? coef(j) : 0.0;
+      a.g0.t[1][b] = 0.0;
+      a.g0.phys[b] = g0.phys[b];
+    }
+    a.gk.ntiles = gk.ntiles;
+    a.g0.ntiles = g0.ntiles;
+    a.gk.nseg = gk.nseg;
+    a.g0.nseg = g0.nseg;
+    for (int s = 0; s < MAX_SEGS; s++) {
+      a.gk.seg_src[s] = gk.seg_src[s];
+      a.gk.seg_dst[s] = gk.seg_dst[s];
+      a.gk.seg_len[s] = gk.seg_len[s];
+      a.g0.seg_src[s] = g0.seg_src[s];
+      a.g0.seg_dst[s] = g0.seg_dst[s];
+      a.g0.seg_len[s] = g0.seg_len[s];
+    }
+    a.prefetch = ctx->super_prefetch;
+    a.queue = dq;
+    a.done = done;
+    CUDA_TRY(cudaMemsetAsync(ctx->d_super, 0, 256 + (size_t)a.nchunks * sizeof(unsigned), ctx->stream));
+    if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
+    CUDA_TRY(launch_superpass(&ctx->tmaps[(size_t)k], a, (gk.rot_local >> 3) & 1, ctx->super_groups, ctx->num_sms,
+                              ctx->stream));
+    if (ctx->profile) {
+      CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, ctx->stream));
+      ctx->ev_used++;
+    }
+    ctx->stats.pass_launches++;
+    ctx->stats.kernel_launches_total++;
+  }
+  // final: the group that was not "post" in the last pass rotates for step K-1
+  const int kf = ((K - 1) % 2 == 0) ? 2 : 1;
+  const Group& gr = ctx->geom.groups[(size_t)kf];
+  TmaArgs ta = ctx->tma_static[(size_t)kf];
+  ta.psi = ctx->state;
+  ta.phi = nullptr;
+  ta.n_phi = n_phi;
+  for (int b = 0; b < TILE_BITS; b++) {
+    ta.t[0][b] = ((gr.rot_local >> b) & 1) ? coef(K - 1) : 0.0;
+    ta.t[1][b] = 0.0;
+    ta.phys[b] = gr.phys[b];
+  }
+  ta.ntiles = gr.ntiles;
+  ta.nseg = gr.nseg;
+  for (int s = 0; s < MAX_SEGS; s++) {
+    ta.seg_src[s] = gr.seg_src[s];
+    ta.seg_dst[s] = gr.seg_dst[s];
+    ta.seg_len[s] = gr.seg_len[s];
+  }
+  const int grid = (int)std::min<int64_t>(gr.ntiles / 2, ctx->num_sms);
+  if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
+  CUDA_TRY(launch_pass_tma(&ctx->tmaps[(size_t)kf], ta, FP_GK_PRE, (gr.rot_local >> 3) & 1, 1, grid, ctx->stream));
+  if (ctx->profile) {
+    CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, ctx->stream));
+    ctx->ev_used++;
+  }
+  ctx->stats.pass_launches++;
+  ctx->stats.kernel_launches_total++;
+  return QAA_OK;
+}
+
 static const Program* get_program(qaa_ctx* ctx, int g, bool pre, bool d, bool post) {
   auto key = std::make_tuple(g, (int)pre, (int)d, (int)post);
   auto it = ctx->progs.find(key);
@@ -847,6 +1010,11 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
     ctx->stats.pass_launches++;
     ctx->stats.kernel_launches_total++;
     return QAA_OK;
+  }
+  if (super_usable(ctx) && ctx->step_spanning) {
+    bool tangent = true;
+    for (int64_t k = 0; k < K; k++) tangent = tangent && sc[(size_t)k].form == 0;
+    if (tangent) return evolve_super(ctx, K, sc, dphi, n_phi);
   }
   std::vector<PassPlan> plan;
   build_pass_schedule((int)ctx->geom.groups.size(), K, ctx->step_spanning != 0, &plan);
@@ -1241,6 +1409,7 @@ qaa_status qaa_get_stats(qaa_ctx* ctx, qaa_stats* out) {
   s.row_bits = ctx->row_bits;
   const int P = s.groups;
   s.passes_per_step_num = (ctx->step_spanning && P > 1) ? P - 1 : P;
+  if (ctx->L > RESIDENT_MAX_L && super_usable(ctx) && ctx->step_spanning) s.passes_per_step_num = 1;
   s.passes_per_step_den = 1;
   s.bytes_per_pass = s.amps_local * 32;
   *out = s;

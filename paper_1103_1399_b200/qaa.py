@@ -19,7 +19,7 @@ __all__ = [
     "qaa_init_basis", "qaa_evolve", "qaa_success_prob", "qaa_energy", "qaa_norm2", "qaa_sigma_x",
     "qaa_num_solutions", "qaa_max_energy", "qaa_copy_state", "qaa_set_state", "qaa_copy_energy_table",
     "qaa_state_ptr", "qaa_set_option", "qaa_get_stats", "qaa_reset_stats", "qaa_plan_describe",
-    "qaa_version", "OPT_ROW_BITS", "OPT_PROFILE", "OPT_STEP_SPANNING", "OPT_CTAS_PER_SM", "OPT_KERNEL", "OPT_TMA_GROUPS",
+    "qaa_version", "OPT_ROW_BITS", "OPT_PROFILE", "OPT_STEP_SPANNING", "OPT_CTAS_PER_SM", "OPT_KERNEL", "OPT_TMA_GROUPS", "OPT_SUPER",
     "PLAN_RECORD", "SHARD_RECORD", "TorchComm", "qaa_plan_describe_sharded",
 ]
 
@@ -28,7 +28,7 @@ library_path = os.path.join(_HERE, "libqaa.so")
 
 STATUS = {0: "QAA_OK", 1: "QAA_E_USAGE", 2: "QAA_E_INPUT", 3: "QAA_E_CAP", 4: "QAA_E_STATE",
           5: "QAA_E_CUDA", 6: "QAA_E_NCCL"}
-OPT_ROW_BITS, OPT_PROFILE, OPT_STEP_SPANNING, OPT_CTAS_PER_SM, OPT_KERNEL, OPT_TMA_GROUPS = 1, 2, 3, 4, 5, 6
+OPT_ROW_BITS, OPT_PROFILE, OPT_STEP_SPANNING, OPT_CTAS_PER_SM, OPT_KERNEL, OPT_TMA_GROUPS, OPT_SUPER = 1, 2, 3, 4, 5, 6, 7
 PLAN_RECORD = 10
 SHARD_RECORD = 10
 

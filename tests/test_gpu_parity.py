@@ -334,3 +334,21 @@ def test_torch_owned_state(q, orc):
     want = orc.evolve(14, orc.energy_table(14, cl), orc.init_uniform(14), 1.0, 4)
     assert_close(t.cpu().numpy()[: 1 << 14], want)
     c.close()
+
+
+@pytest.mark.parametrize("n", [22, 23, 24, 26])
+@pytest.mark.parametrize("sup", [1, 5, 0])
+@pytest.mark.parametrize("K", [1, 2, 5])
+def test_super_pass_parity(q, ctx, orc, n, sup, K):
+    """L2-blocked D passes (QAA_OPT_SUPER bit 0, one consumer group; bit 2 = no
+    L2 prefetch) against the oracle; 0 = the two-pass plan."""
+    ctx.set_option(q.OPT_SUPER, sup)
+    cl = instance(n)
+    psi0 = cnf.random_state(n, 31 + n)
+    sched = np.random.default_rng(n + K).uniform(0, 1, K)
+    got, want, _ = run_both(q, ctx, orc, n, cl, 1.3, K, schedule=sched, psi0=psi0)
+    assert_close(got, want)
+    st = ctx.stats()
+    if sup & 1:
+        assert st["pass_launches"] == K + 1  # one HBM round trip per step + the final partial pass
+    ctx.set_option(q.OPT_SUPER, 0)
