@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=26)
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="map every rank to cuda:0 (functional test of --gpus N on a 1-GPU box; not a perf number)")
     return ap.parse_args()
 
 
@@ -180,13 +182,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.share_gpu:  # functional test of the sharded path with all ranks on one GPU
+        local = 0
     if world > 1 and world != args.gpus:
         raise SystemExit(f"WORLD_SIZE={world} but --gpus {args.gpus}")
     torch.cuda.set_device(local)
     comm = None
     if world > 1:
         if not dist.is_initialized():
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            if args.share_gpu:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         # host collectives of libqaa (IPC bootstrap, one barrier per step) over gloo
         comm_group = dist.new_group(backend="gloo")
     import paper_1103_1399_b200 as q
@@ -218,7 +225,7 @@ def run_ours(args):
     ctx.reset_stats()
     ctx.set_option(q.OPT_PROFILE, 1)
     if world > 1:
-        dist.barrier()
+        dist.barrier(group=comm_group)
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -231,13 +238,13 @@ def run_ours(args):
         ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
-        dist.barrier()
+        dist.barrier(group=comm_group)
     ms = ev0.elapsed_time(ev1)
     st = ctx.stats()
     ctx.set_option(q.OPT_PROFILE, 0)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if world > 1:  # max over ranks (host tensor over the gloo group)
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=comm_group)
         ms = float(t.item())
     trotter = args.steps * chunk
     value = trotter / (ms / 1e3)
@@ -292,8 +299,8 @@ def run_ours(args):
         emax = ctx2.max_energy()
         ctx2.close()
         if world > 1:
-            t = torch.tensor([e2e_s], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t = torch.tensor([e2e_s], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=comm_group)
             e2e_s = float(t.item())
         h2d = 32 * len(cl) + chunk * ((emax + 1) * 16 + 12)
         d2h = 16 + 8

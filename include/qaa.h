@@ -151,6 +151,24 @@ qaa_status qaa_norm2(qaa_ctx* ctx, double* out);
  * holds n doubles. Synchronises. Collective. */
 qaa_status qaa_sigma_x(qaa_ctx* ctx, double* out);
 
+/* Batched small-n sweep (the paper's regime of many small
+ * instances): evolve `nrep` independent copies of the uniform state
+ * of the loaded instance, replica r for total time T[r] in K[r] steps of the
+ * midpoint schedule (splitting order of QAA_OPT_ORDER), all in ONE launch with
+ * one CTA per replica and the state resident in shared memory (no HBM traffic);
+ * out[r] = P_succ of replica r (host array of nrep doubles). The context's own
+ * state is not touched. Synchronises.
+ * Errors: USAGE (world > 1, n > 12, nrep < 1, NULL arrays, T[r] < 0 or not
+ * finite, K[r] < 1), STATE (no instance). */
+qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, double* out);
+
+/* Energy-table enumerator as a workload (the paper's own GPU
+ * kernel): recompute the loaded instance's local table
+ * E(x) `reps` times (after one warm-up) and return the average device time per
+ * table in *ms (CUDA events on the context's stream). The table is rewritten
+ * with identical values. Synchronises. Errors: USAGE, STATE (no instance). */
+qaa_status qaa_time_energy_table(qaa_ctx* ctx, int reps, double* ms);
+
 /* *out = |Z|, the number of satisfying assignments (all ranks). */
 qaa_status qaa_num_solutions(qaa_ctx* ctx, uint64_t* out);
 
@@ -197,7 +215,11 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        is one HBM round trip (group k and group 0 processed chunk by chunk
  *                        in L2; parity-tested, but slower than the default two-pass plan in
  *                        round 1); bit 1: two consumer groups (known to stall); bit 2: no
- *                        L2 prefetch. */
+ *                        L2 prefetch.
+ *  QAA_OPT_ORDER         1 (default) = first-order Lie-Trotter, D then X (R7);
+ *                        2 = second-order Strang splitting, D^{1/2} X D^{1/2} per step, at
+ *                        the same HBM cost (the half D's of adjacent steps are merged, the
+ *                        closing half step rides on the last pass). Single GPU. */
 enum {
   QAA_OPT_ROW_BITS = 1,
   QAA_OPT_PROFILE = 2,
@@ -205,7 +227,8 @@ enum {
   QAA_OPT_CTAS_PER_SM = 4,
   QAA_OPT_KERNEL = 5,
   QAA_OPT_TMA_GROUPS = 6,
-  QAA_OPT_SUPER = 7
+  QAA_OPT_SUPER = 7,
+  QAA_OPT_ORDER = 8
 };
 qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value);
 

@@ -58,6 +58,19 @@ def trotter_product(n: int, diag, psi0, T: float, K: int, schedule=None) -> np.n
     return psi
 
 
+def strang_product(n: int, diag, psi0, T: float, K: int, schedule=None) -> np.ndarray:
+    """prod_k expm(-i dt s_k H_P / 2) expm(-i dt (1-s_k) H_B) expm(-i dt s_k H_P / 2) psi0."""
+    dt = T / K
+    HB = h_b(n)
+    HP = h_p(diag)
+    psi = np.array(psi0, dtype=np.complex128)
+    for k in range(K):
+        s = schedule[k] if schedule is not None else (k + 0.5) / K
+        half = scipy.linalg.expm(-0.5j * dt * s * HP)
+        psi = half @ (scipy.linalg.expm(-1j * dt * (1.0 - s) * HB) @ (half @ psi))
+    return psi
+
+
 def exact_piecewise(n: int, diag, psi0, T: float, K: int, substeps: int) -> np.ndarray:
     """Exact propagation of i d/dt psi = H(s(t)) psi with H frozen on each of
     K*substeps sub-intervals at its midpoint s (converges to the continuous

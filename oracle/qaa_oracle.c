@@ -161,6 +161,24 @@ int oracle_evolve(int n, const uint16_t* E, double* psi, double T, int64_t K, co
   return ORACLE_OK;
 }
 
+/* NEXT F4: second-order Strang splitting of the same step,
+ * exp(-i dt s_k H_P / 2) exp(-i dt (1 - s_k) H_B) exp(-i dt s_k H_P / 2),
+ * written literally step by step (no merging of adjacent half steps). */
+int oracle_evolve_strang(int n, const uint16_t* E, double* psi, double T, int64_t K, const double* sched) {
+  if (n < 1 || n > 40 || K < 1 || !(T >= 0.0) || !isfinite(T)) return ORACLE_E_USAGE;
+  if (sched)
+    for (int64_t k = 0; k < K; k++)
+      if (!(sched[k] >= 0.0 && sched[k] <= 1.0)) return ORACLE_E_USAGE;
+  const double dt = T / (double)K;
+  for (int64_t k = 0; k < K; k++) {
+    double s = sched ? sched[k] : ((double)k + 0.5) / (double)K;
+    apply_D(n, psi, E, 0.5 * dt, s);
+    apply_X(n, psi, dt, s);
+    apply_D(n, psi, E, 0.5 * dt, s);
+  }
+  return ORACLE_OK;
+}
+
 /* O-8 helpers: pairwise (recursive halving) summation of f over [lo, hi) in a
  * fixed order, so the error grows like log2(N) * eps rather than N * eps. */
 typedef double (*term_fn)(const void* ctx, int64_t x);

@@ -302,6 +302,14 @@ __global__ void __launch_bounds__(1024, 1) qaa_resident_kernel(const ResidentArg
       __syncthreads();
     }
   }
+  if (a.final_d) {  // Strang: closing half step D(s_{K-1})^{1/2}
+    const double2* phi = a.phi_all + a.K * a.n_phi;
+    for (int x = tid; x < N; x += nt) {
+      const double2 f = phi[e[x]], v = s[x];
+      s[x] = make_double2(fma(f.x, v.x, -f.y * v.y), fma(f.x, v.y, f.y * v.x));
+    }
+    __syncthreads();
+  }
   for (int x = tid; x < N; x += nt) a.psi[x] = s[x];
 }
 
@@ -311,6 +319,66 @@ cudaError_t launch_resident(const ResidentArgs& a, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int threads = a.L >= 10 ? 1024 : ((1 << a.L) < 64 ? 64 : (1 << a.L));
   qaa_resident_kernel<<<1, threads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int NV>
+__device__ __forceinline__ void block_reduce(double (&acc)[NV], double* sh);
+
+// Batched sweep: block r evolves its own copy of the uniform
+// state (L <= 12, resident in shared memory) with its own step count and
+// coefficient rows, then reduces P_succ = sum_{E=0} |psi|^2 (fixed tree).
+__global__ void __launch_bounds__(512) qaa_sweep_kernel(const SweepArgs a) {
+  extern __shared__ double2 smem[];
+  double2* s = smem;
+  uint8_t* e = reinterpret_cast<uint8_t*>(smem + (1 << a.L));
+  __shared__ double red[32];
+  const int r = blockIdx.x;
+  const int N = 1 << a.L, half = N >> 1, tid = threadIdx.x, nt = blockDim.x;
+  const int64_t K = a.K[r], off = a.row_off[r];
+  for (int x = tid; x < N; x += nt) {
+    s[x] = make_double2(a.amp0, 0.0);
+    e[x] = a.E[x];
+  }
+  __syncthreads();
+  for (int64_t k = 0; k < K + (a.final_d ? 1 : 0); k++) {
+    const double2* phi = a.phi_all + (off + k) * a.n_phi;
+    for (int x = tid; x < N; x += nt) {
+      const double2 f = phi[e[x]], v = s[x];
+      s[x] = make_double2(fma(f.x, v.x, -f.y * v.y), fma(f.x, v.y, f.y * v.x));
+    }
+    __syncthreads();
+    if (k == K) break;  // Strang closing half step: no X after it
+    const double c = a.coef[off + k];
+    const int form = a.form[off + k];
+    for (int j = 0; j < a.L; j++) {
+      for (int p = tid; p < half; p += nt) {
+        const int x = ((p >> j) << (j + 1)) | (p & ((1 << j) - 1));
+        const int y = x | (1 << j);
+        double2 u = s[x], w = s[y];
+        if (form == 0)
+          rot_pair<0>(u, w, c);
+        else
+          rot_pair<1>(u, w, c);
+        s[x] = u;
+        s[y] = w;
+      }
+      __syncthreads();
+    }
+  }
+  double acc[1] = {0.0};
+  for (int x = tid; x < N; x += nt)
+    if (e[x] == 0) acc[0] += fma(s[x].x, s[x].x, s[x].y * s[x].y);
+  block_reduce<1>(acc, red);
+  if (tid == 0) a.out[r] = acc[0];
+}
+
+cudaError_t launch_sweep(const SweepArgs& a, int nrep, cudaStream_t st) {
+  const size_t smem = (sizeof(double2) + 1) * ((size_t)1 << a.L);
+  cudaError_t e = cudaFuncSetAttribute(qaa_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int threads = a.L >= 9 ? 512 : ((1 << a.L) < 64 ? 64 : (1 << a.L));
+  qaa_sweep_kernel<<<nrep, threads, smem, st>>>(a);
   return cudaGetLastError();
 }
 

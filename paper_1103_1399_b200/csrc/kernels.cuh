@@ -127,8 +127,27 @@ struct ResidentArgs {
   int n_phi;
   const double* coef;       // K coefficients
   const int32_t* form;      // K forms
+  int final_d;              // 1: apply row K of phi_all after the last X (Strang closing half step)
 };
 cudaError_t launch_resident(const ResidentArgs& a, cudaStream_t st);
+
+// Batched small-n sweep (F1): nrep independent evolutions of the uniform
+// state, one CTA each, replica r with K[r] steps whose table rows start at
+// row_off[r]; out[r] = P_succ.
+struct SweepArgs {
+  const uint8_t* E;
+  int L;
+  double amp0;              // 2^{-n/2}
+  const int64_t* K;
+  const int64_t* row_off;
+  const double2* phi_all;
+  int n_phi;
+  const double* coef;
+  const int32_t* form;
+  int final_d;
+  double* out;
+};
+cudaError_t launch_sweep(const SweepArgs& a, int nrep, cudaStream_t st);
 
 // Energy table (K1; the paper's kernel):
 // E[x] = sum_c [(xg & M_c) == V_c], xg = x_offset + x, also folding

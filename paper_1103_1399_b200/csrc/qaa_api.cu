@@ -71,6 +71,7 @@ struct qaa_ctx {
   int row_bits = 3;
   int profile = 0;
   int step_spanning = 1;
+  int order = 1;  // 1: Lie-Trotter (D then X, R7); 2: Strang (half D, X, half D; NEXT F4)
   int ctas_per_sm = 1;
   int kernel_mode = 1;  // 1: TMA warp-specialised pass, 0: register-prefetch pass
   int tma_groups = 0;   // consumer groups per TMA CTA: 0 = auto (1 without D, 2 with D)
@@ -79,6 +80,9 @@ struct qaa_ctx {
   int super_prefetch = 1;
   SuperArgs super_static[4];
   bool super_ok[4] = {false, false, false, false};
+  void* clause_recs = nullptr;  // device clause records (A1) of the loaded instance
+  size_t clause_recs_cap = 0;
+  int n_recs = 0;
   void* d_super = nullptr;  // done[] counters + queue
   size_t d_super_cap = 0;
   // TMA state per tile group (built at load)
@@ -221,6 +225,7 @@ void qaa_destroy(qaa_ctx* ctx) {
   if (ctx->h_out) cudaFreeHost(ctx->h_out);
   if (ctx->d_counters) cudaFree(ctx->d_counters);
   if (ctx->d_super) cudaFree(ctx->d_super);
+  if (ctx->clause_recs) cudaFree(ctx->clause_recs);
   for (size_t g = 1; g < ctx->Eg.size(); g++)
     if (ctx->Eg[g]) cudaFree(ctx->Eg[g]);
   for (int b = 0; b < 2; b++) {
@@ -261,6 +266,10 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       return QAA_OK;
     case QAA_OPT_STEP_SPANNING:
       ctx->step_spanning = value != 0;
+      return QAA_OK;
+    case QAA_OPT_ORDER:
+      if (value != 1 && value != 2) return fail(ctx, QAA_E_USAGE, "splitting order must be 1 or 2");
+      ctx->order = (int)value;
       return QAA_OK;
     case QAA_OPT_SUPER:
       if (value < 0 || value > 7) return fail(ctx, QAA_E_USAGE, "super option must be in 0..7");
@@ -607,19 +616,20 @@ qaa_status qaa_load_instance(qaa_ctx* ctx, int n, int m, const int32_t* lits) {
     ctx->geom = Geometry();
   }
   ctx->progs.clear();
-  // clause records to device (scratch: reuse the coefficient buffer)
+  // clause records to device (kept for qaa_time_energy_table)
   const size_t rec_bytes = std::max<size_t>(recs.size(), 1) * sizeof(ClauseRecHost);
   {
-    qaa_status st = ensure_buffer(ctx, &ctx->d_coef, &ctx->d_coef_cap, rec_bytes);
+    qaa_status st = ensure_buffer(ctx, &ctx->clause_recs, &ctx->clause_recs_cap, rec_bytes);
     if (st) return st;
   }
   if (ctx->coef_pending) CUDA_TRY(cudaEventSynchronize(ctx->coef_done));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   if (!recs.empty())
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_coef, recs.data(), rec_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(ctx->clause_recs, recs.data(), rec_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->n_recs = (int)recs.size();
   CUDA_TRY(cudaMemsetAsync(ctx->d_counters, 0, 16, ctx->stream));
   const uint64_t x_offset = (uint64_t)ctx->rank << L;
-  CUDA_TRY(launch_energy_table(ctx->E, N, x_offset, (const uint64_t*)ctx->d_coef, (int)recs.size(), ctx->d_counters,
+  CUDA_TRY(launch_energy_table(ctx->E, N, x_offset, (const uint64_t*)ctx->clause_recs, (int)recs.size(), ctx->d_counters,
                                (unsigned long long*)(ctx->d_counters + 2), ctx->num_sms, ctx->stream));
   ctx->stats.kernel_launches_total++;
   unsigned hc[4];
@@ -637,7 +647,7 @@ qaa_status qaa_load_instance(qaa_ctx* ctx, int n, int m, const int32_t* lits) {
     qaa_status st = ensure_buffer(ctx, &p, &ctx->E_B_cap, (size_t)N);
     ctx->E_B = (uint8_t*)p;
     if (st) return st;
-    CUDA_TRY(launch_energy_table(ctx->E_B, N, (uint64_t)ctx->rank << (L - ctx->gbits), (const uint64_t*)ctx->d_coef,
+    CUDA_TRY(launch_energy_table(ctx->E_B, N, (uint64_t)ctx->rank << (L - ctx->gbits), (const uint64_t*)ctx->clause_recs,
                                  (int)recs.size(), ctx->d_counters, (unsigned long long*)(ctx->d_counters + 2),
                                  ctx->num_sms, ctx->stream, L - ctx->gbits, L));
     ctx->stats.kernel_launches_total++;
@@ -711,9 +721,12 @@ struct StepCoef {
 };
 }  // namespace
 
-static void build_step(double T, int64_t K, double s, int n, int n_phi, double2* phi_row, StepCoef* sc) {
+// One row of the coefficient table: the X coefficient of step s (tan or cot of
+// beta = dt (1-s)/2) and Phi[e] = e^{-i theta e} * (X normalisation)^n. theta is
+// dt s for Lie-Trotter; Strang passes the merged half steps (R7, §4).
+static void build_step(double T, int64_t K, double s, double theta, int n, int n_phi, double2* phi_row,
+                       StepCoef* sc) {
   const double dt = T / (double)K;
-  const double theta = dt * s;              // D: exp(-i theta E)
   const double beta = 0.5 * dt * (1.0 - s);  // X: exp(-i beta (1 - sigma^x)) per qubit
   const double cb = std::cos(beta), sb = std::sin(beta);
   double mag;
@@ -946,7 +959,9 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
       if (!(schedule[k] >= 0.0 && schedule[k] <= 1.0))
         return fail(ctx, QAA_E_USAGE, "schedule[%lld] = %g outside [0, 1]", (long long)k, schedule[k]);
   const int n_phi = (int)ctx->emax + 1;
-  const size_t phi_bytes = (size_t)K * n_phi * sizeof(double2);
+  if (ctx->order == 2 && ctx->world > 1)
+    return fail(ctx, QAA_E_USAGE, "second-order (Strang) splitting is single-GPU in this build");
+  const size_t phi_bytes = (size_t)(ctx->order == 2 ? K + 1 : K) * n_phi * sizeof(double2);
   const size_t coef_bytes = (size_t)K * sizeof(double);
   const size_t form_bytes = (size_t)K * sizeof(int32_t);
   const size_t total = phi_bytes + coef_bytes + form_bytes + 256;
@@ -963,11 +978,23 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
   double* hcoef = (double*)((char*)ctx->h_coef + phi_bytes);
   int32_t* hform = (int32_t*)((char*)ctx->h_coef + phi_bytes + coef_bytes);
   std::vector<StepCoef> sc((size_t)K);
+  const double dtK = T / (double)K;
   for (int64_t k = 0; k < K; k++) {
     const double s = schedule ? schedule[k] : ((double)k + 0.5) / (double)K;  // R8 midpoint
-    build_step(T, K, s, ctx->n, n_phi, hphi + (size_t)k * n_phi, &sc[(size_t)k]);
+    double theta = dtK * s;
+    if (ctx->order == 2) {  // Strang: D(s_{k-1})^{1/2} D(s_k)^{1/2} merged before X_k
+      const double sp = k == 0 ? 0.0 : (schedule ? schedule[k - 1] : ((double)k - 0.5) / (double)K);
+      theta = 0.5 * dtK * (sp + s);
+    }
+    build_step(T, K, s, theta, ctx->n, n_phi, hphi + (size_t)k * n_phi, &sc[(size_t)k]);
     hcoef[k] = sc[(size_t)k].coef;
     hform[k] = sc[(size_t)k].form;
+  }
+  if (ctx->order == 2) {  // closing half step D(s_{K-1})^{1/2}, no X after it
+    const double sl = schedule ? schedule[K - 1] : ((double)K - 0.5) / (double)K;
+    const double theta = 0.5 * dtK * sl;
+    for (int e = 0; e < n_phi; e++)
+      hphi[(size_t)K * n_phi + e] = make_double2(std::cos(theta * (double)e), -std::sin(theta * (double)e));
   }
   // the device table is read by kernels still queued from a previous evolve:
   // growing it must not free memory under them
@@ -996,6 +1023,7 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
     ra.n_phi = n_phi;
     ra.coef = dcoef;
     ra.form = dform;
+    ra.final_d = ctx->order == 2 ? 1 : 0;
     size_t ev = ctx->ev_used;
     if (ctx->profile) {
       qaa_status st = ensure_events(ctx, ev + 1);
@@ -1011,13 +1039,16 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
     ctx->stats.kernel_launches_total++;
     return QAA_OK;
   }
-  if (super_usable(ctx) && ctx->step_spanning) {
+  if (super_usable(ctx) && ctx->step_spanning && ctx->order == 1) {
     bool tangent = true;
     for (int64_t k = 0; k < K; k++) tangent = tangent && sc[(size_t)k].form == 0;
     if (tangent) return evolve_super(ctx, K, sc, dphi, n_phi);
   }
   std::vector<PassPlan> plan;
   build_pass_schedule((int)ctx->geom.groups.size(), K, ctx->step_spanning != 0, &plan);
+  // Strang: the closing half step D_K follows the pass that completes X_{K-1}
+  // (its program becomes rotate + D; it runs on the generic kernel)
+  if (ctx->order == 2) plan.back().d_step = K;
   const int max_grid = ctx->num_sms * ctx->ctas_per_sm;
   if (ctx->profile) {
     qaa_status st = ensure_events(ctx, ctx->ev_used + plan.size());
@@ -1068,7 +1099,9 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
       }
       const int grid = (int)std::min<int64_t>(gr.ntiles / 2, ctx->num_sms);
       if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
-      const int ng = ctx->tma_groups ? ctx->tma_groups : (d ? 2 : 1);
+      // auto: one consumer group for the contiguous group-0 rotate pass (two tiles
+      // in flight), two elsewhere (measured, profiles/r01_*)
+      const int ng = ctx->tma_groups ? ctx->tma_groups : ((fp == FP_G0_PRE) ? 1 : 2);
       CUDA_TRY(launch_pass_tma(&ctx->tmaps[(size_t)pp.group], ta, fp, (gr.rot_local >> 3) & 1, ng, grid, ctx->stream));
       if (ctx->profile) {
         CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, ctx->stream));
@@ -1384,6 +1417,113 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps) {
   if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "state_ptr before load_instance");
   *out = ctx->state;
   *amps = 1ull << ctx->L;
+  return QAA_OK;
+}
+
+qaa_status qaa_time_energy_table(qaa_ctx* ctx, int reps, double* ms) {
+  CHECK_CTX();
+  if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "time_energy_table before load_instance");
+  if (reps < 1 || !ms) return fail(ctx, QAA_E_USAGE, "reps must be >= 1 and ms non-NULL");
+  if (!ctx->clause_recs) return fail(ctx, QAA_E_STATE, "no clause records");
+  const int64_t N = (int64_t)1 << ctx->L;
+  cudaEvent_t a, b;
+  CUDA_TRY(cudaEventCreate(&a));
+  CUDA_TRY(cudaEventCreate(&b));
+  // warm-up, then `reps` timed launches recomputing E in place (same values)
+  CUDA_TRY(launch_energy_table(ctx->E, N, (uint64_t)ctx->rank << ctx->L, (const uint64_t*)ctx->clause_recs,
+                               ctx->n_recs, ctx->d_counters, (unsigned long long*)(ctx->d_counters + 2), ctx->num_sms,
+                               ctx->stream));
+  CUDA_TRY(cudaEventRecord(a, ctx->stream));
+  for (int r = 0; r < reps; r++)
+    CUDA_TRY(launch_energy_table(ctx->E, N, (uint64_t)ctx->rank << ctx->L, (const uint64_t*)ctx->clause_recs,
+                                 ctx->n_recs, ctx->d_counters, (unsigned long long*)(ctx->d_counters + 2),
+                                 ctx->num_sms, ctx->stream));
+  CUDA_TRY(cudaEventRecord(b, ctx->stream));
+  CUDA_TRY(cudaEventSynchronize(b));
+  float t = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&t, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  ctx->stats.kernel_launches_total += reps + 1;
+  *ms = (double)t / reps;
+  return QAA_OK;
+}
+
+qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, double* out) {
+  CHECK_CTX();
+  if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "sweep before load_instance");
+  if (ctx->world != 1 || ctx->L > RESIDENT_MAX_L)
+    return fail(ctx, QAA_E_USAGE, "sweep needs world = 1 and n <= %d (state resident in one CTA)", RESIDENT_MAX_L);
+  if (nrep < 1 || !T || !K || !out) return fail(ctx, QAA_E_USAGE, "sweep needs nrep >= 1 and non-NULL arrays");
+  int64_t rows = 0;
+  for (int r = 0; r < nrep; r++) {
+    if (!(T[r] >= 0.0) || !std::isfinite(T[r])) return fail(ctx, QAA_E_USAGE, "T[%d] = %g invalid", r, T[r]);
+    if (K[r] < 1) return fail(ctx, QAA_E_USAGE, "K[%d] = %lld < 1", r, (long long)K[r]);
+    rows += K[r] + (ctx->order == 2 ? 1 : 0);
+  }
+  const int n_phi = (int)ctx->emax + 1;
+  const size_t phi_bytes = (size_t)rows * n_phi * sizeof(double2);
+  const size_t tail = (size_t)rows * (sizeof(double) + sizeof(int32_t)) + (size_t)nrep * 2 * sizeof(int64_t);
+  const size_t total = phi_bytes + tail + (size_t)nrep * sizeof(double) + 512;
+  if (ctx->coef_pending) {
+    CUDA_TRY(cudaEventSynchronize(ctx->coef_done));
+    ctx->coef_pending = false;
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  qaa_status st = ensure_host(ctx, &ctx->h_coef, &ctx->h_coef_cap, total);
+  if (st) return st;
+  st = ensure_buffer(ctx, &ctx->d_coef, &ctx->d_coef_cap, total);
+  if (st) return st;
+  char* hb = (char*)ctx->h_coef;
+  double2* hphi = (double2*)hb;
+  double* hcoef = (double*)(hb + phi_bytes);
+  int32_t* hform = (int32_t*)(hcoef + rows);
+  int64_t* hK = (int64_t*)(((uintptr_t)(hform + rows) + 15) & ~(uintptr_t)15);
+  int64_t* hoff = hK + nrep;
+  int64_t row = 0;
+  for (int r = 0; r < nrep; r++) {
+    hK[r] = K[r];
+    hoff[r] = row;
+    const double dt = T[r] / (double)K[r];
+    for (int64_t k = 0; k < K[r]; k++) {
+      const double s = ((double)k + 0.5) / (double)K[r];
+      double theta = dt * s;
+      if (ctx->order == 2) theta = 0.5 * dt * ((k == 0 ? 0.0 : ((double)k - 0.5) / (double)K[r]) + s);
+      StepCoef c;
+      build_step(T[r], K[r], s, theta, ctx->n, n_phi, hphi + (size_t)(row + k) * n_phi, &c);
+      hcoef[row + k] = c.coef;
+      hform[row + k] = c.form;
+    }
+    row += K[r];
+    if (ctx->order == 2) {
+      const double theta = 0.5 * dt * (((double)K[r] - 0.5) / (double)K[r]);
+      for (int e = 0; e < n_phi; e++)
+        hphi[(size_t)row * n_phi + e] = make_double2(std::cos(theta * (double)e), -std::sin(theta * (double)e));
+      hcoef[row] = 0.0;
+      hform[row] = 0;
+      row++;
+    }
+  }
+  const size_t used = (size_t)((char*)(hoff + nrep) - hb);
+  CUDA_TRY(cudaMemcpyAsync(ctx->d_coef, ctx->h_coef, used, cudaMemcpyHostToDevice, ctx->stream));
+  char* db = (char*)ctx->d_coef;
+  SweepArgs a;
+  a.E = ctx->E;
+  a.L = ctx->L;
+  a.amp0 = 1.0 / std::sqrt(std::ldexp(1.0, ctx->n));
+  a.phi_all = (const double2*)db;
+  a.n_phi = n_phi;
+  a.coef = (const double*)(db + phi_bytes);
+  a.form = (const int32_t*)(db + ((char*)hform - hb));
+  a.K = (const int64_t*)(db + ((char*)hK - hb));
+  a.row_off = (const int64_t*)(db + ((char*)hoff - hb));
+  a.final_d = ctx->order == 2 ? 1 : 0;
+  double* dout = (double*)(db + ((used + 15) & ~(size_t)15));
+  a.out = dout;
+  CUDA_TRY(launch_sweep(a, nrep, ctx->stream));
+  ctx->stats.kernel_launches_total++;
+  CUDA_TRY(cudaMemcpyAsync(out, dout, (size_t)nrep * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return QAA_OK;
 }
 

@@ -16,10 +16,10 @@ import numpy as np
 __all__ = [
     "QaaError", "Context", "lib", "library_path", "STATUS",
     "qaa_create", "qaa_destroy", "qaa_last_error", "qaa_load_instance", "qaa_init_uniform",
-    "qaa_init_basis", "qaa_evolve", "qaa_success_prob", "qaa_energy", "qaa_norm2", "qaa_sigma_x",
+    "qaa_init_basis", "qaa_evolve", "qaa_sweep", "qaa_time_energy_table", "qaa_success_prob", "qaa_energy", "qaa_norm2", "qaa_sigma_x",
     "qaa_num_solutions", "qaa_max_energy", "qaa_copy_state", "qaa_set_state", "qaa_copy_energy_table",
     "qaa_state_ptr", "qaa_set_option", "qaa_get_stats", "qaa_reset_stats", "qaa_plan_describe",
-    "qaa_version", "OPT_ROW_BITS", "OPT_PROFILE", "OPT_STEP_SPANNING", "OPT_CTAS_PER_SM", "OPT_KERNEL", "OPT_TMA_GROUPS", "OPT_SUPER",
+    "qaa_version", "OPT_ROW_BITS", "OPT_PROFILE", "OPT_STEP_SPANNING", "OPT_CTAS_PER_SM", "OPT_KERNEL", "OPT_TMA_GROUPS", "OPT_SUPER", "OPT_ORDER",
     "PLAN_RECORD", "SHARD_RECORD", "TorchComm", "qaa_plan_describe_sharded",
 ]
 
@@ -28,7 +28,8 @@ library_path = os.path.join(_HERE, "libqaa.so")
 
 STATUS = {0: "QAA_OK", 1: "QAA_E_USAGE", 2: "QAA_E_INPUT", 3: "QAA_E_CAP", 4: "QAA_E_STATE",
           5: "QAA_E_CUDA", 6: "QAA_E_NCCL"}
-OPT_ROW_BITS, OPT_PROFILE, OPT_STEP_SPANNING, OPT_CTAS_PER_SM, OPT_KERNEL, OPT_TMA_GROUPS, OPT_SUPER = 1, 2, 3, 4, 5, 6, 7
+OPT_ROW_BITS, OPT_PROFILE, OPT_STEP_SPANNING, OPT_CTAS_PER_SM, OPT_KERNEL, OPT_TMA_GROUPS, OPT_SUPER, OPT_ORDER = \
+    1, 2, 3, 4, 5, 6, 7, 8
 PLAN_RECORD = 10
 SHARD_RECORD = 10
 
@@ -38,7 +39,7 @@ EXPORTS = [
     "qaa_init_basis", "qaa_evolve", "qaa_success_prob", "qaa_energy", "qaa_norm2", "qaa_sigma_x",
     "qaa_num_solutions", "qaa_max_energy", "qaa_copy_state", "qaa_set_state", "qaa_copy_energy_table",
     "qaa_state_ptr", "qaa_set_option", "qaa_get_stats", "qaa_reset_stats", "qaa_plan_describe", "qaa_version",
-    "qaa_plan_describe_sharded",
+    "qaa_plan_describe_sharded", "qaa_sweep", "qaa_time_energy_table",
 ]
 
 
@@ -146,6 +147,8 @@ def lib():
             "qaa_reset_stats": ([P], I),
             "qaa_plan_describe": ([I, I, I, I64, P, I64, ctypes.POINTER(I64)], I),
             "qaa_plan_describe_sharded": ([I, I, I, I64, P, I64, ctypes.POINTER(I64)], I),
+            "qaa_sweep": ([P, I, P, P, P], I),
+            "qaa_time_energy_table": ([P, I, ctypes.POINTER(D)], I),
             "qaa_version": ([], ctypes.c_char_p),
         }
         for name, (args, res) in sig.items():
@@ -246,6 +249,23 @@ def qaa_sigma_x(ctx, n: int) -> np.ndarray:
     out = np.zeros(n, dtype=np.float64)
     _check(ctx, lib().qaa_sigma_x(ctx, _dptr(out)))
     return out
+
+
+def qaa_sweep(ctx, T, K) -> np.ndarray:
+    """F1: P_succ of independent evolutions (T[r], K[r]) of the uniform state, one launch."""
+    Ta = np.ascontiguousarray(T, dtype=np.float64)
+    Ka = np.ascontiguousarray(K, dtype=np.int64)
+    assert Ta.size == Ka.size
+    out = np.zeros(Ta.size, dtype=np.float64)
+    _check(ctx, lib().qaa_sweep(ctx, int(Ta.size), _dptr(Ta), _dptr(Ka), _dptr(out)))
+    return out
+
+
+def qaa_time_energy_table(ctx, reps: int = 5) -> float:
+    """F2: average device ms to recompute the energy table (the paper's kernel)."""
+    out = ctypes.c_double()
+    _check(ctx, lib().qaa_time_energy_table(ctx, int(reps), ctypes.byref(out)))
+    return out.value
 
 
 def qaa_num_solutions(ctx) -> int:
@@ -399,6 +419,12 @@ class Context:
 
     def sigma_x(self):
         return qaa_sigma_x(self.ctx, self.n)
+
+    def time_energy_table(self, reps=5):
+        return qaa_time_energy_table(self.ctx, reps)
+
+    def sweep(self, T, K):
+        return qaa_sweep(self.ctx, T, K)
 
     def num_solutions(self):
         return qaa_num_solutions(self.ctx)

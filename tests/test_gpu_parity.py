@@ -352,3 +352,52 @@ def test_super_pass_parity(q, ctx, orc, n, sup, K):
     if sup & 1:
         assert st["pass_launches"] == K + 1  # one HBM round trip per step + the final partial pass
     ctx.set_option(q.OPT_SUPER, 0)
+
+
+@pytest.mark.parametrize("n", [6, 12, 16, 22, 23])
+@pytest.mark.parametrize("span", [1, 0])
+@pytest.mark.parametrize("kernel", [1, 0])
+def test_strang_parity(q, ctx, orc, n, span, kernel):
+    """NEXT F4: second-order Strang splitting (QAA_OPT_ORDER = 2) against the
+    oracle's literal half-D / X / half-D steps."""
+    ctx.set_option(q.OPT_ORDER, 2)
+    ctx.set_option(q.OPT_STEP_SPANNING, span)
+    ctx.set_option(q.OPT_KERNEL, kernel)
+    cl = instance(n)
+    ctx.load_instance(n, cl)
+    psi0 = cnf.random_state(n, 77)
+    ctx.set_state(psi0)
+    K = 6
+    sched = np.random.default_rng(n).uniform(0, 1, K)
+    ctx.evolve(2.2, K, sched)
+    want = orc.evolve_strang(n, orc.energy_table(n, cl), psi0, 2.2, K, sched)
+    assert_close(ctx.state(), want)
+    ctx.set_option(q.OPT_ORDER, 1)
+
+
+@pytest.mark.parametrize("n", [6, 8, 12])
+@pytest.mark.parametrize("order", [1, 2])
+def test_sweep_parity(q, ctx, orc, n, order):
+    """NEXT F1: batched T sweep (one CTA per replica) against one oracle run per
+    replica (configs[1]-style sweep T in {1,2,5,10,20} at dt = 0.05)."""
+    cl, sol = (cnf.load_instance(n) if n != 6 else (cnf.paper_instance()[1], 10))
+    ctx.set_option(q.OPT_ORDER, order)
+    ctx.load_instance(n, cl)
+    Ts = np.array([1.0, 2.0, 5.0, 10.0, 20.0])
+    Ks = (Ts / 0.05).astype(np.int64)
+    got = ctx.sweep(Ts, Ks)
+    E = orc.energy_table(n, cl)
+    for T, K, p in zip(Ts, Ks, got):
+        ev = orc.evolve if order == 1 else orc.evolve_strang
+        want = ev(n, E, orc.init_uniform(n), float(T), int(K))
+        assert abs(p - orc.observables(n, E, want)["success"]) < 1e-12
+    ctx.set_option(q.OPT_ORDER, 1)
+
+
+def test_sweep_errors(q, ctx):
+    ctx.load_instance(14, instance(14))
+    with pytest.raises(q.QaaError):
+        ctx.sweep([1.0], [10])  # n > 12
+    ctx.load_instance(8, instance(8))
+    with pytest.raises(q.QaaError):
+        ctx.sweep([1.0], [0])

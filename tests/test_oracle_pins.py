@@ -290,3 +290,28 @@ def test_energy_at_matches_table(oracle_mod):
     assert list(oracle_mod.energy_at(n, cl, xs)) == [int(E[int(x)]) for x in xs]
     bf = brute_force_energy(n, cl)
     assert list(oracle_mod.energy_at(n, cl, xs)) == [bf[int(x)] for x in xs]
+
+
+# --------------------------------------------------------------------------- NEXT F4: Strang splitting
+@pytest.mark.parametrize("n,m,T,K,seed", [(3, 6, 2.0, 5, 1), (5, 20, 4.0, 9, 2), (6, 27, 10.0, 20, 3)])
+def test_strang_vs_dense_product(oracle_mod, n, m, T, K, seed):
+    cl = cnf.random_instance(n, m, seed)
+    E = oracle_mod.energy_table(n, cl)
+    psi0 = cnf.random_state(n, seed)
+    sched = np.random.default_rng(seed).uniform(0, 1, K)
+    got = oracle_mod.evolve_strang(n, E, psi0, T, K, sched)
+    want = dense.strang_product(n, brute_force_energy(n, cl), psi0, T, K, sched)
+    assert np.max(np.abs(got - want)) < 1e-13
+
+
+def test_strang_second_order_convergence(oracle_mod):
+    """Strang splitting is second order: halving dt quarters the error against the
+    exact evolution (eigendecomposition on 8000 sub-intervals)."""
+    n, cl = cnf.paper_instance()
+    E = oracle_mod.energy_table(n, cl)
+    diag = brute_force_energy(n, cl)
+    psi0 = oracle_mod.init_uniform(n)
+    ref = dense.exact_piecewise(n, diag, psi0, 10.0, 1, 8000)
+    errs = [np.max(np.abs(oracle_mod.evolve_strang(n, E, psi0, 10.0, K) - ref)) for K in (50, 100, 200)]
+    r1, r2 = errs[0] / errs[1], errs[1] / errs[2]
+    assert 3.5 < r1 < 4.5 and 3.5 < r2 < 4.5, errs
