@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=None, help="qubits (default 30 + log2(gpus))")
+    ap.add_argument("--qubits", dest="n", type=int, default=None, help="qubits n (default 30 + log2(gpus))")
     ap.add_argument("--chunk", type=int, default=20, help="Trotter steps per bench step")
     ap.add_argument("--row-bits", type=int, default=3)
     ap.add_argument("--step-spanning", type=int, default=1)
@@ -204,7 +204,10 @@ def run_ours(args):
         comm = q.TorchComm(comm_group)
     cl, sol = cnf.load_instance(n) if os.path.exists(cnf.instance_path(n)) else (
         cnf.random_instance(n, int(round(4.5 * n)), 1000 + n), None)
-    stream = torch.cuda.current_stream(local)
+    # a dedicated (non-default) stream: libqaa enqueues every kernel on it and
+    # the timing events below are recorded on the same stream
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     ctx = q.Context(local, stream=stream.cuda_stream, rank=rank, world=world, comm=comm)
     ctx.set_option(q.OPT_ROW_BITS, args.row_bits)
     ctx.set_option(q.OPT_STEP_SPANNING, args.step_spanning)
@@ -326,7 +329,10 @@ def run_ours(args):
                 "config": {"workload": f"n={n} unique-solution 3-SAT (inputs/instances), T=200, K=1e4 (dt=0.02), "
                                        f"{chunk} Trotter steps + P_succ per bench step",
                            "n": n, "m": len(cl), "chunk": chunk, "row_bits": args.row_bits,
-                           "step_spanning": args.step_spanning, "kernel": "tma" if args.kernel else "register",
+                           "step_spanning": args.step_spanning,
+                           "kernel": ("tma" if args.kernel else "register") if world == 1 else
+                           "register + fused peer-store layout swap (sharded)",
+                           "shared_gpu_functional_test": bool(args.share_gpu),
                            "passes_per_step":
                                st["passes_per_step_num"] / st["passes_per_step_den"], "tile_groups": st["groups"],
                            "l2": "state 16 GiB >> 126 MB L2 (no flush needed)",

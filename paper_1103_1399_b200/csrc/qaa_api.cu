@@ -1550,6 +1550,7 @@ qaa_status qaa_get_stats(qaa_ctx* ctx, qaa_stats* out) {
   const int P = s.groups;
   s.passes_per_step_num = (ctx->step_spanning && P > 1) ? P - 1 : P;
   if (ctx->L > RESIDENT_MAX_L && super_usable(ctx) && ctx->step_spanning) s.passes_per_step_num = 1;
+  if (ctx->world > 1) s.passes_per_step_num = P;  // sharded: one phase of P passes per step (§7)
   s.passes_per_step_den = 1;
   s.bytes_per_pass = s.amps_local * 32;
   *out = s;

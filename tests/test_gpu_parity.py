@@ -401,3 +401,42 @@ def test_sweep_errors(q, ctx):
     ctx.load_instance(8, instance(8))
     with pytest.raises(q.QaaError):
         ctx.sweep([1.0], [0])
+
+
+@pytest.mark.parametrize("n", [31, 32, 33])
+def test_max_size_closed_forms(q, orc, n):
+    """Largest single-GPU sizes (n = 33: 128 GiB state, four tile groups):
+    s = 1 closed form psi_K(x) = 2^{-n/2} e^{-i T E(x)} on sampled x with E from
+    the oracle, and the norm after a few general steps."""
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    need = (16 + 1 + 3) * (1 << n) + (4 << 30)
+    if free < need:
+        pytest.skip(f"needs {need >> 30} GiB free, have {free >> 30}")
+    cl, sol = cnf.load_instance(n)
+    with q.Context(0) as c:
+        c.load_instance(n, cl)
+        assert c.num_solutions() == 1 and c.energy_table(sol, 1)[0] == 0
+        c.init_uniform()
+        T, K = 0.21, 3
+        c.evolve(T, K, np.ones(K))
+        rng = np.random.default_rng(n)
+        for s0 in list(rng.integers(0, (1 << n) - 32, 12)) + [sol - 5]:
+            xs = np.arange(s0, s0 + 32, dtype=np.uint64)
+            want = 2.0 ** (-n / 2) * np.exp(-1j * T * orc.energy_at(n, cl, xs).astype(float))
+            assert_close(c.state(int(s0), 32), want, atol=1e-15, rtol_l2=1e-12)
+        c.evolve(0.06, 3)
+        assert abs(c.norm2() - 1.0) < 1e-12
+
+
+def test_empty_instance_large(q, ctx, orc):
+    """m = 0: E = 0 everywhere, Z = all 2^n assignments (full-pass success path)."""
+    n = 20
+    ctx.load_instance(n, [])
+    assert ctx.num_solutions() == 1 << n and ctx.max_energy() == 0
+    psi0 = cnf.random_state(n, 2)
+    ctx.set_state(psi0)
+    ctx.evolve(1.0, 4)
+    want = orc.evolve(n, orc.energy_table(n, []), psi0, 1.0, 4)
+    assert_close(ctx.state(), want)
+    assert abs(ctx.success_prob() - ctx.norm2()) < 1e-13

@@ -16,7 +16,7 @@ from inputs import cnf  # noqa: E402
 
 out = {"workload": "energy table E(x), x in [0, 2^n) (K1 / the paper's kernel)", "rows": []}
 with q.Context(0) as c:
-    for n in (20, 24, 28, 30):
+    for n in (20, 24, 30, 32):
         cl, _ = cnf.load_instance(n)
         c.load_instance(n, cl)
         ms = c.time_energy_table(5)
