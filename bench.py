@@ -47,7 +47,8 @@ def parse():
     ap.add_argument("--qubits", dest="n", type=int, default=None, help="qubits n (default 30 + log2(gpus))")
     ap.add_argument("--chunk", type=int, default=20, help="Trotter steps per bench step")
     ap.add_argument("--row-bits", type=int, default=3)
-    ap.add_argument("--step-spanning", type=int, default=1)
+    ap.add_argument("--step-spanning", type=int, default=2,
+                    help="2 = D only on strided groups (default), 1 = cyclic, 0 = no spanning")
     ap.add_argument("--ctas-per-sm", type=int, default=1)
     ap.add_argument("--kernel", type=int, default=1, help="1 = TMA warp-specialised pass, 0 = register pass")
     ap.add_argument("--tma-groups", type=int, default=0, help="0 = auto, 1 or 2 consumer groups per TMA CTA")

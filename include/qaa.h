@@ -199,9 +199,12 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        every tile keeps (128/256/512-byte rows). Default 3.
  *  QAA_OPT_PROFILE       1 = record a CUDA event pair around every pass kernel
  *                        launch of evolve (read back with qaa_get_stats).
- *  QAA_OPT_STEP_SPANNING 1 (default) = merge the last tile group of step k with
- *                        the first of step k+1 around D_{k+1};
- *                        0 = one D per step in the first pass only.
+ *  QAA_OPT_STEP_SPANNING 2 (default) = step spanning with D only on the strided
+ *                        groups (group 0 is a plain contiguous pass every step);
+ *                        1 = cyclic step spanning (D visits every group); both merge
+ *                        the last tile group of step k with the first of step k+1
+ *                        around D_{k+1}: P-1 passes per step;
+ *                        0 = one D per step in the first pass only (P passes/step).
  *  QAA_OPT_CTAS_PER_SM   register-kernel variant: 1 = one CTA per SM with register
  *                        double-buffered prefetch, 2 = two CTAs per SM, no prefetch.
  *  QAA_OPT_KERNEL        1 (default) = warp-specialised TMA pass kernel (producer warp +

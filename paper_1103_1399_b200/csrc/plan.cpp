@@ -93,9 +93,35 @@ bool build_geometry(int L, int row_bits, Geometry* g, std::string* err) {
   return true;
 }
 
-void build_pass_schedule(int P, int64_t K, bool step_spanning, std::vector<PassPlan>* out) {
+void build_pass_schedule(int P, int64_t K, int step_spanning, std::vector<PassPlan>* out) {
   out->clear();
   if (K <= 0 || P <= 0) return;
+  if (step_spanning == 2 && P >= 3) {
+    // Group 0 never hosts D: D_{k+1} always rides on a strided group g >= 1
+    // (rotate step k, D_{k+1}, rotate step k+1 on its tile), and every step
+    // visits group 0 with a plain contiguous pass. Same pass count as the
+    // cyclic schedule (K (P-1) + 1) but without the 4-transpose group-0 D pass
+    // and without plain passes over 128-byte-row tiles when P = 3.
+    int dg = 1;
+    out->push_back({1, -1, 0, 0});
+    for (int64_t k = 0; k < K; k++) {
+      std::vector<int> rem{0};
+      for (int g = 1; g < P; g++)
+        if (g != dg) rem.push_back(g);
+      int next = dg;
+      for (size_t i = 0; i < rem.size(); i++) {
+        const int g = rem[i];
+        if (i + 1 == rem.size() && k + 1 < K) {
+          out->push_back({g, k, k + 1, k + 1});
+          next = g;
+        } else {
+          out->push_back({g, k, -1, -1});
+        }
+      }
+      dg = next;
+    }
+    return;
+  }
   if (!step_spanning || P == 1) {
     for (int64_t k = 0; k < K; k++)
       for (int g = 0; g < P; g++) out->push_back({g, g == 0 ? -1 : k, g == 0 ? k : -1, g == 0 ? k : -1});

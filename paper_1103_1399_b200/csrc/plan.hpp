@@ -87,7 +87,11 @@ struct PassPlan {
 bool build_geometry(int L, int row_bits, Geometry* g, std::string* err);
 
 // Pass schedule for K steps (step_spanning: see header comment).
-void build_pass_schedule(int ngroups, int64_t K, bool step_spanning, std::vector<PassPlan>* out);
+// step_spanning: 0 = one D per step in the first (group-0) pass, P passes per
+// step; 1 = cyclic spanning, P-1 passes per step, D visits every group;
+// 2 = spanning with D only on groups >= 1 (group 0 always a plain pass; falls
+// back to 1 when P < 3).
+void build_pass_schedule(int ngroups, int64_t K, int step_spanning, std::vector<PassPlan>* out);
 
 // ---------------------------------------------------------------- sharded plan
 // World W = 2^g ranks hold the state on its top g qubits.

@@ -70,7 +70,7 @@ struct qaa_ctx {
   // options
   int row_bits = 3;
   int profile = 0;
-  int step_spanning = 1;
+  int step_spanning = 2;  // plan.hpp build_pass_schedule modes
   int order = 1;  // 1: Lie-Trotter (D then X, R7); 2: Strang (half D, X, half D; NEXT F4)
   int ctas_per_sm = 1;
   int kernel_mode = 1;  // 1: TMA warp-specialised pass, 0: register-prefetch pass
@@ -265,7 +265,8 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       ctx->profile = value != 0;
       return QAA_OK;
     case QAA_OPT_STEP_SPANNING:
-      ctx->step_spanning = value != 0;
+      if (value < 0 || value > 2) return fail(ctx, QAA_E_USAGE, "step_spanning must be 0, 1 or 2");
+      ctx->step_spanning = (int)value;
       return QAA_OK;
     case QAA_OPT_ORDER:
       if (value != 1 && value != 2) return fail(ctx, QAA_E_USAGE, "splitting order must be 1 or 2");
@@ -1045,7 +1046,7 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
     if (tangent) return evolve_super(ctx, K, sc, dphi, n_phi);
   }
   std::vector<PassPlan> plan;
-  build_pass_schedule((int)ctx->geom.groups.size(), K, ctx->step_spanning != 0, &plan);
+  build_pass_schedule((int)ctx->geom.groups.size(), K, ctx->step_spanning, &plan);
   // Strang: the closing half step D_K follows the pass that completes X_{K-1}
   // (its program becomes rotate + D; it runs on the generic kernel)
   if (ctx->order == 2) plan.back().d_step = K;
@@ -1076,7 +1077,7 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
       else if (pre && d && post) fp = FP_G0_PRE_D_POST;
     } else if ((gr.rot_local & ~0xFF8u) == 0) {
       if (pre && !d && !post) fp = FP_GK_PRE;
-      else if (pre && d && post) fp = FP_GK_PRE_D_POST;
+      else if (d && post) fp = FP_GK_PRE_D_POST;  // without pre: its t0 row is all zeros
     }
     if ((pre && sc[(size_t)pp.pre_step].form != 0) || (post && sc[(size_t)pp.post_step].form != 0)) fp = -1;
     if (fp >= 0 && ctx->kernel_mode == 1 && ctx->tma_ok[(size_t)pp.group]) {
@@ -1590,7 +1591,7 @@ qaa_status qaa_plan_describe(int n_local, int row_bits, int step_spanning, int64
   std::string e;
   if (!build_geometry(n_local, row_bits, &g, &e)) return QAA_E_USAGE;
   std::vector<PassPlan> plan;
-  build_pass_schedule((int)g.groups.size(), K, step_spanning != 0, &plan);
+  build_pass_schedule((int)g.groups.size(), K, step_spanning, &plan);
   *count = (int64_t)plan.size();
   for (int64_t i = 0; i < (int64_t)plan.size() && i < cap; i++) {
     const PassPlan& pp = plan[(size_t)i];

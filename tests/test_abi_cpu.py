@@ -99,7 +99,7 @@ def simulate(rec, L, K):
 
 @pytest.mark.parametrize("L", [1, 5, 12, 13, 14, 16, 20, 21, 22, 24, 27, 30, 31, 33])
 @pytest.mark.parametrize("c", [3, 4])
-@pytest.mark.parametrize("span", [0, 1])
+@pytest.mark.parametrize("span", [0, 1, 2])
 def test_plan_covers_every_qubit_once_per_step(q, L, c, span):
     for K in (1, 2, 3, 7):
         rec = q.qaa_plan_describe(L, c, span, K)
@@ -111,10 +111,20 @@ def test_plan_covers_every_qubit_once_per_step(q, L, c, span):
 def test_plan_pass_counts(q, L, c, P):
     """P tile groups: K*(P-1)+1 passes with step spanning, K*P without."""
     K = 10
-    rec = q.qaa_plan_describe(L, c, 1, K)
-    assert len(set(int(g) for g in rec[:, 0])) == P
-    assert len(rec) == (K * (P - 1) + 1 if P > 1 else K)
+    for span in (1, 2):
+        rec = q.qaa_plan_describe(L, c, span, K)
+        assert len(set(int(g) for g in rec[:, 0])) == P
+        assert len(rec) == (K * (P - 1) + 1 if P > 1 else K)
     assert len(q.qaa_plan_describe(L, c, 0, K)) == K * P
+
+
+def test_plan_group0_never_hosts_d(q):
+    """Default schedule (mode 2): D only on strided groups, group 0 plain every step."""
+    for L in (22, 26, 30, 31, 33):
+        rec = q.qaa_plan_describe(L, 3, 2, 9)
+        assert all(int(r[0]) != 0 for r in rec if int(r[2]) >= 0)
+        g0 = [r for r in rec if int(r[0]) == 0]
+        assert len(g0) == 9 and all(int(r[1]) >= 0 and int(r[2]) < 0 for r in g0)
 
 
 def test_plan_register_programs_cost(q):

@@ -127,7 +127,7 @@ def test_resident_parity(q, ctx, orc, n):
 
 
 @pytest.mark.parametrize("n", [13, 14, 15, 16, 18, 21, 22, 23])
-@pytest.mark.parametrize("span", [1, 0])
+@pytest.mark.parametrize("span", [2, 1, 0])
 @pytest.mark.parametrize("variant", ["tma", "reg1", "reg2"])
 def test_pass_parity_small(q, ctx, orc, n, span, variant):
     ctx.set_option(q.OPT_KERNEL, 1 if variant == "tma" else 0)
@@ -355,7 +355,7 @@ def test_super_pass_parity(q, ctx, orc, n, sup, K):
 
 
 @pytest.mark.parametrize("n", [6, 12, 16, 22, 23])
-@pytest.mark.parametrize("span", [1, 0])
+@pytest.mark.parametrize("span", [2, 1, 0])
 @pytest.mark.parametrize("kernel", [1, 0])
 def test_strang_parity(q, ctx, orc, n, span, kernel):
     """NEXT F4: second-order Strang splitting (QAA_OPT_ORDER = 2) against the
