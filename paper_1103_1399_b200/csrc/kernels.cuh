@@ -71,7 +71,7 @@ struct FastArgs {
 cudaError_t launch_remap(const double2* src, double2* const* peers, int64_t N, int gshift, int rank, int num_sms,
                          cudaStream_t st);
 constexpr int FAST_XBUF = TILE + TILE / 16;  // padded exchange buffer (amplitudes)
-constexpr size_t FAST_SMEM_BYTES = sizeof(double2) * (FAST_XBUF + 256);
+constexpr size_t FAST_SMEM_BYTES = sizeof(double2) * (FAST_XBUF + 256 * 8);  // + 8 copies of the D table
 cudaError_t pass_fast_setup();
 cudaError_t launch_pass_fast(const FastArgs& a, int prog, bool lane3, bool prefetch, int grid, cudaStream_t st);
 
@@ -93,6 +93,9 @@ struct TmaArgs {
   int ndims;        // tensor-map rank (2..5) otherwise
   int dim_seg[5];   // per dim: -1 = tile dim (coordinate 0), else the tile-id segment giving the coordinate
 };
+// the TMA kernels keep 8 bank-group copies of the D table in shared memory:
+// they need E_max + 1 <= TMA_MAX_PHI (else the host uses the register kernels)
+constexpr int TMA_MAX_PHI = 64;
 cudaError_t pass_tma_setup();
 // L2-blocked D pass (pass_tma.cu qaa_superpass): group k rotate/D/rotate and
 // group 0 rotate over the same L2-resident chunk; see the comment there.

@@ -121,11 +121,11 @@ __device__ __forceinline__ void xchg(double2* xb, double2 (&v)[RPT], int lane, i
   __syncthreads();
 }
 
-__device__ __forceinline__ void diag(double2 (&v)[RPT], const uint32_t (&ep)[4], const double2* phis) {
+__device__ __forceinline__ void diag(double2 (&v)[RPT], const uint32_t (&ep)[4], const double2* phis, int lane) {
 #pragma unroll
   for (int r = 0; r < RPT; r++) {
     const int e = (ep[r >> 2] >> ((r & 3) * 8)) & 0xff;
-    const double2 f = phis[e];
+    const double2 f = phis[e * 8 + (lane & 7)];  // 8 bank-group copies: conflict-free lookup
     const double2 x = v[r];
     v[r] = make_double2(fma(f.x, x.x, -f.y * x.y), fma(f.x, x.y, f.y * x.x));
   }
@@ -144,7 +144,7 @@ __device__ __forceinline__ void program(const FastArgs& a, double2 (&v)[RPT], co
   const double(&t0)[TILE_BITS] = a.t[0];
   const double(&t1)[TILE_BITS] = a.t[1];
   if (PROG == FP_G0_DPOST) {
-    diag(v, ep, phis);
+    diag(v, ep, phis, lane);
     rot_regs<PA>(v, t1);
     xchg<PA, PC>(xb, v, lane, warp);
     rot_regs<PC>(v, t1);
@@ -162,7 +162,7 @@ __device__ __forceinline__ void program(const FastArgs& a, double2 (&v)[RPT], co
     rot_regs<PC>(v, t0);
     xchg<PC, PB>(xb, v, lane, warp);
     rot_regs<PB>(v, t0);
-    diag(v, ep, phis);
+    diag(v, ep, phis, lane);
     rot_regs<PB>(v, t1);
     xchg<PB, PC>(xb, v, lane, warp);
     rot_regs<PC>(v, t1);
@@ -178,7 +178,7 @@ __device__ __forceinline__ void program(const FastArgs& a, double2 (&v)[RPT], co
     xchg<PA, PB>(xb, v, lane, warp);
     rot_regs<PB>(v, t0);
     if (LANE3) rot_lane(v, 3, t0[3]);
-    diag(v, ep, phis);
+    diag(v, ep, phis, lane);
     rot_regs<PB>(v, t1);
     if (LANE3) rot_lane(v, 3, t1[3]);
     xchg<PB, PA>(xb, v, lane, warp);
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(NTHREADS, PREFETCH ? 1 : 2) qaa_pass_fast(cons
   using PI = ProgInfo<PROG>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (PI::has_d)
-    for (int e = tid; e < a.n_phi; e += NTHREADS) phis[e] = a.phi[e];
+    for (int e = tid; e < a.n_phi * 8; e += NTHREADS) phis[e] = a.phi[e >> 3];
   __syncthreads();
   const Off pa = make_off<PA>(a, lane, warp);
   const Off pe = make_off<PI::e_pat>(a, lane, warp);

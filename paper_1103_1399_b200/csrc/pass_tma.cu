@@ -25,6 +25,7 @@ namespace {
 constexpr int TMA_SLOTS = 3;
 constexpr int SLOT_BYTES = FAST_XBUF * 16;  // 69632: padded exchange layout
 constexpr int TMA_MAX_GROUPS = 2;
+constexpr int PHI_COPIES = 8;  // bank-group copies of the D table (diag below)
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -175,7 +176,10 @@ __device__ __forceinline__ void diag(double2 (&v)[RPT], const uint8_t* es, const
 #pragma unroll
   for (int r = 0; r < RPT; r++) {
     const int e = es[tl | (r << reg_shift<P>())];
-    const double2 f = phis[e];
+    // Phi is stored 8x interleaved (entry e of copy c at 8e + c): the 8 lanes of
+    // a quarter-warp read copies lane & 7, i.e. 8 distinct 16-byte bank groups,
+    // whatever their energies -- a conflict-free 128-bit lookup
+    const double2 f = phis[e * PHI_COPIES + (lane & (PHI_COPIES - 1))];
     const double2 x = v[r];
     v[r] = make_double2(fma(f.x, x.x, -f.y * x.y), fma(f.x, x.y, f.y * x.x));
   }
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_pass_tma(const __grid_co
   // full[NG*s + g]: slot s landed for consumer group g. Tile j uses slot j % 3
   // and group j % NG, so each (slot, group) barrier is used by every (3 NG)-th
   // tile, always by the same group, and a parity wait can never see a stale phase.
-  uint64_t* full = reinterpret_cast<uint64_t*>(phis + 256);
+  uint64_t* full = reinterpret_cast<uint64_t*>(phis + TMA_MAX_PHI * PHI_COPIES);
   using I = Info<PROG>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // tiles of this CTA: pairs (2m, 2m+1), m = blockIdx.x + i gridDim.x (ntiles is even)
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_pass_tma(const __grid_co
     for (int64_t j = 0; j < TMA_SLOTS && j < nt; j++) issue_tile<PROG, NG>(&tmap, a, j, slots, eslots, full);
   }
   if (I::has_d)
-    for (int e = tid; e < a.n_phi; e += NG * NTHREADS) phis[e] = a.phi[e];
+    for (int e = tid; e < a.n_phi * PHI_COPIES; e += NG * NTHREADS) phis[e] = a.phi[e / PHI_COPIES];
   __syncthreads();
   // NG consumer groups of 8 warps; the group that frees a slot refills it with
   // tile j + 3 -- no producer warp, so 16 warps x 128 registers fit the
@@ -488,7 +492,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
   double2* slots = reinterpret_cast<double2*>(sm);
   uint8_t* eslots = sm + TMA_SLOTS * SLOT_BYTES;
   double2* phis = reinterpret_cast<double2*>(eslots + TMA_SLOTS * TILE);
-  uint64_t* full = reinterpret_cast<uint64_t*>(phis + 256);
+  uint64_t* full = reinterpret_cast<uint64_t*>(phis + TMA_MAX_PHI * PHI_COPIES);
   uint64_t* late = full + NG * TMA_SLOTS;  // per group: deferred group-0 loads
   SlotMeta* meta = reinterpret_cast<SlotMeta*>(late + NG);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -498,7 +502,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int64_t J = 0; J < TMA_SLOTS; J++) super_issue<NG>(&kmap, a, J, slots, eslots, full, meta);
   }
-  for (int e = tid; e < a.gk.n_phi; e += NG * NTHREADS) phis[e] = a.gk.phi[e];
+  for (int e = tid; e < a.gk.n_phi * PHI_COPIES; e += NG * NTHREADS) phis[e] = a.gk.phi[e / PHI_COPIES];
   __syncthreads();
   const int g = warp >> 3, lw = warp & 7, gtid = tid & (NTHREADS - 1);
   const Off psk = make_off<PA>(a.gk, lane, lw);  // GK_PRE_D_POST stores in pattern PA
@@ -585,8 +589,9 @@ TmaKernel pick(int prog, bool lane3, int ng) { return ng == 1 ? pick_ng<1>(prog,
 
 }  // namespace
 
-constexpr size_t TMA_SMEM_BYTES = (size_t)TMA_SLOTS * SLOT_BYTES + (size_t)TMA_SLOTS * TILE + 256 * 16 +
-                                   TMA_MAX_GROUPS * TMA_SLOTS * 8 + TMA_MAX_GROUPS * 8 + TMA_SLOTS * 16;
+constexpr size_t TMA_SMEM_BYTES = (size_t)TMA_SLOTS * SLOT_BYTES + (size_t)TMA_SLOTS * TILE +
+                                   (size_t)TMA_MAX_PHI * PHI_COPIES * 16 + TMA_MAX_GROUPS * TMA_SLOTS * 8 +
+                                   TMA_MAX_GROUPS * 8 + TMA_SLOTS * 16;
 
 cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, int ngroups, int grid,
                              cudaStream_t st) {

@@ -846,7 +846,7 @@ static qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<Step
 // and the other group as "pre" of the next pass.
 static bool super_usable(qaa_ctx* ctx) {
   return ctx->super_mode && ctx->world == 1 && ctx->kernel_mode == 1 && ctx->geom.groups.size() == 3 &&
-         ctx->super_ok[1] && ctx->super_ok[2];
+         ctx->super_ok[1] && ctx->super_ok[2] && (int)ctx->emax + 1 <= TMA_MAX_PHI;
 }
 
 static qaa_status evolve_super(qaa_ctx* ctx, int64_t K, const std::vector<StepCoef>& sc, const double2* dphi,
@@ -1080,7 +1080,7 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
       else if (d && post) fp = FP_GK_PRE_D_POST;  // without pre: its t0 row is all zeros
     }
     if ((pre && sc[(size_t)pp.pre_step].form != 0) || (post && sc[(size_t)pp.post_step].form != 0)) fp = -1;
-    if (fp >= 0 && ctx->kernel_mode == 1 && ctx->tma_ok[(size_t)pp.group]) {
+    if (fp >= 0 && ctx->kernel_mode == 1 && ctx->tma_ok[(size_t)pp.group] && n_phi <= TMA_MAX_PHI) {
       TmaArgs ta = ctx->tma_static[(size_t)pp.group];
       ta.psi = ctx->state;
       ta.phi = d ? dphi + (size_t)pp.d_step * n_phi : nullptr;

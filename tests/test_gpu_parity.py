@@ -440,3 +440,16 @@ def test_empty_instance_large(q, ctx, orc):
     want = orc.evolve(n, orc.energy_table(n, []), psi0, 1.0, 4)
     assert_close(ctx.state(), want)
     assert abs(ctx.success_prob() - ctx.norm2()) < 1e-13
+
+
+def test_large_emax_falls_back(q, ctx, orc):
+    """E_max + 1 > TMA_MAX_PHI (64): the register kernels take over (same results)."""
+    n = 14
+    cl = [(1, 2, 3)] * 70 + cnf.random_instance(n, 30, 5)
+    ctx.load_instance(n, cl)
+    assert ctx.max_energy() >= 64
+    psi0 = cnf.random_state(n, 8)
+    ctx.set_state(psi0)
+    ctx.evolve(0.7, 4)
+    want = orc.evolve(n, orc.energy_table(n, cl), psi0, 0.7, 4)
+    assert_close(ctx.state(), want)

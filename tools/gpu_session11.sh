@@ -1,0 +1,4 @@
+set -x
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+timeout 200 python bench.py --steps 5 --warmup 2 --no-cpu-baseline --no-e2e > gpurun_out/b11.json 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 16 --csv --log-file gpurun_out/launches11.csv python bench.py --steps 1 --warmup 1 --chunk 6 --no-cpu-baseline --no-e2e > /dev/null 2>&1
