@@ -162,6 +162,25 @@ qaa_status qaa_sigma_x(qaa_ctx* ctx, double* out);
  * finite, K[r] < 1), STATE (no instance). */
 qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, double* out);
 
+/* Low spectrum of H(s) (the adiabatic-theorem diagnostic of
+ * P:66-67): Lanczos with full re-orthogonalisation on the matrix-free
+ * H(s) psi (same weights as evolve, incl. the driving term), from a fixed
+ * pseudo-random start vector, at most kmax iterations (stops early on an
+ * invariant subspace). evals[0..nev-1] = the nev smallest Ritz values (gap =
+ * evals[1] - evals[0]); if overlap != NULL, *overlap = |<g(s)|psi>|^2 /
+ * <psi|psi> with g(s) the ground Ritz vector and psi the current state; *iters
+ * (optional) = iterations used. Stores kmax+1 vectors of 2^n amplitudes.
+ * Synchronises. Errors: USAGE (s outside [0,1], kmax not in 2..512, nev not in
+ * 1..kmax), CAP (world > 1, n > 24, basis does not fit), STATE. */
+qaa_status qaa_spectrum(qaa_ctx* ctx, double s, int kmax, int nev, double* evals, double* overlap, int* iters);
+
+/* Driving term (the paper's unspecified "driving Hamiltonian",
+ * P:193, R3): from the next evolve/energy/sweep on, H(s) = (1-s) H_B + s H_P +
+ * s(1-s) (gx H_B + gz H_P), i.e. the step weights become (1-s) + gx s(1-s) for
+ * H_B and s + gz s(1-s) for H_P (energy(s) reports this H(s)). gx = gz = 0
+ * (default) is Eq. 1 exactly. Errors: USAGE (not finite). */
+qaa_status qaa_set_driver(qaa_ctx* ctx, double gx, double gz);
+
 /* Energy-table enumerator as a workload (the paper's own GPU
  * kernel): recompute the loaded instance's local table
  * E(x) `reps` times (after one warm-up) and return the average device time per

@@ -58,6 +58,22 @@ def trotter_product(n: int, diag, psi0, T: float, K: int, schedule=None) -> np.n
     return psi
 
 
+def driven_product(n: int, diag, psi0, T: float, K: int, gx: float, gz: float, schedule=None) -> np.ndarray:
+    """prod_k expm(-i dt wB_k H_B) expm(-i dt wP_k H_P) psi0 with wB = (1-s) + gx s(1-s),
+    wP = s + gz s(1-s): the Trotter product of H(s) + s(1-s)(gx H_B + gz H_P)."""
+    dt = T / K
+    HB = h_b(n)
+    HP = h_p(diag)
+    psi = np.array(psi0, dtype=np.complex128)
+    for k in range(K):
+        s = schedule[k] if schedule is not None else (k + 0.5) / K
+        wB = (1 - s) + gx * s * (1 - s)
+        wP = s + gz * s * (1 - s)
+        psi = scipy.linalg.expm(-1j * dt * wP * HP) @ psi
+        psi = scipy.linalg.expm(-1j * dt * wB * HB) @ psi
+    return psi
+
+
 def strang_product(n: int, diag, psi0, T: float, K: int, schedule=None) -> np.ndarray:
     """prod_k expm(-i dt s_k H_P / 2) expm(-i dt (1-s_k) H_B) expm(-i dt s_k H_P / 2) psi0."""
     dt = T / K

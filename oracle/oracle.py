@@ -37,10 +37,12 @@ def lib():
         L.oracle_init_uniform.argtypes = [ctypes.c_int, P]
         L.oracle_evolve.argtypes = [ctypes.c_int, P, P, ctypes.c_double, ctypes.c_int64, P]
         L.oracle_evolve_strang.argtypes = [ctypes.c_int, P, P, ctypes.c_double, ctypes.c_int64, P]
+        L.oracle_evolve_driven.argtypes = [ctypes.c_int, P, P, ctypes.c_double, ctypes.c_int64, P,
+                                           ctypes.c_double, ctypes.c_double]
         L.oracle_observables.argtypes = [ctypes.c_int, P, P, P]
         L.oracle_energy.argtypes = [ctypes.c_int, P, P, ctypes.c_double, P]
         for f in ("oracle_energy_table", "oracle_energy_at", "oracle_init_uniform", "oracle_evolve",
-                  "oracle_evolve_strang", "oracle_observables", "oracle_energy"):
+                  "oracle_evolve_strang", "oracle_evolve_driven", "oracle_observables", "oracle_energy"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -118,6 +120,20 @@ def evolve_strang(n: int, E: np.ndarray, psi: np.ndarray, T: float, K: int, sche
         assert sch.size == K
     _check(lib().oracle_evolve_strang(n, _ptr(E), _ptr(out), float(T), int(K),
                                       _ptr(sch) if sch is not None else None), "evolve_strang")
+    return out
+
+
+def evolve_driven(n: int, E: np.ndarray, psi: np.ndarray, T: float, K: int, gx: float, gz: float,
+                  schedule=None) -> np.ndarray:
+    """NEXT F4: Lie-Trotter steps of H(s) + s(1-s)(gx H_B + gz H_P) on a copy of psi."""
+    out = np.array(psi, dtype=np.complex128, copy=True, order="C")
+    E = np.ascontiguousarray(E, dtype=np.uint16)
+    sch = None
+    if schedule is not None:
+        sch = np.ascontiguousarray(schedule, dtype=np.float64)
+    _check(lib().oracle_evolve_driven(n, _ptr(E), _ptr(out), float(T), int(K),
+                                      _ptr(sch) if sch is not None else None, float(gx), float(gz)),
+           "evolve_driven")
     return out
 
 

@@ -179,6 +179,48 @@ int oracle_evolve_strang(int n, const uint16_t* E, double* psi, double T, int64_
   return ORACLE_OK;
 }
 
+/* NEXT F4 driving term (the paper's "driving Hamiltonian", form not
+ * given; R3): H(s) = (1-s) H_B + s H_P + s(1-s)(gx H_B + gz H_P).
+ * Step k: exp(-i dt wP H_P) then exp(-i dt wB H_B) with wP = s + gz s(1-s),
+ * wB = (1-s) + gx s(1-s), written out like O-6/O-7. */
+int oracle_evolve_driven(int n, const uint16_t* E, double* psi, double T, int64_t K, const double* sched,
+                         double gx, double gz) {
+  if (n < 1 || n > 40 || K < 1 || !(T >= 0.0) || !isfinite(T)) return ORACLE_E_USAGE;
+  const int64_t N = (int64_t)1 << n;
+  const double dt = T / (double)K;
+  for (int64_t k = 0; k < K; k++) {
+    double s = sched ? sched[k] : ((double)k + 0.5) / (double)K;
+    double wP = s + gz * s * (1.0 - s);
+    double wB = (1.0 - s) + gx * s * (1.0 - s);
+    /* D: psi[x] <- e^{-i dt wP E(x)} psi[x] */
+    for (int64_t x = 0; x < N; x++) {
+      double phi = dt * wP * (double)E[x];
+      double c = cos(phi), sn = -sin(phi);
+      double re = psi[2 * x], im = psi[2 * x + 1];
+      psi[2 * x] = c * re - sn * im;
+      psi[2 * x + 1] = c * im + sn * re;
+    }
+    /* X: beta = dt wB / 2 on every qubit, as in O-7 */
+    double beta = 0.5 * dt * wB;
+    double gr = cos(beta), gi = -sin(beta);
+    double Ar = gr * cos(beta), Ai = gi * cos(beta);
+    double Br = -gi * sin(beta), Bi = gr * sin(beta);
+    for (int j = 0; j < n; j++) {
+      int64_t bit = (int64_t)1 << j;
+      for (int64_t x = 0; x < N; x++) {
+        if (x & bit) continue;
+        int64_t y = x | bit;
+        double xr = psi[2 * x], xi = psi[2 * x + 1], yr = psi[2 * y], yi = psi[2 * y + 1];
+        psi[2 * x] = (Ar * xr - Ai * xi) + (Br * yr - Bi * yi);
+        psi[2 * x + 1] = (Ar * xi + Ai * xr) + (Br * yi + Bi * yr);
+        psi[2 * y] = (Br * xr - Bi * xi) + (Ar * yr - Ai * yi);
+        psi[2 * y + 1] = (Br * xi + Bi * xr) + (Ar * yi + Ai * yr);
+      }
+    }
+  }
+  return ORACLE_OK;
+}
+
 /* O-8 helpers: pairwise (recursive halving) summation of f over [lo, hi) in a
  * fixed order, so the error grows like log2(N) * eps rather than N * eps. */
 typedef double (*term_fn)(const void* ctx, int64_t x);

@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libqaa.so")
-SOURCES = ["qaa_api.cu", "kernels.cu", "pass_fast.cu", "pass_tma.cu", "plan.cpp"]
+SOURCES = ["qaa_api.cu", "kernels.cu", "pass_fast.cu", "pass_tma.cu", "spectrum.cu", "plan.cpp"]
 HEADERS = ["kernels.cuh", "plan.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

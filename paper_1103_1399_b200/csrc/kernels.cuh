@@ -134,6 +134,19 @@ struct ResidentArgs {
 };
 cudaError_t launch_resident(const ResidentArgs& a, cudaStream_t st);
 
+// Lanczos spectrum of H(s) (F3, spectrum.cu).
+struct LanczosArgs {
+  int n;
+  int num_sms;
+  const uint8_t* E;
+  double wb, wp;          // weights of H_B and H_P at s
+  int kmax, nev;
+  double2* basis;         // (kmax + 1) * 2^n vectors
+  double* scratch;        // >= 8 * num_sms doubles
+  const double2* state;   // for the ground-state overlap (may be null)
+};
+cudaError_t lanczos_spectrum(const LanczosArgs& p, cudaStream_t st, double* evals, double* overlap, int* iters);
+
 // Batched small-n sweep (F1): nrep independent evolutions of the uniform
 // state, one CTA each, replica r with K[r] steps whose table rows start at
 // row_off[r]; out[r] = P_succ.

@@ -72,6 +72,7 @@ struct qaa_ctx {
   int profile = 0;
   int step_spanning = 2;  // plan.hpp build_pass_schedule modes
   int order = 1;  // 1: Lie-Trotter (D then X, R7); 2: Strang (half D, X, half D; NEXT F4)
+  double drv_x = 0.0, drv_z = 0.0;  // driving term s(1-s)(g_x H_B + g_z H_P) (NEXT F4, R3)
   int ctas_per_sm = 1;
   int kernel_mode = 1;  // 1: TMA warp-specialised pass, 0: register-prefetch pass
   int tma_groups = 0;   // consumer groups per TMA CTA: 0 = auto (1 without D, 2 with D)
@@ -722,13 +723,20 @@ struct StepCoef {
 };
 }  // namespace
 
-// One row of the coefficient table: the X coefficient of step s (tan or cot of
-// beta = dt (1-s)/2) and Phi[e] = e^{-i theta e} * (X normalisation)^n. theta is
-// dt s for Lie-Trotter; Strang passes the merged half steps (R7, §4).
-static void build_step(double T, int64_t K, double s, double theta, int n, int n_phi, double2* phi_row,
+// Weights of H_B and H_P at s: Eq. 1 gives (1 - s, s); the optional driving
+// term s(1-s)(g_x H_B + g_z H_P) (NEXT F4, R3) adds s(1-s) g to each. With
+// g = 0 both are bit-identical to 1 - s and s.
+static double weight_b(const qaa_ctx* c, double s) { return (1.0 - s) + c->drv_x * s * (1.0 - s); }
+static double weight_p(const qaa_ctx* c, double s) { return s + c->drv_z * s * (1.0 - s); }
+
+// One row of the coefficient table: the X coefficient of a step whose H_B
+// weight is wb (tan or cot of beta = dt wb / 2) and Phi[e] = e^{-i theta e} *
+// (X normalisation)^n. theta is dt wP(s) for Lie-Trotter; Strang passes the
+// merged half steps (R7, §4).
+static void build_step(double T, int64_t K, double wb, double theta, int n, int n_phi, double2* phi_row,
                        StepCoef* sc) {
   const double dt = T / (double)K;
-  const double beta = 0.5 * dt * (1.0 - s);  // X: exp(-i beta (1 - sigma^x)) per qubit
+  const double beta = 0.5 * dt * wb;  // X: exp(-i beta (1 - sigma^x)) per qubit
   const double cb = std::cos(beta), sb = std::sin(beta);
   double mag;
   // tangent form (I + i t sigma^x), t = tan beta, whenever |t| <= 1e4: it is a
@@ -982,18 +990,18 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
   const double dtK = T / (double)K;
   for (int64_t k = 0; k < K; k++) {
     const double s = schedule ? schedule[k] : ((double)k + 0.5) / (double)K;  // R8 midpoint
-    double theta = dtK * s;
+    double theta = dtK * weight_p(ctx, s);
     if (ctx->order == 2) {  // Strang: D(s_{k-1})^{1/2} D(s_k)^{1/2} merged before X_k
       const double sp = k == 0 ? 0.0 : (schedule ? schedule[k - 1] : ((double)k - 0.5) / (double)K);
-      theta = 0.5 * dtK * (sp + s);
+      theta = 0.5 * dtK * (weight_p(ctx, sp) + weight_p(ctx, s));
     }
-    build_step(T, K, s, theta, ctx->n, n_phi, hphi + (size_t)k * n_phi, &sc[(size_t)k]);
+    build_step(T, K, weight_b(ctx, s), theta, ctx->n, n_phi, hphi + (size_t)k * n_phi, &sc[(size_t)k]);
     hcoef[k] = sc[(size_t)k].coef;
     hform[k] = sc[(size_t)k].form;
   }
   if (ctx->order == 2) {  // closing half step D(s_{K-1})^{1/2}, no X after it
     const double sl = schedule ? schedule[K - 1] : ((double)K - 0.5) / (double)K;
-    const double theta = 0.5 * dtK * sl;
+    const double theta = 0.5 * dtK * weight_p(ctx, sl);
     for (int e = 0; e < n_phi; e++)
       hphi[(size_t)K * n_phi + e] = make_double2(std::cos(theta * (double)e), -std::sin(theta * (double)e));
   }
@@ -1336,7 +1344,7 @@ qaa_status qaa_energy(qaa_ctx* ctx, double s, double* out) {
   if (st) return st;
   double hb = 0.0;
   for (int j = 0; j < ctx->n; j++) hb += 0.5 * (b[0] - sx[(size_t)j]);
-  *out = (1.0 - s) * hb + s * b[1];
+  *out = weight_b(ctx, s) * hb + weight_p(ctx, s) * b[1];
   return QAA_OK;
 }
 
@@ -1421,6 +1429,54 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps) {
   return QAA_OK;
 }
 
+qaa_status qaa_spectrum(qaa_ctx* ctx, double s, int kmax, int nev, double* evals, double* overlap, int* iters) {
+  CHECK_CTX();
+  if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "spectrum before load_instance");
+  if (!(s >= 0.0 && s <= 1.0)) return fail(ctx, QAA_E_USAGE, "s = %g outside [0, 1]", s);
+  if (kmax < 2 || kmax > 512 || nev < 1 || nev > kmax || !evals)
+    return fail(ctx, QAA_E_USAGE, "need 2 <= kmax <= 512, 1 <= nev <= kmax, evals != NULL");
+  if (ctx->world != 1 || ctx->L > 24) return fail(ctx, QAA_E_CAP, "spectrum: single GPU, n <= 24");
+  if (overlap && !ctx->initialized) return fail(ctx, QAA_E_STATE, "overlap needs an initialised state");
+  const size_t vec = ((size_t)1 << ctx->L) * sizeof(double2);
+  void* basis = nullptr;
+  cudaError_t e = cudaMalloc(&basis, vec * (size_t)(kmax + 1));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ctx, QAA_E_CAP, "Lanczos basis of %d vectors does not fit", kmax + 1);
+  }
+  qaa_status st = ensure_part(ctx, (size_t)ctx->num_sms * 8 + 16);
+  if (st) {
+    cudaFree(basis);
+    return st;
+  }
+  LanczosArgs p;
+  p.n = ctx->L;
+  p.num_sms = ctx->num_sms;
+  p.E = ctx->E;
+  p.wb = weight_b(ctx, s);
+  p.wp = weight_p(ctx, s);
+  p.kmax = kmax;
+  p.nev = nev;
+  p.basis = (double2*)basis;
+  p.scratch = ctx->d_part;
+  p.state = overlap ? ctx->state : nullptr;
+  int it = 0;
+  e = lanczos_spectrum(p, ctx->stream, evals, overlap, &it);
+  cudaFree(basis);
+  if (e != cudaSuccess) return fail(ctx, QAA_E_CUDA, "Lanczos failed: %s", cudaGetErrorString(e));
+  ctx->stats.kernel_launches_total += 4 * (int64_t)it * (it + 1);
+  if (iters) *iters = it;
+  return QAA_OK;
+}
+
+qaa_status qaa_set_driver(qaa_ctx* ctx, double gx, double gz) {
+  if (!ctx) return QAA_E_USAGE;
+  if (!std::isfinite(gx) || !std::isfinite(gz)) return fail(ctx, QAA_E_USAGE, "driver weights must be finite");
+  ctx->drv_x = gx;
+  ctx->drv_z = gz;
+  return QAA_OK;
+}
+
 qaa_status qaa_time_energy_table(qaa_ctx* ctx, int reps, double* ms) {
   CHECK_CTX();
   if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "time_energy_table before load_instance");
@@ -1488,16 +1544,17 @@ qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, 
     const double dt = T[r] / (double)K[r];
     for (int64_t k = 0; k < K[r]; k++) {
       const double s = ((double)k + 0.5) / (double)K[r];
-      double theta = dt * s;
-      if (ctx->order == 2) theta = 0.5 * dt * ((k == 0 ? 0.0 : ((double)k - 0.5) / (double)K[r]) + s);
+      double theta = dt * weight_p(ctx, s);
+      if (ctx->order == 2)
+        theta = 0.5 * dt * (weight_p(ctx, k == 0 ? 0.0 : ((double)k - 0.5) / (double)K[r]) + weight_p(ctx, s));
       StepCoef c;
-      build_step(T[r], K[r], s, theta, ctx->n, n_phi, hphi + (size_t)(row + k) * n_phi, &c);
+      build_step(T[r], K[r], weight_b(ctx, s), theta, ctx->n, n_phi, hphi + (size_t)(row + k) * n_phi, &c);
       hcoef[row + k] = c.coef;
       hform[row + k] = c.form;
     }
     row += K[r];
     if (ctx->order == 2) {
-      const double theta = 0.5 * dt * (((double)K[r] - 0.5) / (double)K[r]);
+      const double theta = 0.5 * dt * weight_p(ctx, ((double)K[r] - 0.5) / (double)K[r]);
       for (int e = 0; e < n_phi; e++)
         hphi[(size_t)row * n_phi + e] = make_double2(std::cos(theta * (double)e), -std::sin(theta * (double)e));
       hcoef[row] = 0.0;

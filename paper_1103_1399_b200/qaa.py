@@ -16,7 +16,7 @@ import numpy as np
 __all__ = [
     "QaaError", "Context", "lib", "library_path", "STATUS",
     "qaa_create", "qaa_destroy", "qaa_last_error", "qaa_load_instance", "qaa_init_uniform",
-    "qaa_init_basis", "qaa_evolve", "qaa_sweep", "qaa_time_energy_table", "qaa_success_prob", "qaa_energy", "qaa_norm2", "qaa_sigma_x",
+    "qaa_init_basis", "qaa_evolve", "qaa_sweep", "qaa_time_energy_table", "qaa_set_driver", "qaa_spectrum", "qaa_success_prob", "qaa_energy", "qaa_norm2", "qaa_sigma_x",
     "qaa_num_solutions", "qaa_max_energy", "qaa_copy_state", "qaa_set_state", "qaa_copy_energy_table",
     "qaa_state_ptr", "qaa_set_option", "qaa_get_stats", "qaa_reset_stats", "qaa_plan_describe",
     "qaa_version", "OPT_ROW_BITS", "OPT_PROFILE", "OPT_STEP_SPANNING", "OPT_CTAS_PER_SM", "OPT_KERNEL", "OPT_TMA_GROUPS", "OPT_SUPER", "OPT_ORDER",
@@ -39,7 +39,7 @@ EXPORTS = [
     "qaa_init_basis", "qaa_evolve", "qaa_success_prob", "qaa_energy", "qaa_norm2", "qaa_sigma_x",
     "qaa_num_solutions", "qaa_max_energy", "qaa_copy_state", "qaa_set_state", "qaa_copy_energy_table",
     "qaa_state_ptr", "qaa_set_option", "qaa_get_stats", "qaa_reset_stats", "qaa_plan_describe", "qaa_version",
-    "qaa_plan_describe_sharded", "qaa_sweep", "qaa_time_energy_table",
+    "qaa_plan_describe_sharded", "qaa_sweep", "qaa_time_energy_table", "qaa_set_driver", "qaa_spectrum",
 ]
 
 
@@ -149,6 +149,8 @@ def lib():
             "qaa_plan_describe_sharded": ([I, I, I, I64, P, I64, ctypes.POINTER(I64)], I),
             "qaa_sweep": ([P, I, P, P, P], I),
             "qaa_time_energy_table": ([P, I, ctypes.POINTER(D)], I),
+            "qaa_set_driver": ([P, D, D], I),
+            "qaa_spectrum": ([P, D, I, I, P, ctypes.POINTER(D), ctypes.POINTER(I)], I),
             "qaa_version": ([], ctypes.c_char_p),
         }
         for name, (args, res) in sig.items():
@@ -259,6 +261,21 @@ def qaa_sweep(ctx, T, K) -> np.ndarray:
     out = np.zeros(Ta.size, dtype=np.float64)
     _check(ctx, lib().qaa_sweep(ctx, int(Ta.size), _dptr(Ta), _dptr(Ka), _dptr(out)))
     return out
+
+
+def qaa_spectrum(ctx, s: float, kmax: int = 64, nev: int = 3, overlap: bool = False):
+    """F3: (nev smallest Ritz values of H(s), ground-state overlap or None, iterations)."""
+    ev = np.zeros(nev, dtype=np.float64)
+    ov = ctypes.c_double()
+    it = ctypes.c_int()
+    _check(ctx, lib().qaa_spectrum(ctx, float(s), int(kmax), int(nev), _dptr(ev),
+                                   ctypes.byref(ov) if overlap else None, ctypes.byref(it)))
+    return ev, (ov.value if overlap else None), it.value
+
+
+def qaa_set_driver(ctx, gx: float, gz: float):
+    """F4 driving term s(1-s)(gx H_B + gz H_P) added to Eq. 1."""
+    _check(ctx, lib().qaa_set_driver(ctx, float(gx), float(gz)))
 
 
 def qaa_time_energy_table(ctx, reps: int = 5) -> float:
@@ -419,6 +436,12 @@ class Context:
 
     def sigma_x(self):
         return qaa_sigma_x(self.ctx, self.n)
+
+    def spectrum(self, s, kmax=64, nev=3, overlap=False):
+        return qaa_spectrum(self.ctx, s, kmax, nev, overlap)
+
+    def set_driver(self, gx, gz):
+        qaa_set_driver(self.ctx, gx, gz)
 
     def time_energy_table(self, reps=5):
         return qaa_time_energy_table(self.ctx, reps)

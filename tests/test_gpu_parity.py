@@ -453,3 +453,61 @@ def test_large_emax_falls_back(q, ctx, orc):
     ctx.evolve(0.7, 4)
     want = orc.evolve(n, orc.energy_table(n, cl), psi0, 0.7, 4)
     assert_close(ctx.state(), want)
+
+
+@pytest.mark.parametrize("n", [8, 16, 22])
+@pytest.mark.parametrize("g", [(0.7, 0.0), (1.2, -0.5)])
+def test_driver_parity(q, ctx, orc, n, g):
+    """NEXT F4 driving term s(1-s)(gx H_B + gz H_P) against the oracle; energy(s)
+    reports the driven H(s)."""
+    cl = instance(n)
+    ctx.load_instance(n, cl)
+    ctx.set_driver(*g)
+    psi0 = cnf.random_state(n, 5)
+    ctx.set_state(psi0)
+    sched = np.random.default_rng(n).uniform(0, 1, 5)
+    ctx.evolve(1.9, 5, sched)
+    E = orc.energy_table(n, cl)
+    want = orc.evolve_driven(n, E, psi0, 1.9, 5, g[0], g[1], sched)
+    assert_close(ctx.state(), want)
+    s = 0.35
+    wb, wp = (1 - s) + g[0] * s * (1 - s), s + g[1] * s * (1 - s)
+    ob = orc.observables(n, E, want)
+    hb = sum(0.5 * (ob["norm2"] - sx) for sx in ob["sigma_x"])
+    assert abs(ctx.energy(s) - (wb * hb + wp * ob["hp"])) < 1e-11
+    ctx.set_driver(0.0, 0.0)
+
+
+@pytest.mark.parametrize("n", [6, 8, 10])
+@pytest.mark.parametrize("s", [0.0, 0.3, 0.62, 1.0])
+def test_spectrum_vs_dense(q, ctx, n, s):
+    """NEXT F3: Lanczos Ritz values of the matrix-free H(s) against numpy's dense
+    eigvalsh of H(s) built from Kronecker products (oracle/dense.py) with H_P from
+    brute force; Lanczos from one start vector sees each distinct eigenvalue once."""
+    from oracle import dense
+    from qaa_testutil import brute_force_energy
+    cl = cnf.paper_instance()[1] if n == 6 else instance(n)
+    ctx.load_instance(n, cl)
+    ev, _, it = ctx.spectrum(s, kmax=min(1 << n, 160), nev=3)
+    w = np.linalg.eigvalsh(dense.h_s(n, brute_force_energy(n, cl), s))
+    distinct = [w[0]]
+    for x in w[1:]:
+        if x - distinct[-1] > 1e-8:
+            distinct.append(x)
+    assert np.allclose(ev, distinct[:3], atol=1e-9, rtol=0), (ev, distinct[:3], it)
+
+
+def test_spectrum_closed_forms_and_overlap(q, ctx):
+    """s = 0: H_B has eigenvalues 0, 1, 2 and psi0 is its ground state
+    (overlap 1); s = 1: H_P's lowest levels are the two smallest energies."""
+    n = 16
+    cl, sol = cnf.load_instance(n)
+    ctx.load_instance(n, cl)
+    ctx.init_uniform()
+    ev, ov, _ = ctx.spectrum(0.0, kmax=60, nev=3, overlap=True)
+    assert np.allclose(ev, [0.0, 1.0, 2.0], atol=1e-9)
+    assert abs(ov - 1.0) < 1e-9
+    ev1, _, _ = ctx.spectrum(1.0, kmax=80, nev=2)
+    E = ctx.energy_table().astype(int)
+    levels = sorted(set(E.tolist()))[:2]
+    assert np.allclose(ev1, levels, atol=1e-9)

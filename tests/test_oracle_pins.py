@@ -315,3 +315,25 @@ def test_strang_second_order_convergence(oracle_mod):
     errs = [np.max(np.abs(oracle_mod.evolve_strang(n, E, psi0, 10.0, K) - ref)) for K in (50, 100, 200)]
     r1, r2 = errs[0] / errs[1], errs[1] / errs[2]
     assert 3.5 < r1 < 4.5 and 3.5 < r2 < 4.5, errs
+
+
+# --------------------------------------------------------------------------- NEXT F4: driving term
+@pytest.mark.parametrize("gx,gz", [(0.7, 0.0), (0.0, -0.4), (1.3, 0.9)])
+def test_driven_vs_dense(oracle_mod, gx, gz):
+    n, cl = cnf.paper_instance()
+    E = oracle_mod.energy_table(n, cl)
+    psi0 = cnf.random_state(n, 4)
+    sched = np.random.default_rng(2).uniform(0, 1, 12)
+    got = oracle_mod.evolve_driven(n, E, psi0, 5.0, 12, gx, gz, sched)
+    want = dense.driven_product(n, brute_force_energy(n, cl), psi0, 5.0, 12, gx, gz, sched)
+    assert np.max(np.abs(got - want)) < 1e-13
+
+
+def test_driven_zero_is_eq1(oracle_mod):
+    """g = 0 reduces the driven step to Eq. 1 exactly (same arithmetic path values)."""
+    n, cl = cnf.paper_instance()
+    E = oracle_mod.energy_table(n, cl)
+    psi0 = cnf.random_state(n, 6)
+    a = oracle_mod.evolve_driven(n, E, psi0, 3.0, 9, 0.0, 0.0)
+    b = oracle_mod.evolve(n, E, psi0, 3.0, 9)
+    assert np.max(np.abs(a - b)) < 1e-15
