@@ -45,14 +45,15 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--qubits", dest="n", type=int, default=None, help="qubits n (default 30 + log2(gpus))")
-    ap.add_argument("--chunk", type=int, default=20, help="Trotter steps per bench step")
+    ap.add_argument("--chunk", type=int, default=100, help="Trotter steps per bench step")
     ap.add_argument("--row-bits", type=int, default=3)
     ap.add_argument("--step-spanning", type=int, default=2,
                     help="2 = D only on strided groups (default), 1 = cyclic, 0 = no spanning")
     ap.add_argument("--ctas-per-sm", type=int, default=1)
     ap.add_argument("--kernel", type=int, default=1, help="1 = TMA warp-specialised pass, 0 = register pass")
     ap.add_argument("--tma-groups", type=int, default=0, help="0 = auto, 1 or 2 consumer groups per TMA CTA")
-    ap.add_argument("--super", type=int, default=0, help="QAA_OPT_SUPER bits (1 = L2-blocked D passes, experimental)")
+    ap.add_argument("--super", type=int, default=1,
+                    help="QAA_OPT_SUPER bits (1 = L2-blocked Trotter steps, default; 0 = two HBM passes per step)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=26)
@@ -252,30 +253,47 @@ def run_ours(args):
         ms = float(t.item())
     trotter = args.steps * chunk
     value = trotter / (ms / 1e3)
-    # roofline of the dominant kernel (qaa_pass_kernel): algorithmic bytes per
-    # launch = 32 B/amp (read + write psi) + 1 B/amp (E) on D passes.
+    # roofline of the dominant kernel: algorithmic bytes per launch = 32 B/amp
+    # (read + write psi) + 1 B/amp (E) on D launches. With L2-blocked steps
+    # (default) the dominant kernel is qaa_superpass: one launch = one Trotter
+    # step = one HBM round trip (33 B/amp); the first/last passes of each evolve
+    # call are plain qaa_pass_tma launches.
     L = st["n_local"]
     amps = 1 << L
     npass = st["pass_launches"]
     n_d = trotter  # one D per Trotter step
-    alg_bytes = npass * 32 * amps + n_d * amps
-    kernel_ms = st["pass_kernel_ms"]
-    achieved = alg_bytes / (kernel_ms / 1e3) / 1e9 if kernel_ms > 0 else None
     peaks = measured_peaks()
     peak = peaks.get("hbm_gbs", 6650.0)
+    clocks = clk.summary()
+    if st["super_launches"] > 0 and st["super_kernel_ms"] > 0:
+        kname, nl, kms = "qaa_superpass", st["super_launches"], st["super_kernel_ms"]
+        alg_bytes = nl * 33 * amps
+    else:
+        kname = "qaa_pass_tma" if (args.kernel == 1 and world == 1) else "qaa_pass_fast"
+        nl, kms = npass, st["pass_kernel_ms"]
+        alg_bytes = npass * 32 * amps + n_d * amps
+    achieved = alg_bytes / (kms / 1e3) / 1e9 if kms > 0 else None
     tr = traffic_from_profiles()
     traffic = None
-    if tr and tr.get("n") == n and tr.get("bytes_per_launch"):
+    if tr and tr.get("n") == n and tr.get("kernel") == kname and tr.get("bytes_per_launch"):
         traffic = tr["bytes_per_launch"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "kernel": "qaa_pass_tma" if (args.kernel == 1 and world == 1) else "qaa_pass_fast",
-                "launches": npass,
-                "avg_launch_ms": kernel_ms / max(npass, 1),
-                "alg_bytes_per_launch": alg_bytes / max(npass, 1),
-                "kernel_share_of_step": kernel_ms / ms if ms > 0 else None,
+                "kernel": kname, "launches": nl,
+                "avg_launch_ms": kms / max(nl, 1),
+                "alg_bytes_per_launch": alg_bytes / max(nl, 1),
+                "kernel_share_of_step": kms / ms if ms > 0 else None,
+                "all_pass_launches": npass, "all_pass_kernel_ms": st["pass_kernel_ms"],
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback B200_PROFILING.md"}
-    clocks = clk.summary()
+    if kname == "qaa_superpass":
+        # one HBM round trip per step: the launch is bound on chip by the SM's
+        # shared-memory/L1 data path (128 B/clk/SM), 273 B/amp per launch
+        sm_hz = (clocks.get("sm_mhz") or 1965.0) * 1e6
+        onchip_peak = 128 * 148 * sm_hz / 1e9
+        onchip = 273 * amps / (kms / nl / 1e3) / 1e9
+        roofline["onchip"] = {"bound": "smem/L1 data path", "bytes_per_amp": 273, "achieved": onchip,
+                              "peak": onchip_peak, "unit": "GB/s", "frac": onchip / onchip_peak,
+                              "peak_source": "128 B/clk/SM x 148 SMs x median SM clock under load"}
     gpu_launches = st["kernel_launches_total"]
     ctx.close()  # free the shard buffers before the e2e context allocates its own
 

@@ -232,12 +232,14 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *  QAA_OPT_TMA_GROUPS    consumer groups (8 warps each) per TMA CTA: 0 = auto (1 for
  *                        passes without D: two tiles in flight; 2 for D passes: two
  *                        groups overlap their transposes and FMAs), or force 1 / 2.
- *  QAA_OPT_SUPER         bit 0 (default 0, experimental): L2-blocked D passes when the plan
- *                        has three tile groups (22 <= n <= 30 on one GPU): each Trotter step
- *                        is one HBM round trip (group k and group 0 processed chunk by chunk
- *                        in L2; parity-tested, but slower than the default two-pass plan in
- *                        round 1); bit 1: two consumer groups (known to stall); bit 2: no
- *                        L2 prefetch.
+ *  QAA_OPT_SUPER         bit 0 (default 1): L2-blocked Trotter steps when the plan has three
+ *                        tile groups (22 <= n <= 30 on one GPU) and schedule mode 2: each pass
+ *                        pair [group 0 rotate][group k rotate, D, rotate] runs as ONE launch
+ *                        over 32 MiB chunks resident in L2, one HBM round trip per step
+ *                        (K + 2 launches for K steps); bit 1: one consumer group per CTA
+ *                        (default two); bits 2-3: L2 eviction hints (0 = evict-last for the
+ *                        group-0 output read back by the group-k sub-pass and evict-first
+ *                        for dead data; 1 = no hints; 2 = evict-first only).
  *  QAA_OPT_ORDER         1 (default) = first-order Lie-Trotter, D then X (R7);
  *                        2 = second-order Strang splitting, D^{1/2} X D^{1/2} per step, at
  *                        the same HBM cost (the half D's of adjacent steps are merged, the
@@ -266,6 +268,9 @@ typedef struct {
   int64_t amps_local;
   int n, n_local, groups, tile_bits, row_bits;
   int64_t kernel_launches_total; /* every kernel this context launched since reset */
+  int64_t super_launches;    /* of pass_launches: L2-blocked launches (QAA_OPT_SUPER) */
+  double super_kernel_ms;    /* of pass_kernel_ms: their event-timed durations */
+  int64_t super_kernels_timed;
 } qaa_stats;
 qaa_status qaa_get_stats(qaa_ctx* ctx, qaa_stats* out);
 qaa_status qaa_reset_stats(qaa_ctx* ctx);

@@ -97,17 +97,17 @@ struct TmaArgs {
 // they need E_max + 1 <= TMA_MAX_PHI (else the host uses the register kernels)
 constexpr int TMA_MAX_PHI = 64;
 cudaError_t pass_tma_setup();
-// L2-blocked D pass (pass_tma.cu qaa_superpass): group k rotate/D/rotate and
-// group 0 rotate over the same L2-resident chunk; see the comment there.
+// L2-blocked Trotter step (pass_tma.cu qaa_superpass): group 0 rotate, then
+// group k rotate/D/rotate, over the same L2-resident chunk; see the comment there.
 struct SuperArgs {
   TmaArgs gk;          // group k: t[0] = step j, t[1] = step j+1; phi/n_phi = D_{j+1}; Eg = its energy slices
-  TmaArgs g0;          // group 0 (contiguous tiles): t[0] = step j+1
+  TmaArgs g0;          // group 0 (contiguous tiles): t[0] = step j
   int64_t nchunks;
   int tpc_bits;        // tiles per chunk per sub-pass = 2^tpc_bits
   uint32_t k_imask, k_cmask;  // group-k tile id = pdep(i, k_imask) | pdep(c, k_cmask)
   uint32_t z_imask, z_cmask;  // group-0 tile id
-  int prefetch;        // bulk-prefetch each chunk's group-0 tiles into L2 first
-  unsigned* done;      // [nchunks] group-k tiles stored per chunk (zeroed before launch)
+  int hints;           // L2 eviction hints: 0 none, 1 evict-first for dead data, 2 + evict-last for group-0 output
+  unsigned* done;      // [nchunks] group-0 tiles stored per chunk (zeroed before launch)
   unsigned long long* queue;  // global work counter (zeroed before launch)
 };
 cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, int ngroups, int grid,

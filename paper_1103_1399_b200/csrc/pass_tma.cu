@@ -84,6 +84,69 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, cons
       break;
   }
 }
+// L2 eviction-priority hints (createpolicy + .L2::cache_hint), used by the
+// L2-blocked pass to keep the chunk data that is read again and stream out the rest
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(sa(dst)),
+      "l"(src), "r"(bytes), "r"(sa(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_hint(void* dst, const CUtensorMap* map, const int (&c)[5], int rank,
+                                              uint64_t* bar, uint64_t pol) {
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  switch (rank) {
+    case 2:
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+          "[%1, {%2, %3}], [%4], %5;" ::"r"(sa(dst)),
+          "l"(m), "r"(c[0]), "r"(c[1]), "r"(sa(bar)), "l"(pol)
+          : "memory");
+      break;
+    case 3:
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+          "[%1, {%2, %3, %4}], [%5], %6;" ::"r"(sa(dst)),
+          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(sa(bar)), "l"(pol)
+          : "memory");
+      break;
+    case 4:
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+          "[%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(sa(dst)),
+          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(sa(bar)), "l"(pol)
+          : "memory");
+      break;
+    default:
+      asm volatile(
+          "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+          "[%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(sa(dst)),
+          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(sa(bar)), "l"(pol)
+          : "memory");
+      break;
+  }
+}
+__device__ __forceinline__ void st_hint(double2* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void group_bar(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(NTHREADS) : "memory");
@@ -324,22 +387,25 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_pass_tma(const __grid_co
 }
 
 // ============================================================================
-// L2-blocked D pass ("super-pass"): group k (rotate step j, D_{j+1}, rotate
-// step j+1) and group 0 (rotate step j+1) over the same data, chunk by chunk.
+// L2-blocked Trotter step ("super-pass"): group 0 (rotate step j) and then
+// group k (rotate step j, D_{j+1}, rotate step j+1) over the same L2-resident
+// chunk -- exactly the pass pair [G0 pre j][Gk pre j, D_{j+1}, post j+1] of the
+// schedule-mode-2 plan, fused into one HBM round trip.
 // A chunk fixes every physical bit outside (group 0 u group k) tile bits, so
-// its 2^(tpc_bits) group-k tiles and 2^(tpc_bits) group-0 tiles cover the same
-// 2^(12+tpc_bits) amplitudes (32 MiB at n = 30): the group-0 tiles of a chunk
-// are bulk-prefetched into L2 (contiguous 64 KiB reads), the group-k sub-pass
-// runs out of L2, then the group-0 sub-pass, whose dirty lines leave L2 as
-// contiguous write-backs. One HBM round trip per Trotter step instead of two.
+// its 2^tpc_bits group-0 tiles and 2^tpc_bits group-k tiles cover the same
+// 2^(12+tpc_bits) amplitudes (32 MiB at n = 30). Group-0 tiles come from HBM
+// as contiguous 64 KiB bulk copies and are written back into L2; the group-k
+// tiles of the chunk (128-byte strided rows) then hit L2, and their dirty
+// lines leave L2 as write-backs.
 //
-// Work is a global queue, per chunk c: P(c) prefetch items, G(c) group-k
-// tiles, then Z(c-1) group-0 tiles of the previous chunk, so a group-0 tile of
-// chunk c is fetched >= 2^tpc_bits items after the last group-k tile of c.
-// Dependency: a group-0 tile of chunk c needs every group-k tile of c stored
-// (done[c] == 2^tpc_bits). The issuing thread never waits: if the dependency is
-// not met yet, the slot is marked "deferred" and the owning group -- which by
-// queue order holds no item that c still needs -- waits and loads it itself.
+// Work is one global queue: A(0), then for c = 0..nch-1: [A(c+1)] B(c), where
+// A(c) = the group-0 tiles of chunk c and B(c) = its group-k tiles. B(c) needs
+// every A(c) tile stored (done[c] == 2^tpc_bits); the one-segment lag keeps two
+// chunks live in L2. The issuing thread never waits: an unmet dependency marks
+// the slot "deferred", and the owning group -- whose own later items were all
+// fetched after it, so hold nothing chunk c needs -- waits and loads it itself.
+// A group's items are fetched in order (item J is fetched when J-3 is freed,
+// and J-3, J-1 belong to the same group), so its first END is its last item.
 // ============================================================================
 __device__ __forceinline__ uint32_t pdep32(uint32_t x, uint32_t mask) {
   uint32_t r = 0;
@@ -350,16 +416,16 @@ __device__ __forceinline__ uint32_t pdep32(uint32_t x, uint32_t mask) {
   return r;
 }
 
-enum SuperKind : int { SK_END = 0, SK_GK = 1, SK_G0 = 2, SK_G0_DEFERRED = 3 };
+enum SuperKind : int { SK_END = 0, SK_A = 1, SK_B = 2, SK_B_DEFERRED = 3 };
 
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 // bounded wait: a lost arrival becomes a trap (launch error) instead of a hang
 __device__ __forceinline__ void mbar_wait_bounded(uint64_t* b, uint32_t parity) {
@@ -380,47 +446,28 @@ __device__ __forceinline__ void mbar_arrive_notx(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(b)) : "memory");
 }
 
-// queue position q -> (kind, chunk, intra index); returns false past the end
+// queue position q -> (kind, chunk, intra index); false past the end
 __device__ __forceinline__ bool decode_item(const SuperArgs& a, unsigned long long q, int* kind, int64_t* c,
                                             uint32_t* i) {
   const unsigned long long tpc = 1ull << a.tpc_bits;
-  const unsigned long long per = (a.prefetch ? 3ull : 2ull) * tpc;  // items per chunk segment
-  const unsigned long long total = (unsigned long long)a.nchunks * per + tpc;
-  if (q >= total) return false;
-  const unsigned long long seg = q / per, r = q % per;
-  // segment seg: [P(seg)] G(seg) Z(seg - 1); the last segment holds only Z(nchunks-1)
-  if ((int64_t)seg >= a.nchunks) {
-    *kind = SK_G0;
-    *c = a.nchunks - 1;
-    *i = (uint32_t)r;
-    return true;
-  }
-  unsigned long long rr = r;
-  if (a.prefetch) {
-    if (rr < tpc) {
-      *kind = -1;  // prefetch
-      *c = (int64_t)seg;
-      *i = (uint32_t)rr;
-      return true;
-    }
-    rr -= tpc;
-  }
-  if (rr < tpc) {
-    *kind = SK_GK;
-    *c = (int64_t)seg;
-    *i = (uint32_t)rr;
-    return true;
-  }
-  rr -= tpc;
-  if (seg == 0) {  // no Z(-1): treat as a prefetch-like no-op
-    *kind = -2;
+  const unsigned long long nch = (unsigned long long)a.nchunks;
+  if (q >= 2 * nch * tpc) return false;
+  if (q < tpc) {
+    *kind = SK_A;
     *c = 0;
-    *i = 0;
+    *i = (uint32_t)q;
     return true;
   }
-  *kind = SK_G0;
-  *c = (int64_t)seg - 1;
-  *i = (uint32_t)rr;
+  const unsigned long long r0 = q - tpc, u = r0 / (2 * tpc), r = r0 % (2 * tpc);
+  if (u + 1 < nch && r < tpc) {
+    *kind = SK_A;
+    *c = (int64_t)(u + 1);
+    *i = (uint32_t)r;
+  } else {
+    *kind = SK_B;
+    *c = (int64_t)u;
+    *i = (uint32_t)(u + 1 < nch ? r - tpc : r);
+  }
   return true;
 }
 
@@ -431,56 +478,52 @@ struct SlotMeta {
   int pad;
 };
 
-// fetch the next work item for slot s (tile J of this CTA) and start its load
-template <int NG>
-__device__ void super_issue(const CUtensorMap* kmap, const SuperArgs& a, int64_t J, double2* slots, uint8_t* eslots,
-                            uint64_t* full, SlotMeta* meta) {
-  const int s = (int)(J % TMA_SLOTS);
-  uint64_t* fb = &full[NG * s + (int)(J % NG)];
-  int kind;
-  int64_t c;
-  uint32_t i;
-  while (true) {
-    const unsigned long long q = atomicAdd(a.queue, 1ull);
-    if (!decode_item(a, q, &kind, &c, &i)) {
-      meta[s] = SlotMeta{SK_END, 0, 0, 0};
-      mbar_arrive_notx(fb);
-      return;
-    }
-    if (kind == -1) {  // L2 prefetch of a group-0 tile of chunk c (contiguous 64 KiB)
-      const uint32_t T0 = pdep32(i, a.z_imask) | pdep32((uint32_t)c, a.z_cmask);
-      prefetch_l2(a.g0.psi + tbase(a.g0, T0), TILE * 16u);
-      continue;
-    }
-    if (kind == -2) continue;
-    break;
-  }
-  if (kind == SK_GK) {
-    const uint32_t T = pdep32(i, a.k_imask) | pdep32((uint32_t)c, a.k_cmask);
-    meta[s] = SlotMeta{SK_GK, (int)c, T, 0};
-    mbar_expect_tx(fb, TILE * 16u + (uint32_t)TILE);
+// group-k tile T (tensor-map rows) and its energy slice, completing on bar
+__device__ __forceinline__ void load_gk(const CUtensorMap* kmap, const SuperArgs& a, uint32_t T, double2* dst,
+                                       uint8_t* edst, uint64_t* bar, uint64_t pol) {
+  mbar_expect_tx(bar, TILE * 16u + (uint32_t)TILE);
+  if (a.gk.contiguous) {
+    bulk_g2s_hint(dst, a.gk.psi + tbase(a.gk, T), TILE * 16u, bar, pol);
+  } else {
     int cc[5];
 #pragma unroll
     for (int d = 0; d < 5; d++) {
       const int sg = a.gk.dim_seg[d];
       cc[d] = sg < 0 ? 0 : (int)((T >> a.gk.seg_src[sg]) & ((1u << a.gk.seg_len[sg]) - 1));
     }
-    double2* dst = slots + (size_t)s * FAST_XBUF;
-    if (a.gk.contiguous)
-      bulk_g2s(dst, a.gk.psi + tbase(a.gk, T), TILE * 16u, fb);
-    else
-      tma_load(dst, kmap, cc, a.gk.ndims, fb);
-    bulk_g2s(eslots + (size_t)s * TILE, a.gk.Eg + (int64_t)T * TILE, TILE, fb);
+    tma_load_hint(dst, kmap, cc, a.gk.ndims, bar, pol);
+  }
+  bulk_g2s_hint(edst, a.gk.Eg + (int64_t)T * TILE, TILE, bar, pol);
+}
+
+// fetch the next work item for slot J % 3 (tile J of this CTA) and start its load
+template <int NG>
+__device__ void super_issue(const CUtensorMap* kmap, const SuperArgs& a, int64_t J, double2* slots, uint8_t* eslots,
+                            uint64_t* full, SlotMeta* meta, uint64_t pol_dead) {
+  const int s = (int)(J % TMA_SLOTS);
+  uint64_t* fb = &full[NG * s + (int)(J % NG)];
+  int kind;
+  int64_t c;
+  uint32_t i;
+  if (!decode_item(a, atomicAdd(a.queue, 1ull), &kind, &c, &i)) {
+    meta[s] = SlotMeta{SK_END, 0, 0, 0};
+    mbar_arrive_notx(fb);
     return;
   }
-  const uint32_t T0 = pdep32(i, a.z_imask) | pdep32((uint32_t)c, a.z_cmask);
-  if (ld_acquire(&a.done[c]) >= (1u << a.tpc_bits)) {
-    fence_async_global();
-    meta[s] = SlotMeta{SK_G0, (int)c, T0, 0};
+  if (kind == SK_A) {
+    const uint32_t T = pdep32(i, a.z_imask) | pdep32((uint32_t)c, a.z_cmask);
+    meta[s] = SlotMeta{SK_A, (int)c, T, 0};
     mbar_expect_tx(fb, TILE * 16u);
-    bulk_g2s(slots + (size_t)s * FAST_XBUF, a.g0.psi + tbase(a.g0, T0), TILE * 16u, fb);
+    bulk_g2s_hint(slots + (size_t)s * FAST_XBUF, a.g0.psi + tbase(a.g0, T), TILE * 16u, fb, pol_dead);
+    return;
+  }
+  const uint32_t T = pdep32(i, a.k_imask) | pdep32((uint32_t)c, a.k_cmask);
+  if (ld_acquire(&a.done[c]) >= (1u << a.tpc_bits)) {
+    fence_async_global();  // generic-proxy stores of chunk c -> this async-proxy read
+    meta[s] = SlotMeta{SK_B, (int)c, T, 0};
+    load_gk(kmap, a, T, slots + (size_t)s * FAST_XBUF, eslots + (size_t)s * TILE, fb, pol_dead);
   } else {
-    meta[s] = SlotMeta{SK_G0_DEFERRED, (int)c, T0, 0};
+    meta[s] = SlotMeta{SK_B_DEFERRED, (int)c, T, 0};
     mbar_arrive_notx(fb);
   }
 }
@@ -493,14 +536,18 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
   uint8_t* eslots = sm + TMA_SLOTS * SLOT_BYTES;
   double2* phis = reinterpret_cast<double2*>(eslots + TMA_SLOTS * TILE);
   uint64_t* full = reinterpret_cast<uint64_t*>(phis + TMA_MAX_PHI * PHI_COPIES);
-  uint64_t* late = full + NG * TMA_SLOTS;  // per group: deferred group-0 loads
+  uint64_t* late = full + NG * TMA_SLOTS;  // per group: deferred group-k loads
   SlotMeta* meta = reinterpret_cast<SlotMeta*>(late + NG);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // hints: data read once more in this launch (group-0 output) stays, the rest
+  // (the loaded tiles, group-k output, energy slices) is marked evict-first
+  const uint64_t pol_dead = a.hints ? policy_evict_first() : policy_evict_normal();
+  const uint64_t pol_keep = a.hints == 2 ? policy_evict_last() : policy_evict_normal();
   if (tid == 0) {
     for (int s = 0; s < NG * TMA_SLOTS; s++) mbar_init(&full[s], 1);
     for (int g = 0; g < NG; g++) mbar_init(&late[g], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int64_t J = 0; J < TMA_SLOTS; J++) super_issue<NG>(&kmap, a, J, slots, eslots, full, meta);
+    for (int64_t J = 0; J < TMA_SLOTS; J++) super_issue<NG>(&kmap, a, J, slots, eslots, full, meta, pol_dead);
   }
   for (int e = tid; e < a.gk.n_phi * PHI_COPIES; e += NG * NTHREADS) phis[e] = a.gk.phi[e / PHI_COPIES];
   __syncthreads();
@@ -518,49 +565,47 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
       // tile J+3 belongs to the other group and is only ever issued by the
       // finisher of J: pass the end marker on before leaving
       group_bar(g);
-      if (gtid == 0) super_issue<NG>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta);
+      if (gtid == 0) super_issue<NG>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
       break;
     }
     double2* xb = slots + (size_t)s * FAST_XBUF;
-    if (m.kind == SK_G0_DEFERRED) {
+    uint8_t* es = eslots + (size_t)s * TILE;
+    if (m.kind == SK_B_DEFERRED) {
       if (gtid == 0) {
         for (uint32_t it = 0; ld_acquire(&a.done[m.c]) < (1u << a.tpc_bits); it++) {
-          __nanosleep(64);
+          __nanosleep(32);
           if (it > (1u << 26)) __trap();
         }
         fence_async_global();
-        mbar_expect_tx(&late[g], TILE * 16u);
-        bulk_g2s(xb, a.g0.psi + tbase(a.g0, m.T), TILE * 16u, &late[g]);
+        load_gk(&kmap, a, m.T, xb, es, &late[g], pol_dead);
       }
       mbar_wait_bounded(&late[g], late_phase & 1);
       late_phase++;
     }
-    const bool isk = m.kind == SK_GK;
+    const bool isb = m.kind != SK_A;
 #pragma unroll
     for (int r = 0; r < RPT; r++) v[r] = xb[tlA | (r << 8)];
     group_bar(g);
-    if (isk)
-      program<FP_GK_PRE_D_POST, LANE3>(a.gk, v, xb, eslots + (size_t)s * TILE, phis, lane, lw, g);
+    if (isb)
+      program<FP_GK_PRE_D_POST, LANE3>(a.gk, v, xb, es, phis, lane, lw, g);
     else
       program<FP_G0_PRE, false>(a.g0, v, xb, nullptr, phis, lane, lw, g);
     fence_async_shared();
     group_bar(g);
-    if (gtid == 0) super_issue<NG>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta);
-    if (isk) {
+    if (gtid == 0) super_issue<NG>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
+    if (isb) {
       double2* dst = a.gk.psi + tbase(a.gk, m.T);
 #pragma unroll
-      for (int r = 0; r < RPT; r++) dst[roff(psk, r)] = v[r];
-      // publish: this group-k tile is stored (release for the group-0 tiles of chunk c)
-      __threadfence();
-      group_bar(g);
-      if (gtid == 0) {
-        __threadfence();  // cumulative: every store this group made before the barrier
-        atomicAdd(&a.done[m.c], 1u);
-      }
+      for (int r = 0; r < RPT; r++) st_hint(dst + roff(psk, r), v[r], pol_dead);
     } else {
       double2* dst = a.g0.psi + tbase(a.g0, m.T);
 #pragma unroll
-      for (int r = 0; r < RPT; r++) dst[roff(ps0, r)] = v[r];
+      for (int r = 0; r < RPT; r++) st_hint(dst + roff(ps0, r), v[r], pol_keep);
+      // publish: the group's stores of this group-0 tile happen before the
+      // barrier; one gpu-scope release add makes them visible to the
+      // acquiring issuer of chunk c's group-k tiles (the grid-sync pattern)
+      group_bar(g);
+      if (gtid == 0) red_release_add(&a.done[m.c], 1u);
     }
   }
 }

@@ -76,9 +76,9 @@ struct qaa_ctx {
   int ctas_per_sm = 1;
   int kernel_mode = 1;  // 1: TMA warp-specialised pass, 0: register-prefetch pass
   int tma_groups = 0;   // consumer groups per TMA CTA: 0 = auto (1 without D, 2 with D)
-  int super_mode = 0;   // L2-blocked D passes (qaa_superpass) when the plan has 3 tile groups
-  int super_groups = 1;
-  int super_prefetch = 1;
+  int super_mode = 1;   // L2-blocked D passes (qaa_superpass) when the plan has 3 tile groups
+  int super_groups = 2;
+  int super_hints = 2;
   SuperArgs super_static[4];
   bool super_ok[4] = {false, false, false, false};
   void* clause_recs = nullptr;  // device clause records (A1) of the loaded instance
@@ -106,6 +106,7 @@ struct qaa_ctx {
   // stats
   qaa_stats stats;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+  std::vector<char> ev_super;  // ev_pool[i] timed an L2-blocked (qaa_superpass) launch
   size_t ev_used = 0;
   std::string err;
 };
@@ -274,12 +275,13 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       ctx->order = (int)value;
       return QAA_OK;
     case QAA_OPT_SUPER:
-      if (value < 0 || value > 7) return fail(ctx, QAA_E_USAGE, "super option must be in 0..7");
-      // bit 0: enable L2-blocked D passes; bit 1: two consumer groups (experimental:
-      // known to stall at the end of the work queue); bit 2: no L2 prefetch
+      if (value < 0 || value > 15) return fail(ctx, QAA_E_USAGE, "super option must be in 0..15");
+      // bit 0: L2-blocked Trotter steps; bit 1: one consumer group per CTA (default two);
+      // bits 2-3: L2 eviction hints (0 = evict-last for the group-0 output that the
+      // group-k sub-pass reads back + evict-first for dead data; 1 = none; 2 = evict-first only)
       ctx->super_mode = (int)(value & 1);
-      ctx->super_groups = (value & 2) ? 2 : 1;
-      ctx->super_prefetch = (value & 4) ? 0 : 1;
+      ctx->super_groups = (value & 2) ? 1 : 2;
+      ctx->super_hints = ((value >> 2) & 3) == 1 ? 0 : (((value >> 2) & 3) == 2 ? 1 : 2);
       return QAA_OK;
     case QAA_OPT_TMA_GROUPS:
       if (value < 0 || value > 2) return fail(ctx, QAA_E_USAGE, "tma groups must be 0 (auto), 1 or 2");
@@ -312,6 +314,16 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     cudaGetLastError();
   }
   return fn;
+}
+
+// experiment knob (QAA_L2_PROMO = 0/64/128/256): L2 sector promotion of the
+// strided-row tensor-map loads
+static CUtensorMapL2promotion l2_promotion() {
+  const char* e = getenv("QAA_L2_PROMO");
+  const int v = e ? atoi(e) : 0;
+  return v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                 : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                            : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
 }
 
 static qaa_status build_tma(qaa_ctx* ctx) {
@@ -374,7 +386,7 @@ static qaa_status build_tma(qaa_ctx* ctx) {
         for (int d = 0; d < nd; d++) estr[d] = 1;
         CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)nd, (void*)ctx->state, gdim, gstride + 1,
                          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                         l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         ok = r == CUDA_SUCCESS;
       } else {
         ok = false;
@@ -844,21 +856,18 @@ static qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<Step
   return QAA_OK;
 }
 
-// Single-GPU evolve with L2-blocked D passes (3 tile groups, pass_tma.cu
-// qaa_superpass): every Trotter step is ONE HBM round trip.
-//   pass 0:        group 1: D_0, rotate step 0          | group 0: rotate step 0
-//   pass j (odd):  group 2: rotate j-1, D_j, rotate j   | group 0: rotate j
-//   pass j (even): group 1: rotate j-1, D_j, rotate j   | group 0: rotate j
-//   final:         the other group: rotate K-1 (plain TMA pass)
-// Each step rotates group 0 once (with its D), group k as "post" of its pass
-// and the other group as "pre" of the next pass.
+// L2-blocked Trotter steps (pass_tma.cu qaa_superpass). The schedule-mode-2
+// plan with 3 tile groups is, after its first pass, a sequence of pass pairs
+//   [group 0: rotate step j] [group k: rotate step j, D_{j+1}, rotate step j+1]
+// (k alternating 1, 2); each pair becomes ONE launch over L2-resident chunks,
+// so every Trotter step but the first and last is one HBM round trip.
 static bool super_usable(qaa_ctx* ctx) {
   return ctx->super_mode && ctx->world == 1 && ctx->kernel_mode == 1 && ctx->geom.groups.size() == 3 &&
          ctx->super_ok[1] && ctx->super_ok[2] && (int)ctx->emax + 1 <= TMA_MAX_PHI;
 }
 
-static qaa_status evolve_super(qaa_ctx* ctx, int64_t K, const std::vector<StepCoef>& sc, const double2* dphi,
-                               int n_phi) {
+static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_pre, double t_post,
+                                    const double2* phi, int n_phi) {
   const int64_t nch = std::max(ctx->super_static[1].nchunks, ctx->super_static[2].nchunks);
   const size_t need = (size_t)nch * sizeof(unsigned) + 256;
   if (ctx->d_super_cap < need) {
@@ -866,86 +875,42 @@ static qaa_status evolve_super(qaa_ctx* ctx, int64_t K, const std::vector<StepCo
     qaa_status st = ensure_buffer(ctx, &ctx->d_super, &ctx->d_super_cap, need);
     if (st) return st;
   }
-  if (ctx->profile) {
-    qaa_status st = ensure_events(ctx, ctx->ev_used + (size_t)K + 1);
-    if (st) return st;
-  }
-  unsigned long long* dq = (unsigned long long*)ctx->d_super;
-  unsigned* done = (unsigned*)((char*)ctx->d_super + 256);
-  auto coef = [&](int64_t step) { return sc[(size_t)step].coef; };
-  for (int64_t j = 0; j < K; j++) {
-    const int k = (j % 2 == 0) ? 1 : 2;
-    SuperArgs a = ctx->super_static[k];
-    const Group& gk = ctx->geom.groups[(size_t)k];
-    const Group& g0 = ctx->geom.groups[0];
-    a.gk.psi = ctx->state;
-    a.g0.psi = ctx->state;
-    a.gk.phi = dphi + (size_t)j * n_phi;
-    a.gk.n_phi = n_phi;
-    for (int b = 0; b < TILE_BITS; b++) {
-      const bool rk = (gk.rot_local >> b) & 1;
-      a.gk.t[0][b] = (j >= 1 && rk) ? coef(j - 1) : 0.0;
-      a.gk.t[1][b] = rk ? coef(j) : 0.0;
-      a.gk.phys[b] = gk.phys[b];
-      a.g0.t[0][b] = ((g0.rot_local >> b) & 1) ? coef(j) : 0.0;
-      a.g0.t[1][b] = 0.0;
-      a.g0.phys[b] = g0.phys[b];
-    }
-    a.gk.ntiles = gk.ntiles;
-    a.g0.ntiles = g0.ntiles;
-    a.gk.nseg = gk.nseg;
-    a.g0.nseg = g0.nseg;
-    for (int s = 0; s < MAX_SEGS; s++) {
-      a.gk.seg_src[s] = gk.seg_src[s];
-      a.gk.seg_dst[s] = gk.seg_dst[s];
-      a.gk.seg_len[s] = gk.seg_len[s];
-      a.g0.seg_src[s] = g0.seg_src[s];
-      a.g0.seg_dst[s] = g0.seg_dst[s];
-      a.g0.seg_len[s] = g0.seg_len[s];
-    }
-    a.prefetch = ctx->super_prefetch;
-    a.queue = dq;
-    a.done = done;
-    CUDA_TRY(cudaMemsetAsync(ctx->d_super, 0, 256 + (size_t)a.nchunks * sizeof(unsigned), ctx->stream));
-    if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
-    CUDA_TRY(launch_superpass(&ctx->tmaps[(size_t)k], a, (gk.rot_local >> 3) & 1, ctx->super_groups, ctx->num_sms,
-                              ctx->stream));
-    if (ctx->profile) {
-      CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, ctx->stream));
-      ctx->ev_used++;
-    }
-    ctx->stats.pass_launches++;
-    ctx->stats.kernel_launches_total++;
-  }
-  // final: the group that was not "post" in the last pass rotates for step K-1
-  const int kf = ((K - 1) % 2 == 0) ? 2 : 1;
-  const Group& gr = ctx->geom.groups[(size_t)kf];
-  TmaArgs ta = ctx->tma_static[(size_t)kf];
-  ta.psi = ctx->state;
-  ta.phi = nullptr;
-  ta.n_phi = n_phi;
+  SuperArgs a = ctx->super_static[k];
+  const Group& gk = ctx->geom.groups[(size_t)k];
+  const Group& g0 = ctx->geom.groups[0];
+  a.gk.psi = ctx->state;
+  a.g0.psi = ctx->state;
+  a.gk.phi = phi;
+  a.gk.n_phi = n_phi;
   for (int b = 0; b < TILE_BITS; b++) {
-    ta.t[0][b] = ((gr.rot_local >> b) & 1) ? coef(K - 1) : 0.0;
-    ta.t[1][b] = 0.0;
-    ta.phys[b] = gr.phys[b];
+    const bool rk = (gk.rot_local >> b) & 1;
+    a.gk.t[0][b] = rk ? t_pre : 0.0;
+    a.gk.t[1][b] = rk ? t_post : 0.0;
+    a.gk.phys[b] = gk.phys[b];
+    a.g0.t[0][b] = ((g0.rot_local >> b) & 1) ? t_g0 : 0.0;
+    a.g0.t[1][b] = 0.0;
+    a.g0.phys[b] = g0.phys[b];
   }
-  ta.ntiles = gr.ntiles;
-  ta.nseg = gr.nseg;
+  a.gk.ntiles = gk.ntiles;
+  a.g0.ntiles = g0.ntiles;
+  a.gk.nseg = gk.nseg;
+  a.g0.nseg = g0.nseg;
   for (int s = 0; s < MAX_SEGS; s++) {
-    ta.seg_src[s] = gr.seg_src[s];
-    ta.seg_dst[s] = gr.seg_dst[s];
-    ta.seg_len[s] = gr.seg_len[s];
+    a.gk.seg_src[s] = gk.seg_src[s];
+    a.gk.seg_dst[s] = gk.seg_dst[s];
+    a.gk.seg_len[s] = gk.seg_len[s];
+    a.g0.seg_src[s] = g0.seg_src[s];
+    a.g0.seg_dst[s] = g0.seg_dst[s];
+    a.g0.seg_len[s] = g0.seg_len[s];
   }
-  const int grid = (int)std::min<int64_t>(gr.ntiles / 2, ctx->num_sms);
-  if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
-  CUDA_TRY(launch_pass_tma(&ctx->tmaps[(size_t)kf], ta, FP_GK_PRE, (gr.rot_local >> 3) & 1, 1, grid, ctx->stream));
-  if (ctx->profile) {
-    CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, ctx->stream));
-    ctx->ev_used++;
-  }
-  ctx->stats.pass_launches++;
-  ctx->stats.kernel_launches_total++;
-  return QAA_OK;
+  a.hints = ctx->super_hints;
+  a.queue = (unsigned long long*)ctx->d_super;
+  a.done = (unsigned*)((char*)ctx->d_super + 256);
+  CUDA_TRY(cudaMemsetAsync(ctx->d_super, 0, 256 + (size_t)a.nchunks * sizeof(unsigned), ctx->stream));
+  return launch_superpass(&ctx->tmaps[(size_t)k], a, (gk.rot_local >> 3) & 1, ctx->super_groups, ctx->num_sms,
+                          ctx->stream) == cudaSuccess
+             ? QAA_OK
+             : fail(ctx, QAA_E_CUDA, "superpass launch failed");
 }
 
 static const Program* get_program(qaa_ctx* ctx, int g, bool pre, bool d, bool post) {
@@ -1048,11 +1013,6 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
     ctx->stats.kernel_launches_total++;
     return QAA_OK;
   }
-  if (super_usable(ctx) && ctx->step_spanning && ctx->order == 1) {
-    bool tangent = true;
-    for (int64_t k = 0; k < K; k++) tangent = tangent && sc[(size_t)k].form == 0;
-    if (tangent) return evolve_super(ctx, K, sc, dphi, n_phi);
-  }
   std::vector<PassPlan> plan;
   build_pass_schedule((int)ctx->geom.groups.size(), K, ctx->step_spanning, &plan);
   // Strang: the closing half step D_K follows the pass that completes X_{K-1}
@@ -1075,7 +1035,33 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
   fa.n_phi = n_phi;
   const bool prefetch = ctx->ctas_per_sm == 1;
   const int fast_grid_cap = ctx->num_sms * (prefetch ? 1 : 2);
-  for (const PassPlan& pp : plan) {
+  const bool sup = super_usable(ctx) && ctx->step_spanning == 2 && ctx->order == 1;
+  for (size_t pi = 0; pi < plan.size(); pi++) {
+    const PassPlan& pp = plan[pi];
+    if (sup && pi + 1 < plan.size()) {
+      // [group 0: pre j] [group k: pre j, D_{j+1}, post j+1] -> one L2-blocked launch
+      const PassPlan& pn = plan[pi + 1];
+      if (pp.group == 0 && pp.pre_step >= 0 && pp.d_step < 0 && pp.post_step < 0 && pn.group >= 1 &&
+          pn.pre_step == pp.pre_step && pn.d_step >= 0 && pn.post_step >= 0 &&
+          ctx->super_ok[(size_t)pn.group] && sc[(size_t)pp.pre_step].form == 0 &&
+          sc[(size_t)pn.post_step].form == 0) {
+        if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
+        qaa_status st = launch_super_pair(ctx, pn.group, sc[(size_t)pp.pre_step].coef, sc[(size_t)pn.pre_step].coef,
+                                          sc[(size_t)pn.post_step].coef, dphi + (size_t)pn.d_step * n_phi, n_phi);
+        if (st) return st;
+        if (ctx->profile) {
+          CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, ctx->stream));
+          if (ctx->ev_super.size() < ctx->ev_pool.size()) ctx->ev_super.resize(ctx->ev_pool.size(), 0);
+          ctx->ev_super[ctx->ev_used] = 1;
+          ctx->ev_used++;
+        }
+        ctx->stats.pass_launches++;
+        ctx->stats.super_launches++;
+        ctx->stats.kernel_launches_total++;
+        pi++;
+        continue;
+      }
+    }
     const Group& gr = ctx->geom.groups[pp.group];
     const bool pre = pp.pre_step >= 0, d = pp.d_step >= 0, post = pp.post_step >= 0;
     int fp = -1;
@@ -1595,6 +1581,11 @@ qaa_status qaa_get_stats(qaa_ctx* ctx, qaa_stats* out) {
       CUDA_TRY(cudaEventElapsedTime(&ms, ctx->ev_pool[i].first, ctx->ev_pool[i].second));
       ctx->stats.pass_kernel_ms += ms;
       ctx->stats.pass_kernels_timed++;
+      if (i < ctx->ev_super.size() && ctx->ev_super[i]) {
+        ctx->stats.super_kernel_ms += ms;
+        ctx->stats.super_kernels_timed++;
+        ctx->ev_super[i] = 0;
+      }
     }
     ctx->ev_used = 0;
   }
@@ -1607,7 +1598,7 @@ qaa_status qaa_get_stats(qaa_ctx* ctx, qaa_stats* out) {
   s.row_bits = ctx->row_bits;
   const int P = s.groups;
   s.passes_per_step_num = (ctx->step_spanning && P > 1) ? P - 1 : P;
-  if (ctx->L > RESIDENT_MAX_L && super_usable(ctx) && ctx->step_spanning) s.passes_per_step_num = 1;
+  if (ctx->L > RESIDENT_MAX_L && super_usable(ctx) && ctx->step_spanning == 2) s.passes_per_step_num = 1;
   if (ctx->world > 1) s.passes_per_step_num = P;  // sharded: one phase of P passes per step (§7)
   s.passes_per_step_den = 1;
   s.bytes_per_pass = s.amps_local * 32;

@@ -105,7 +105,8 @@ class qaa_stats(ctypes.Structure):
                 ("bytes_per_pass", ctypes.c_int64), ("amps_local", ctypes.c_int64),
                 ("n", ctypes.c_int), ("n_local", ctypes.c_int), ("groups", ctypes.c_int),
                 ("tile_bits", ctypes.c_int), ("row_bits", ctypes.c_int),
-                ("kernel_launches_total", ctypes.c_int64)]
+                ("kernel_launches_total", ctypes.c_int64), ("super_launches", ctypes.c_int64),
+                ("super_kernel_ms", ctypes.c_double), ("super_kernels_timed", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -337,11 +337,11 @@ def test_torch_owned_state(q, orc):
 
 
 @pytest.mark.parametrize("n", [22, 23, 24, 26])
-@pytest.mark.parametrize("sup", [1, 5, 0])
+@pytest.mark.parametrize("sup", [1, 3, 0])
 @pytest.mark.parametrize("K", [1, 2, 5])
 def test_super_pass_parity(q, ctx, orc, n, sup, K):
-    """L2-blocked D passes (QAA_OPT_SUPER bit 0, one consumer group; bit 2 = no
-    L2 prefetch) against the oracle; 0 = the two-pass plan."""
+    """L2-blocked Trotter steps (QAA_OPT_SUPER bit 0; bit 1 = one consumer group)
+    against the oracle; 0 = the two-pass plan."""
     ctx.set_option(q.OPT_SUPER, sup)
     cl = instance(n)
     psi0 = cnf.random_state(n, 31 + n)
@@ -350,8 +350,8 @@ def test_super_pass_parity(q, ctx, orc, n, sup, K):
     assert_close(got, want)
     st = ctx.stats()
     if sup & 1:
-        assert st["pass_launches"] == K + 1  # one HBM round trip per step + the final partial pass
-    ctx.set_option(q.OPT_SUPER, 0)
+        assert st["pass_launches"] == K + 2  # first pass, K-1 fused pairs, final two passes
+        assert st["super_launches"] == K - 1
 
 
 @pytest.mark.parametrize("n", [6, 12, 16, 22, 23])

@@ -1,0 +1,6 @@
+# Re-entry check of HEAD: full GPU suite + smoke + round artefacts.
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -6
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
+bash tools/gpu_profile_round.sh

@@ -87,8 +87,11 @@ int main() {
   CK(cudaMemset(psi, 0, N * 16));
   int64_t ntiles = N >> 12;
   struct Cfg { int c, row_shift; const char* name; } cfgs[] = {
-    {12, 12, "contiguous 64KiB tiles"}, {3, 12, "128B rows stride 2^12 amps (mid)"}, {3, 21, "128B rows stride 2^21 (hi)"},
-    {4, 12, "256B rows stride 2^12"}, {4, 22, "256B rows stride 2^22"}, {2, 21, "64B rows stride 2^21"}};
+    {12, 12, "contiguous 64KiB tiles"}, {3, 12, "128B rows stride 2^12 (16 pages/tile)"},
+    {3, 13, "128B rows stride 2^13 (32 pages/tile)"}, {3, 14, "128B rows stride 2^14 (64 pages/tile)"},
+    {3, 15, "128B rows stride 2^15 (128 pages/tile)"}, {3, 16, "128B rows stride 2^16 (256 pages/tile)"},
+    {3, 17, "128B rows stride 2^17 (512 pages/tile)"}, {3, 21, "128B rows stride 2^21 (512 pages/tile)"},
+    {4, 12, "256B rows stride 2^12"}, {4, 22, "256B rows stride 2^22"}};
   for (auto& cf : cfgs) {
     for (int occ = 1; occ <= 4; occ *= 2) {
       int blocks = p.multiProcessorCount * occ;
