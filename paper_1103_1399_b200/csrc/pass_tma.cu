@@ -222,16 +222,35 @@ __device__ __forceinline__ void rot_lane(double2 (&v)[RPT], int lanebit, double 
     v[r] = make_double2(fma(-t, py, v[r].x), fma(t, px, v[r].y));
   }
 }
+// Cross-warp exchange through the padded layout. The leading barrier is the
+// write-after-read guard (every warp of the group has finished reading the
+// buffer: the landed tile or the previous exchange), placed after the caller's
+// rotations so warp skew overlaps FMAs; the second orders the STS before the LDS.
 template <int FROM, int TO>
 __device__ __forceinline__ void xchg(double2* xb, double2 (&v)[RPT], int lane, int warp, int g) {
   const int bs = padA(pat_tl<FROM>(lane, warp));
+  group_bar(g);
 #pragma unroll
   for (int r = 0; r < RPT; r++) xb[bs + padA(r << reg_shift<FROM>())] = v[r];
   group_bar(g);
   const int bl = padA(pat_tl<TO>(lane, warp));
 #pragma unroll
   for (int r = 0; r < RPT; r++) v[r] = xb[bl + padA(r << reg_shift<TO>())];
-  group_bar(g);
+}
+// Warp-local exchange PB -> PC, in place in the landed (unpadded) tile. Both
+// patterns hold warp bits 9..11, so a warp only ever touches its own 512
+// amplitudes: no group barrier. Position of local index l: l ^ ((l >> 4) & 7)
+// (bits 4..6 XORed into the 16-byte bank group): a quarter-warp of PB varies
+// bits 0..2, one of PC bits 4..6 -- 8 distinct bank groups either way.
+__device__ __forceinline__ int swz(int l) { return l ^ ((l >> 4) & 7); }
+__device__ __forceinline__ void xchg_local_pb_pc(double2* xb, double2 (&v)[RPT], int lane, int warp) {
+  const int tb = pat_tl<PB>(lane, warp), tc = pat_tl<PC>(lane, warp);
+  __syncwarp();  // every lane's landed read of these positions is done
+#pragma unroll
+  for (int r = 0; r < RPT; r++) xb[swz(tb | (r << 4))] = v[r];
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < RPT; r++) v[r] = xb[swz(tc | r)];
 }
 template <int P>
 __device__ __forceinline__ void diag(double2 (&v)[RPT], const uint8_t* es, const double2* phis, int lane, int warp) {
@@ -261,11 +280,12 @@ __device__ __forceinline__ void program(const TmaArgs& a, double2 (&v)[RPT], dou
     xchg<PC, PB>(xb, v, lane, warp, g);
     rot_regs<PB>(v, t1);
   } else if (PROG == FP_G0_PRE) {
-    rot_regs<PA>(v, t0);
-    xchg<PA, PC>(xb, v, lane, warp, g);
-    rot_regs<PC>(v, t0);
-    xchg<PC, PB>(xb, v, lane, warp, g);
+    // landed read in PB; PB -> PC warp-local; one cross-warp exchange to PA
     rot_regs<PB>(v, t0);
+    xchg_local_pb_pc(xb, v, lane, warp);
+    rot_regs<PC>(v, t0);
+    xchg<PC, PA>(xb, v, lane, warp, g);
+    rot_regs<PA>(v, t0);
   } else if (PROG == FP_G0_PRE_D_POST) {
     rot_regs<PA>(v, t0);
     xchg<PA, PC>(xb, v, lane, warp, g);
@@ -299,8 +319,18 @@ __device__ __forceinline__ void program(const TmaArgs& a, double2 (&v)[RPT], dou
 template <int PROG>
 struct Info {
   static constexpr bool has_d = PROG == FP_G0_DPOST || PROG == FP_G0_PRE_D_POST || PROG == FP_GK_PRE_D_POST;
-  static constexpr int store_pat = (PROG == FP_G0_PRE_D_POST || PROG == FP_GK_PRE_D_POST) ? PA : PB;
+  static constexpr int store_pat = (PROG == FP_G0_PRE_D_POST || PROG == FP_GK_PRE_D_POST || PROG == FP_G0_PRE) ? PA : PB;
+  // pattern of the read from the landed tile (both are conflict-free on the
+  // unpadded layout: a quarter-warp reads 8 consecutive amplitudes)
+  static constexpr int load_pat = PROG == FP_G0_PRE ? PB : PA;
 };
+
+template <int P>
+__device__ __forceinline__ void load_landed(double2 (&v)[RPT], const double2* xb, int lane, int warp) {
+  const int tl = pat_tl<P>(lane, warp);
+#pragma unroll
+  for (int r = 0; r < RPT; r++) v[r] = xb[tl | (r << reg_shift<P>())];
+}
 
 // The CTA's j-th tile. Tiles come in pairs (2m, 2m+1) that differ only in the
 // lowest tile-id bit -- for the strided groups that is physical bit c, so the
@@ -362,16 +392,15 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_pass_tma(const __grid_co
   // NG = 2 overlaps two groups' transposes and FMAs (compute-heavy passes).
   const int g = warp >> 3, lw = warp & 7;
   const Off ps = make_off<I::store_pat>(a, lane, lw);
-  const int tlA = pat_tl<PA>(lane, lw);
   double2 v[RPT];
   for (int64_t j = g; j < nt; j += NG) {
     const int s = (int)(j % TMA_SLOTS);
     mbar_wait(&full[NG * s + g], (uint32_t)((j / (NG * TMA_SLOTS)) & 1));
     double2* xb = slots + (size_t)s * FAST_XBUF;
     const uint8_t* es = eslots + (size_t)s * TILE;
-#pragma unroll
-    for (int r = 0; r < RPT; r++) v[r] = xb[tlA | (r << 8)];  // landed layout: tile-local order
-    group_bar(g);
+    load_landed<I::load_pat>(v, xb, lane, lw);  // landed layout: tile-local order
+    // no barrier: the first shared-memory write of every program is warp-local
+    // in place or an exchange with a leading barrier
     program<PROG, LANE3>(a, v, xb, es, phis, lane, lw, g);
     // release the slot: order this group's generic smem accesses before the
     // async-proxy (TMA) write that refills it
@@ -552,9 +581,8 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
   for (int e = tid; e < a.gk.n_phi * PHI_COPIES; e += NG * NTHREADS) phis[e] = a.gk.phi[e / PHI_COPIES];
   __syncthreads();
   const int g = warp >> 3, lw = warp & 7, gtid = tid & (NTHREADS - 1);
-  const Off psk = make_off<PA>(a.gk, lane, lw);  // GK_PRE_D_POST stores in pattern PA
-  const Off ps0 = make_off<PB>(a.g0, lane, lw);  // G0_PRE stores in pattern PB
-  const int tlA = pat_tl<PA>(lane, lw);
+  const Off psk = make_off<Info<FP_GK_PRE_D_POST>::store_pat>(a.gk, lane, lw);
+  const Off ps0 = make_off<Info<FP_G0_PRE>::store_pat>(a.g0, lane, lw);
   uint32_t late_phase = 0;
   double2 v[RPT];
   for (int64_t J = g;; J += NG) {
@@ -583,13 +611,13 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
       late_phase++;
     }
     const bool isb = m.kind != SK_A;
-#pragma unroll
-    for (int r = 0; r < RPT; r++) v[r] = xb[tlA | (r << 8)];
-    group_bar(g);
-    if (isb)
+    if (isb) {
+      load_landed<Info<FP_GK_PRE_D_POST>::load_pat>(v, xb, lane, lw);
       program<FP_GK_PRE_D_POST, LANE3>(a.gk, v, xb, es, phis, lane, lw, g);
-    else
+    } else {
+      load_landed<Info<FP_G0_PRE>::load_pat>(v, xb, lane, lw);
       program<FP_G0_PRE, false>(a.g0, v, xb, nullptr, phis, lane, lw, g);
+    }
     fence_async_shared();
     group_bar(g);
     if (gtid == 0) super_issue<NG>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
