@@ -634,7 +634,7 @@ cudaError_t launch_reduce_partials(const double* partial, int nblocks, int strid
 }  // namespace qaa
 
 namespace qaa {
-// Eg[T*4096 + l] = E[tbase(T) + off(l)]: the energy slice of tile T of a group,
+// Eg[T*4096 + pack(l)] = E[tbase(T) + off(l)]: the energy slice of tile T of a group,
 // contiguous so the TMA pass can bulk-copy it next to the amplitudes.
 struct PermArgs {
   int phys[TILE_BITS];
@@ -653,7 +653,10 @@ __global__ void __launch_bounds__(256) permute_energy_kernel(const uint8_t* E, u
 #pragma unroll
       for (int b = 0; b < TILE_BITS; b++)
         if ((l >> b) & 1) o += (int64_t)1 << a.phys[b];
-      Eg[T * TILE + l] = E[o];
+      // packed for the pattern-PB D of the group-k programs (pass_tma.cu diag):
+      // thread t = lane + 32 warp of PB holds register r at byte 16 t + r
+      const int lane = (l & 15) | (((l >> 8) & 1) << 4), warp = l >> 9, r = (l >> 4) & 15;
+      Eg[T * TILE + (((lane + 32 * warp) << 4) | r)] = E[o];
     }
   }
 }

@@ -114,7 +114,8 @@ cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool l
                              cudaStream_t st);
 cudaError_t launch_pass_tma(const CUtensorMap* map, const TmaArgs& a, int prog, bool lane3, int ngroups, int grid,
                             cudaStream_t st);
-// gather a group's energy layout: Eg[T*4096 + l] = E[tbase(T) + off(l)]
+// gather a group's energy layout: Eg[T*4096 + pack(l)] = E[tbase(T) + off(l)], pack =
+// the thread-major order of register pattern PB (16 bytes per thread, one LDS.128)
 cudaError_t launch_permute_energy(const uint8_t* E, uint8_t* Eg, const int (&phys)[TILE_BITS], int nseg,
                                   const int* seg_src, const int* seg_dst, const int* seg_len, int64_t ntiles,
                                   int num_sms, cudaStream_t st);

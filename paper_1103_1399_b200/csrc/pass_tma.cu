@@ -26,6 +26,14 @@ constexpr int TMA_SLOTS = 3;
 constexpr int SLOT_BYTES = FAST_XBUF * 16;  // 69632: padded exchange layout
 constexpr int TMA_MAX_GROUPS = 2;
 constexpr int PHI_COPIES = 8;  // bank-group copies of the D table (diag below)
+// dynamic shared memory: 3 slots (padded exchange layout), 3 energy slices, the
+// D table copies, mbarriers (full, late), slot metadata, slot counters (last 16 B)
+constexpr size_t TMA_SMEM_BYTES = (size_t)TMA_SLOTS * SLOT_BYTES + (size_t)TMA_SLOTS * TILE +
+                                   (size_t)TMA_MAX_PHI * PHI_COPIES * 16 + TMA_MAX_GROUPS * TMA_SLOTS * 8 +
+                                   TMA_MAX_GROUPS * 8 + TMA_SLOTS * 16 + 16;
+__device__ __forceinline__ unsigned* slot_counters(unsigned char* sm) {
+  return reinterpret_cast<unsigned*>(sm + TMA_SMEM_BYTES - 16);
+}
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -252,12 +260,17 @@ __device__ __forceinline__ void xchg_local_pb_pc(double2* xb, double2 (&v)[RPT],
 #pragma unroll
   for (int r = 0; r < RPT; r++) v[r] = xb[swz(tc | r)];
 }
-template <int P>
+// D: PACKED = the group-k energy slice in PB thread-major order (16 bytes per
+// thread, one conflict-free LDS.128); otherwise tile-local order, one byte per amplitude
+template <int P, bool PACKED>
 __device__ __forceinline__ void diag(double2 (&v)[RPT], const uint8_t* es, const double2* phis, int lane, int warp) {
   const int tl = pat_tl<P>(lane, warp);
+  uint4 pk = make_uint4(0, 0, 0, 0);
+  if (PACKED) pk = reinterpret_cast<const uint4*>(es)[lane + 32 * warp];
 #pragma unroll
   for (int r = 0; r < RPT; r++) {
-    const int e = es[tl | (r << reg_shift<P>())];
+    const uint32_t w = r < 4 ? pk.x : (r < 8 ? pk.y : (r < 12 ? pk.z : pk.w));
+    const int e = PACKED ? (int)((w >> (8 * (r & 3))) & 0xffu) : es[tl | (r << reg_shift<P>())];
     // Phi is stored 8x interleaved (entry e of copy c at 8e + c): the 8 lanes of
     // a quarter-warp read copies lane & 7, i.e. 8 distinct 16-byte bank groups,
     // whatever their energies -- a conflict-free 128-bit lookup
@@ -273,7 +286,7 @@ __device__ __forceinline__ void program(const TmaArgs& a, double2 (&v)[RPT], dou
   const double(&t0)[TILE_BITS] = a.t[0];
   const double(&t1)[TILE_BITS] = a.t[1];
   if (PROG == FP_G0_DPOST) {
-    diag<PA>(v, es, phis, lane, warp);
+    diag<PA, false>(v, es, phis, lane, warp);
     rot_regs<PA>(v, t1);
     xchg<PA, PC>(xb, v, lane, warp, g);
     rot_regs<PC>(v, t1);
@@ -292,7 +305,7 @@ __device__ __forceinline__ void program(const TmaArgs& a, double2 (&v)[RPT], dou
     rot_regs<PC>(v, t0);
     xchg<PC, PB>(xb, v, lane, warp, g);
     rot_regs<PB>(v, t0);
-    diag<PB>(v, es, phis, lane, warp);
+    diag<PB, false>(v, es, phis, lane, warp);
     rot_regs<PB>(v, t1);
     xchg<PB, PC>(xb, v, lane, warp, g);
     rot_regs<PC>(v, t1);
@@ -308,7 +321,7 @@ __device__ __forceinline__ void program(const TmaArgs& a, double2 (&v)[RPT], dou
     xchg<PA, PB>(xb, v, lane, warp, g);
     rot_regs<PB>(v, t0);
     if (LANE3) rot_lane(v, 3, t0[3]);
-    diag<PB>(v, es, phis, lane, warp);
+    diag<PB, true>(v, es, phis, lane, warp);
     rot_regs<PB>(v, t1);
     if (LANE3) rot_lane(v, 3, t1[3]);
     xchg<PB, PA>(xb, v, lane, warp, g);
@@ -316,6 +329,17 @@ __device__ __forceinline__ void program(const TmaArgs& a, double2 (&v)[RPT], dou
   }
 }
 
+// "Last warp out refills": each warp, once its values of slot s are consumed,
+// bumps the slot's counter (acq_rel at CTA scope); the 8th warp of the group
+// resets it and refills the slot -- no group barrier before the refill.
+__device__ __forceinline__ bool last_warp_out(unsigned* cnt) {
+  unsigned old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(sa(cnt)) : "memory");
+  if (old != (NTHREADS / 32) - 1) return false;
+  *cnt = 0;
+  fence_async_shared();  // generic-proxy accesses of the slot before the async-proxy refill
+  return true;
+}
 template <int PROG>
 struct Info {
   static constexpr bool has_d = PROG == FP_G0_DPOST || PROG == FP_G0_PRE_D_POST || PROG == FP_GK_PRE_D_POST;
@@ -374,8 +398,10 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_pass_tma(const __grid_co
   // and group j % NG, so each (slot, group) barrier is used by every (3 NG)-th
   // tile, always by the same group, and a parity wait can never see a stale phase.
   uint64_t* full = reinterpret_cast<uint64_t*>(phis + TMA_MAX_PHI * PHI_COPIES);
+  unsigned* cnt = slot_counters(sm);
   using I = Info<PROG>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < TMA_SLOTS) cnt[tid] = 0;
   // tiles of this CTA: pairs (2m, 2m+1), m = blockIdx.x + i gridDim.x (ntiles is even)
   const int64_t nt = 2 * ((a.ntiles / 2 - blockIdx.x + gridDim.x - 1) / gridDim.x);
   if (tid == 0) {
@@ -402,11 +428,10 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_pass_tma(const __grid_co
     // no barrier: the first shared-memory write of every program is warp-local
     // in place or an exchange with a leading barrier
     program<PROG, LANE3>(a, v, xb, es, phis, lane, lw, g);
-    // release the slot: order this group's generic smem accesses before the
-    // async-proxy (TMA) write that refills it
-    fence_async_shared();
-    group_bar(g);
-    if ((tid & (NTHREADS - 1)) == 0 && j + TMA_SLOTS < nt)
+    // release the slot (the program's final rotations consumed every value this
+    // warp read from it); the last warp of the group refills it
+    __syncwarp();
+    if (lane == 0 && last_warp_out(&cnt[s]) && j + TMA_SLOTS < nt)
       issue_tile<PROG, NG>(&tmap, a, j + TMA_SLOTS, slots, eslots, full);
     const int64_t T = tile_of(j);
     double2* dst = a.psi + tbase(a, T);
@@ -567,7 +592,9 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
   uint64_t* full = reinterpret_cast<uint64_t*>(phis + TMA_MAX_PHI * PHI_COPIES);
   uint64_t* late = full + NG * TMA_SLOTS;  // per group: deferred group-k loads
   SlotMeta* meta = reinterpret_cast<SlotMeta*>(late + NG);
+  unsigned* cnt = slot_counters(sm);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < TMA_SLOTS) cnt[tid] = 0;
   // hints: data read once more in this launch (group-0 output) stays, the rest
   // (the loaded tiles, group-k output, energy slices) is marked evict-first
   const uint64_t pol_dead = a.hints ? policy_evict_first() : policy_evict_normal();
@@ -618,9 +645,8 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
       load_landed<Info<FP_G0_PRE>::load_pat>(v, xb, lane, lw);
       program<FP_G0_PRE, false>(a.g0, v, xb, nullptr, phis, lane, lw, g);
     }
-    fence_async_shared();
-    group_bar(g);
-    if (gtid == 0) super_issue<NG>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
+    __syncwarp();
+    if (lane == 0 && last_warp_out(&cnt[s])) super_issue<NG>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
     if (isb) {
       double2* dst = a.gk.psi + tbase(a.gk, m.T);
 #pragma unroll
@@ -662,9 +688,7 @@ TmaKernel pick(int prog, bool lane3, int ng) { return ng == 1 ? pick_ng<1>(prog,
 
 }  // namespace
 
-constexpr size_t TMA_SMEM_BYTES = (size_t)TMA_SLOTS * SLOT_BYTES + (size_t)TMA_SLOTS * TILE +
-                                   (size_t)TMA_MAX_PHI * PHI_COPIES * 16 + TMA_MAX_GROUPS * TMA_SLOTS * 8 +
-                                   TMA_MAX_GROUPS * 8 + TMA_SLOTS * 16;
+
 
 cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, int ngroups, int grid,
                              cudaStream_t st) {
