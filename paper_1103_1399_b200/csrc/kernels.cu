@@ -641,6 +641,7 @@ struct PermArgs {
   int nseg;
   int seg_src[MAX_SEGS], seg_dst[MAX_SEGS], seg_len[MAX_SEGS];
   int64_t ntiles;
+  int pb3;
 };
 __global__ void __launch_bounds__(256) permute_energy_kernel(const uint8_t* E, uint8_t* Eg, const PermArgs a) {
   for (int64_t T = blockIdx.x; T < a.ntiles; T += gridDim.x) {
@@ -653,17 +654,25 @@ __global__ void __launch_bounds__(256) permute_energy_kernel(const uint8_t* E, u
 #pragma unroll
       for (int b = 0; b < TILE_BITS; b++)
         if ((l >> b) & 1) o += (int64_t)1 << a.phys[b];
-      // packed for the pattern-PB D of the group-k programs (pass_tma.cu diag):
-      // thread t = lane + 32 warp of PB holds register r at byte 16 t + r
-      const int lane = (l & 15) | (((l >> 8) & 1) << 4), warp = l >> 9, r = (l >> 4) & 15;
+      // packed for the D of the group-k programs (pass_tma.cu diag): thread
+      // t = lane + 32 warp holds register r at byte 16 t + r, in pattern PB, or
+      // PB3 (tile bits 3 and 7 swapped between register and lane bit 3) when
+      // the group rotates tile bit 3
+      int lane = (l & 15) | (((l >> 8) & 1) << 4), r = (l >> 4) & 15;
+      if (a.pb3) {
+        lane = (l & 7) | (((l >> 7) & 1) << 3) | (((l >> 8) & 1) << 4);
+        r = ((l >> 4) & 7) | (((l >> 3) & 1) << 3);
+      }
+      const int warp = l >> 9;
       Eg[T * TILE + (((lane + 32 * warp) << 4) | r)] = E[o];
     }
   }
 }
 cudaError_t launch_permute_energy(const uint8_t* E, uint8_t* Eg, const int (&phys)[TILE_BITS], int nseg,
                                   const int* seg_src, const int* seg_dst, const int* seg_len, int64_t ntiles,
-                                  int num_sms, cudaStream_t st) {
+                                  int pb3, int num_sms, cudaStream_t st) {
   PermArgs a;
+  a.pb3 = pb3;
   for (int b = 0; b < TILE_BITS; b++) a.phys[b] = phys[b];
   a.nseg = nseg;
   for (int s = 0; s < MAX_SEGS; s++) {

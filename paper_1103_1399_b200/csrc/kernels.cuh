@@ -118,7 +118,7 @@ cudaError_t launch_pass_tma(const CUtensorMap* map, const TmaArgs& a, int prog, 
 // the thread-major order of register pattern PB (16 bytes per thread, one LDS.128)
 cudaError_t launch_permute_energy(const uint8_t* E, uint8_t* Eg, const int (&phys)[TILE_BITS], int nseg,
                                   const int* seg_src, const int* seg_dst, const int* seg_len, int64_t ntiles,
-                                  int num_sms, cudaStream_t st);
+                                  int pb3, int num_sms, cudaStream_t st);
 
 // Whole-evolution kernel for L <= 12 local qubits: one CTA keeps the state in
 // shared memory for all K steps (SURVEY §7 hard part 5; latency-bound sizes).

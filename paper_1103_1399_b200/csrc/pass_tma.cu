@@ -234,6 +234,40 @@ __device__ __forceinline__ void rot_lane(double2 (&v)[RPT], int lanebit, double 
 // write-after-read guard (every warp of the group has finished reading the
 // buffer: the landed tile or the previous exchange), placed after the caller's
 // rotations so warp skew overlaps FMAs; the second orders the STS before the LDS.
+// Swap register bit 3 with lane bit 3 (PB <-> PB3: PB3 holds tile bit 3 in
+// register bit 3 and tile bit 7 in lane bit 3). Half the amplitudes move, one
+// 64-bit shuffle pair each: 32 SHFL per thread, half the cost of rotating lane
+// bit 3 in place (every amplitude needs its partner).
+__device__ __forceinline__ void swap_r3_l3(double2 (&v)[RPT], int lane) {
+  const bool hi = (lane >> 3) & 1;
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    const double2 x = hi ? v[r] : v[r | 8];
+    const double2 y = make_double2(__shfl_xor_sync(FULLM, x.x, 8), __shfl_xor_sync(FULLM, x.y, 8));
+    if (hi)
+      v[r] = y;
+    else
+      v[r | 8] = y;
+  }
+}
+// rotate the four register bits of PB3: register bits 0..2 = tile bits 4..6, 3 = tile bit 3
+__device__ __forceinline__ void rot_regs_pb3(double2 (&v)[RPT], const double (&t)[TILE_BITS]) {
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const double c = i < 3 ? t[4 + i] : t[3];
+#pragma unroll
+    for (int r = 0; r < RPT; r++)
+      if (!(r & (1 << i))) rot2(v[r], v[r | (1 << i)], c);
+  }
+}
+// rotate one register bit
+template <int I>
+__device__ __forceinline__ void rot_regbit(double2 (&v)[RPT], double c) {
+#pragma unroll
+  for (int r = 0; r < RPT; r++)
+    if (!(r & (1 << I))) rot2(v[r], v[r | (1 << I)], c);
+}
+
 template <int FROM, int TO>
 __device__ __forceinline__ void xchg(double2* xb, double2 (&v)[RPT], int lane, int warp, int g) {
   const int bs = padA(pat_tl<FROM>(lane, warp));
@@ -320,10 +354,19 @@ __device__ __forceinline__ void program(const TmaArgs& a, double2 (&v)[RPT], dou
     rot_regs<PA>(v, t0);
     xchg<PA, PB>(xb, v, lane, warp, g);
     rot_regs<PB>(v, t0);
-    if (LANE3) rot_lane(v, 3, t0[3]);
-    diag<PB, true>(v, es, phis, lane, warp);
-    rot_regs<PB>(v, t1);
-    if (LANE3) rot_lane(v, 3, t1[3]);
+    if (LANE3) {
+      // tile bit 3 through a register: PB -> PB3, D in PB3 (the packed energy
+      // slice follows PB3), post rotations of bits 3..6, PB3 -> PB, bit 7
+      swap_r3_l3(v, lane);
+      rot_regbit<3>(v, t0[3]);
+      diag<PB, true>(v, es, phis, lane, warp);
+      rot_regs_pb3(v, t1);
+      swap_r3_l3(v, lane);
+      rot_regbit<3>(v, t1[7]);
+    } else {
+      diag<PB, true>(v, es, phis, lane, warp);
+      rot_regs<PB>(v, t1);
+    }
     xchg<PB, PA>(xb, v, lane, warp, g);
     rot_regs<PA>(v, t1);
   }

@@ -405,7 +405,7 @@ static qaa_status build_tma(qaa_ctx* ctx) {
         ok = false;  // not enough memory for the permuted table: register kernel fallback
       } else {
         CUDA_TRY(launch_permute_energy(ctx->E, eg, gr.phys, gr.nseg, gr.seg_src, gr.seg_dst, gr.seg_len, gr.ntiles,
-                                       ctx->num_sms, ctx->stream));
+                                       (gr.rot_local >> 3) & 1, ctx->num_sms, ctx->stream));
         ctx->stats.kernel_launches_total++;
       }
     }

@@ -1,0 +1,3 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "super or tma or pass or n30" 2>&1 | tail -2
+for m in 1 1 0; do timeout 120 python tools/diag_super2.py $m 20 30; done
