@@ -287,11 +287,11 @@ def run_ours(args):
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback B200_PROFILING.md"}
     if kname == "qaa_superpass":
         # one HBM round trip per step: the launch is bound on chip by the SM's
-        # shared-memory/L1 data path (128 B/clk/SM), 273 B/amp per launch
+        # shared-memory/L1 data path (128 B/clk/SM), 257 B/amp per launch
         sm_hz = (clocks.get("sm_mhz") or 1965.0) * 1e6
         onchip_peak = 128 * 148 * sm_hz / 1e9
-        onchip = 273 * amps / (kms / nl / 1e3) / 1e9
-        roofline["onchip"] = {"bound": "smem/L1 data path", "bytes_per_amp": 273, "achieved": onchip,
+        onchip = 257 * amps / (kms / nl / 1e3) / 1e9
+        roofline["onchip"] = {"bound": "smem/L1 data path", "bytes_per_amp": 257, "achieved": onchip,
                               "peak": onchip_peak, "unit": "GB/s", "frac": onchip / onchip_peak,
                               "peak_source": "128 B/clk/SM x 148 SMs x median SM clock under load"}
     gpu_launches = st["kernel_launches_total"]

@@ -316,16 +316,6 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// experiment knob (QAA_L2_PROMO = 0/64/128/256): L2 sector promotion of the
-// strided-row tensor-map loads
-static CUtensorMapL2promotion l2_promotion() {
-  const char* e = getenv("QAA_L2_PROMO");
-  const int v = e ? atoi(e) : 0;
-  return v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                 : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                            : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
-}
-
 static qaa_status build_tma(qaa_ctx* ctx) {
   for (size_t g = 1; g < ctx->Eg.size(); g++)
     if (ctx->Eg[g]) cudaFree(ctx->Eg[g]);
@@ -386,7 +376,7 @@ static qaa_status build_tma(qaa_ctx* ctx) {
         for (int d = 0; d < nd; d++) estr[d] = 1;
         CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)nd, (void*)ctx->state, gdim, gstride + 1,
                          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         ok = r == CUDA_SUCCESS;
       } else {
         ok = false;
