@@ -155,6 +155,12 @@ __device__ __forceinline__ void st_hint(double2* p, double2 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
                : "memory");
 }
+// tile j uses slot j % 3 and consumer group j % NG: each (slot, group)
+// barrier sees one phase per lcm(3, NG) tiles
+template <int NG>
+__device__ __forceinline__ constexpr int period() {
+  return NG % TMA_SLOTS == 0 ? NG : NG * TMA_SLOTS;
+}
 __device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void group_bar(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(NTHREADS) : "memory");
@@ -464,7 +470,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_pass_tma(const __grid_co
   double2 v[RPT];
   for (int64_t j = g; j < nt; j += NG) {
     const int s = (int)(j % TMA_SLOTS);
-    mbar_wait(&full[NG * s + g], (uint32_t)((j / (NG * TMA_SLOTS)) & 1));
+    mbar_wait(&full[NG * s + g], (uint32_t)((j / period<NG>()) & 1));
     double2* xb = slots + (size_t)s * FAST_XBUF;
     const uint8_t* es = eslots + (size_t)s * TILE;
     load_landed<I::load_pat>(v, xb, lane, lw);  // landed layout: tile-local order
@@ -657,7 +663,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
   double2 v[RPT];
   for (int64_t J = g;; J += NG) {
     const int s = (int)(J % TMA_SLOTS);
-    mbar_wait_bounded(&full[NG * s + g], (uint32_t)((J / (NG * TMA_SLOTS)) & 1));
+    mbar_wait_bounded(&full[NG * s + g], (uint32_t)((J / period<NG>()) & 1));
     const SlotMeta m = meta[s];
     if (m.kind == SK_END) {
       // tile J+3 belongs to the other group and is only ever issued by the
