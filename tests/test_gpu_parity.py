@@ -354,6 +354,34 @@ def test_super_pass_parity(q, ctx, orc, n, sup, K):
         assert st["super_launches"] == K - 1
 
 
+@pytest.mark.parametrize("n", [22, 24, 27, 30])
+def test_super_bitwise_equals_two_pass(q, n):
+    """The L2-blocked step runs the very per-tile programs of the two-pass plan,
+    only fused into one launch over L2-resident chunks (dynamic work queue,
+    deferred loads, cross-CTA release/acquire): at full size the whole state must
+    be bitwise identical to the two-pass plan's (itself oracle-parity-tested),
+    which catches any lost, duplicated or early-read tile."""
+    import torch
+    cl = instance(n)
+    K = 7
+    sched = np.random.default_rng(n).uniform(0, 1, K)
+    outs = []
+    for sup in (1, 0):
+        c = q.Context(0, n_max=n, torch_state=True)
+        c.set_option(q.OPT_SUPER, sup)
+        c.load_instance(n, cl)
+        c.init_uniform()
+        c.evolve(1.7, K, sched)
+        st = c.stats()
+        assert (st["super_launches"] == K - 1) if sup else (st["super_launches"] == 0)
+        torch.cuda.synchronize()
+        outs.append(c.state_tensor().clone())
+        c.close()
+    assert torch.equal(outs[0], outs[1])
+    del outs
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("n", [6, 12, 16, 22, 23])
 @pytest.mark.parametrize("span", [2, 1, 0])
 @pytest.mark.parametrize("kernel", [1, 0])
