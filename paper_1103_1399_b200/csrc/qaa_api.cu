@@ -79,6 +79,7 @@ struct qaa_ctx {
   int super_mode = 1;   // L2-blocked D passes (qaa_superpass) when the plan has 3 tile groups
   int super_groups = 2;
   int super_hints = 2;
+  int super_force = 0;
   SuperArgs super_static[4];
   bool super_ok[4] = {false, false, false, false};
   void* clause_recs = nullptr;  // device clause records (A1) of the loaded instance
@@ -275,12 +276,13 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       ctx->order = (int)value;
       return QAA_OK;
     case QAA_OPT_SUPER:
-      if (value < 0 || value > 15) return fail(ctx, QAA_E_USAGE, "super option must be in 0..15");
+      if (value < 0 || value > 31) return fail(ctx, QAA_E_USAGE, "super option must be in 0..31");
       // bit 0: L2-blocked Trotter steps; bit 1: one consumer group per CTA (default two);
       // bits 2-3: L2 eviction hints (0 = evict-last for the group-0 output that the
       // group-k sub-pass reads back + evict-first for dead data; 1 = none; 2 = evict-first only)
       ctx->super_mode = (int)(value & 1);
       ctx->super_groups = (value & 2) ? 1 : 2;
+      ctx->super_force = (value & 16) ? 1 : 0;  // also below SUPER_MIN_CHUNKS (tests)
       ctx->super_hints = ((value >> 2) & 3) == 1 ? 0 : (((value >> 2) & 3) == 2 ? 1 : 2);
       return QAA_OK;
     case QAA_OPT_TMA_GROUPS:
@@ -851,9 +853,15 @@ static qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<Step
 //   [group 0: rotate step j] [group k: rotate step j, D_{j+1}, rotate step j+1]
 // (k alternating 1, 2); each pair becomes ONE launch over L2-resident chunks,
 // so every Trotter step but the first and last is one HBM round trip.
+// It pays from 256 chunks up (n >= 28 on one GPU, measured): below that the
+// strided groups have padded 256-byte rows, the two-pass plan streams at the
+// copy peak and the chunk pipeline is too short (n = 24: 0.44 vs 0.19 ms/step).
+constexpr int64_t SUPER_MIN_CHUNKS = 256;
 static bool super_usable(qaa_ctx* ctx) {
   return ctx->super_mode && ctx->world == 1 && ctx->kernel_mode == 1 && ctx->geom.groups.size() == 3 &&
-         ctx->super_ok[1] && ctx->super_ok[2] && (int)ctx->emax + 1 <= TMA_MAX_PHI;
+         ctx->super_ok[1] && ctx->super_ok[2] && (int)ctx->emax + 1 <= TMA_MAX_PHI &&
+         (ctx->super_force ||
+          std::min(ctx->super_static[1].nchunks, ctx->super_static[2].nchunks) >= SUPER_MIN_CHUNKS);
 }
 
 static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_pre, double t_post,

@@ -337,11 +337,12 @@ def test_torch_owned_state(q, orc):
 
 
 @pytest.mark.parametrize("n", [22, 23, 24, 26])
-@pytest.mark.parametrize("sup", [1, 3, 0])
+@pytest.mark.parametrize("sup", [17, 19, 0])
 @pytest.mark.parametrize("K", [1, 2, 5])
 def test_super_pass_parity(q, ctx, orc, n, sup, K):
-    """L2-blocked Trotter steps (QAA_OPT_SUPER bit 0; bit 1 = one consumer group)
-    against the oracle; 0 = the two-pass plan."""
+    """L2-blocked Trotter steps (QAA_OPT_SUPER bit 0; bit 1 = one consumer group;
+    bit 4 = also below 256 chunks, i.e. at these test sizes) against the oracle;
+    0 = the two-pass plan."""
     ctx.set_option(q.OPT_SUPER, sup)
     cl = instance(n)
     psi0 = cnf.random_state(n, 31 + n)
@@ -366,7 +367,7 @@ def test_super_bitwise_equals_two_pass(q, n):
     K = 7
     sched = np.random.default_rng(n).uniform(0, 1, K)
     outs = []
-    for sup in (1, 0):
+    for sup in (17, 0):
         c = q.Context(0, n_max=n, torch_state=True)
         c.set_option(q.OPT_SUPER, sup)
         c.load_instance(n, cl)
@@ -374,6 +375,13 @@ def test_super_bitwise_equals_two_pass(q, n):
         c.evolve(1.7, K, sched)
         st = c.stats()
         assert (st["super_launches"] == K - 1) if sup else (st["super_launches"] == 0)
+        if sup:  # the default (bit 4 clear) picks the L2-blocked step only from n = 28 up
+            c2 = q.Context(0)
+            c2.load_instance(n, cl)
+            c2.init_uniform()
+            c2.evolve(1.7, 2, sched[:2])
+            assert (c2.stats()["super_launches"] > 0) == (n >= 28)
+            c2.close()
         torch.cuda.synchronize()
         outs.append(c.state_tensor().clone())
         c.close()

@@ -13,7 +13,8 @@ from inputs import cnf  # noqa: E402
 mode = int(sys.argv[1])
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 30
-cl = cnf.load_instance(n)[0]
+import os
+cl = cnf.load_instance(n)[0] if os.path.exists(cnf.instance_path(n)) else cnf.random_instance(n, int(round(4.5 * n)), 1000 + n)
 idx = np.random.default_rng(5).integers(0, 1 << n, 64)
 with q.Context(0) as c:
     c.set_option(q.OPT_SUPER, mode)
@@ -29,7 +30,8 @@ with q.Context(0) as c:
     dt = time.time() - t0
     st = c.stats()
     amps = np.array([c.state(int(i), 1)[0] for i in idx])
-    np.save(f"gpurun_out/super_amps_{mode}.npy", amps)
+    if n == 30:
+        np.save(f"gpurun_out/super_amps_{mode}.npy", amps)
     print(f"mode={mode} K={K} wall={dt*1e3:.1f}ms per_step={dt/K*1e3:.2f}ms "
           f"pass_ms={st['pass_kernel_ms']:.1f} per_step_kernel={st['pass_kernel_ms']/K:.2f}ms "
           f"launches={st['pass_launches']} norm-1={nn-1:.3e}", flush=True)
