@@ -155,10 +155,12 @@ qaa_status qaa_sigma_x(qaa_ctx* ctx, double* out);
  * instances): evolve `nrep` independent copies of the uniform state
  * of the loaded instance, replica r for total time T[r] in K[r] steps of the
  * midpoint schedule (splitting order of QAA_OPT_ORDER), all in ONE launch with
- * one CTA per replica and the state resident in shared memory (no HBM traffic);
+ * the state resident in shared memory (no HBM traffic): one CTA per replica for
+ * n <= 12, one thread-block cluster of 2^(n-13) CTAs (2^13 amplitudes each,
+ * cluster qubits exchanged through distributed shared memory) for 13 <= n <= 16;
  * out[r] = P_succ of replica r (host array of nrep doubles). The context's own
  * state is not touched. Synchronises.
- * Errors: USAGE (world > 1, n > 12, nrep < 1, NULL arrays, T[r] < 0 or not
+ * Errors: USAGE (world > 1, n > 16, nrep < 1, NULL arrays, T[r] < 0 or not
  * finite, K[r] < 1), STATE (no instance). */
 qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, double* out);
 

@@ -17,6 +17,7 @@
 // (g cos beta)^n (resp. (g sin beta)^n) of a whole step is folded into that
 // step's diagonal table Phi_k[e] = e^{-i dt s_k e} * scale_k, computed on the
 // host (R11).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -379,6 +380,176 @@ cudaError_t launch_sweep(const SweepArgs& a, int nrep, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int threads = a.L >= 9 ? 512 : ((1 << a.L) < 64 ? 64 : (1 << a.L));
   qaa_sweep_kernel<<<nrep, threads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// Batched sweep for 13 <= L <= 16 (SURVEY §8(f) F1 as specified there: each
+// replica's state resident in one thread-block cluster's shared memory, all K
+// steps in one launch, zero HBM traffic). Cluster = 2^(L-13) CTAs; CTA q holds
+// the 2^13 amplitudes whose top L-13 bits are q (128 KiB + its 8 KiB energy
+// slice). Per step: D fused into the first of four register phases over the 13
+// local bits (16 amplitudes per thread: bits {0-3}, {4-7}, {8-11}, {12}), then
+// one DSMEM phase per cluster bit (own' from own and the partner CTA's
+// amplitude at the same local index; cluster barriers before the remote reads
+// and before the writes). DSMEM bandwidth (~20 B/clk/SM) bounds these phases:
+// ~6.5 us per cluster bit; reading all 2^cb - 1 other CTAs at once (two
+// barriers per step instead of two per bit) was measured 4x slower at n = 16. Shared memory holds amplitude x at x ^ ((x>>4)&7):
+// every phase's quarter-warp then hits 8 distinct 16-byte bank groups.
+namespace cg = cooperative_groups;
+constexpr int SWEEP_LB = 13;  // local bits per CTA
+
+__device__ __forceinline__ int sw_pos(int x) { return x ^ ((x >> 4) & 7); }
+__device__ __forceinline__ uint32_t dsmem_map(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(r)
+               : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ double2 ld_dsmem(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+// amplitude index of register r of thread t in the phase whose register bits
+// are R[0..3] (the 9 thread bits fill the other local bits in increasing order)
+__device__ __forceinline__ int sw_index(int t, int r, const int (&R)[4]) {
+  int x = 0, tb = 0;
+#pragma unroll
+  for (int b = 0; b < SWEEP_LB; b++) {
+    int rb = -1;
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+      if (R[i] == b) rb = i;
+    if (rb >= 0)
+      x |= ((r >> rb) & 1) << b;
+    else
+      x |= ((t >> tb++) & 1) << b;
+  }
+  return x;
+}
+
+template <int FORM>
+__device__ __forceinline__ void sw_phase(double2* s, const uint8_t* e, const double2* phi, int t, int nrot,
+                                         const int (&R)[4], double c) {
+  double2 v[16];
+  int pos[16];
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    const int x = sw_index(t, r, R);
+    pos[r] = sw_pos(x);
+    v[r] = s[pos[r]];
+    if (phi) {  // D_k (first phase): psi[x] <- Phi_k[E[x]] psi[x]
+      const double2 f = phi[e[x]];
+      v[r] = make_double2(fma(f.x, v[r].x, -f.y * v[r].y), fma(f.x, v[r].y, f.y * v[r].x));
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+    if (i < nrot)
+#pragma unroll
+      for (int r = 0; r < 16; r++)
+        if (!(r & (1 << i))) rot_pair<FORM>(v[r], v[r | (1 << i)], c);
+#pragma unroll
+  for (int r = 0; r < 16; r++) s[pos[r]] = v[r];
+}
+
+template <int FORM>
+__device__ __forceinline__ void sw_step(double2* s, const uint8_t* e, const double2* phi, int t, double c,
+                                        cg::cluster_group& cl, int cb, int q) {
+  const int R0[4] = {0, 1, 2, 3}, R1[4] = {4, 5, 6, 7}, R2[4] = {8, 9, 10, 11}, R3[4] = {12, 9, 10, 11};
+  sw_phase<FORM>(s, e, phi, t, 4, R0, c);
+  __syncthreads();
+  sw_phase<FORM>(s, e, nullptr, t, 4, R1, c);
+  __syncthreads();
+  sw_phase<FORM>(s, e, nullptr, t, 4, R2, c);
+  __syncthreads();
+  sw_phase<FORM>(s, e, nullptr, t, 1, R3, c);
+  for (int b = 0; b < cb; b++) {
+    cl.sync();  // every CTA's phase writes are visible
+    // partner CTA's copy of my positions, through the shared::cluster window
+    const uint32_t rbase = dsmem_map(s, (uint32_t)(q ^ (1 << b)));
+    double2 v[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) {
+      const int p = t + 512 * i;  // any bijection: own and partner amplitude share the position
+      const double2 a = s[p], w = ld_dsmem(rbase + 16u * (uint32_t)p);
+      v[i] = FORM == 0 ? make_double2(fma(-c, w.y, a.x), fma(c, w.x, a.y))
+                       : make_double2(fma(c, a.x, -w.y), fma(c, a.y, w.x));
+    }
+    cl.sync();  // the partner has read my old values
+#pragma unroll
+    for (int i = 0; i < 16; i++) s[t + 512 * i] = v[i];
+  }
+  __syncthreads();  // the next step's first phase reads other threads' amplitudes
+}
+
+__global__ void __launch_bounds__(512, 1) qaa_sweep_cluster_kernel(const SweepArgs a) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = (int)cl.num_blocks(), q = (int)cl.block_rank();
+  const int cb = a.L - SWEEP_LB, r = blockIdx.x / C, t = threadIdx.x;
+  extern __shared__ double2 smem[];
+  double2* s = smem;
+  uint8_t* e = reinterpret_cast<uint8_t*>(smem + (1 << SWEEP_LB));
+  __shared__ double red[32];
+  __shared__ double part;
+  const int64_t K = a.K[r], off = a.row_off[r];
+  for (int x = t; x < (1 << SWEEP_LB); x += 512) {
+    s[x] = make_double2(a.amp0, 0.0);
+    e[x] = a.E[((int64_t)q << SWEEP_LB) | x];
+  }
+  __syncthreads();
+  for (int64_t k = 0; k < K; k++) {
+    const double2* phi = a.phi_all + (off + k) * a.n_phi;
+    if (a.form[off + k] == 0)
+      sw_step<0>(s, e, phi, t, a.coef[off + k], cl, cb, q);
+    else
+      sw_step<1>(s, e, phi, t, a.coef[off + k], cl, cb, q);
+  }
+  if (a.final_d) {  // Strang: closing half step D(s_{K-1})^{1/2}
+    const double2* phi = a.phi_all + (off + K) * a.n_phi;
+    for (int x = t; x < (1 << SWEEP_LB); x += 512) {
+      const double2 f = phi[e[x]], v = s[sw_pos(x)];
+      s[sw_pos(x)] = make_double2(fma(f.x, v.x, -f.y * v.y), fma(f.x, v.y, f.y * v.x));
+    }
+    __syncthreads();
+  }
+  double acc[1] = {0.0};
+  for (int x = t; x < (1 << SWEEP_LB); x += 512)
+    if (e[x] == 0) {
+      const double2 v = s[sw_pos(x)];
+      acc[0] += fma(v.x, v.x, v.y * v.y);
+    }
+  block_reduce<1>(acc, red);
+  if (t == 0) part = acc[0];
+  cl.sync();
+  if (q == 0 && t == 0) {  // fixed order over the cluster's CTAs
+    double sum = 0.0;
+    for (int j = 0; j < C; j++) sum += *cl.map_shared_rank(&part, j);
+    a.out[r] = sum;
+  }
+  cl.sync();  // keep every CTA's shared memory alive until rank 0 has read it
+}
+
+cudaError_t launch_sweep_cluster(const SweepArgs& a, int nrep, cudaStream_t st) {
+  const size_t smem = (sizeof(double2) + 1) * ((size_t)1 << SWEEP_LB);
+  cudaError_t e = cudaFuncSetAttribute(qaa_sweep_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int C = 1 << (a.L - SWEEP_LB);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nrep * C));
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, qaa_sweep_cluster_kernel, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

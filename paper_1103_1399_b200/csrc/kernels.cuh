@@ -165,6 +165,8 @@ struct SweepArgs {
   double* out;
 };
 cudaError_t launch_sweep(const SweepArgs& a, int nrep, cudaStream_t st);
+// 13 <= L <= 16: one thread-block cluster of 2^(L-13) CTAs per replica
+cudaError_t launch_sweep_cluster(const SweepArgs& a, int nrep, cudaStream_t st);
 
 // Energy table (K1; the paper's kernel):
 // E[x] = sum_c [(xg & M_c) == V_c], xg = x_offset + x, also folding

@@ -24,6 +24,7 @@ using namespace qaa;
 namespace {
 constexpr int64_t ZLIST_CAP = 1 << 16;  // keep Z as a sorted list up to this size
 constexpr int RESIDENT_MAX_L = TILE_BITS;
+constexpr int SWEEP_MAX_L = 16;  // qaa_sweep: one CTA up to 12, one cluster of <= 8 CTAs up to 16
 
 struct ClauseRecHost {
   uint64_t mhi, vhi;
@@ -1493,8 +1494,9 @@ qaa_status qaa_time_energy_table(qaa_ctx* ctx, int reps, double* ms) {
 qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, double* out) {
   CHECK_CTX();
   if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "sweep before load_instance");
-  if (ctx->world != 1 || ctx->L > RESIDENT_MAX_L)
-    return fail(ctx, QAA_E_USAGE, "sweep needs world = 1 and n <= %d (state resident in one CTA)", RESIDENT_MAX_L);
+  if (ctx->world != 1 || ctx->L > SWEEP_MAX_L)
+    return fail(ctx, QAA_E_USAGE, "sweep needs world = 1 and n <= %d (state resident in one CTA or cluster)",
+                SWEEP_MAX_L);
   if (nrep < 1 || !T || !K || !out) return fail(ctx, QAA_E_USAGE, "sweep needs nrep >= 1 and non-NULL arrays");
   int64_t rows = 0;
   for (int r = 0; r < nrep; r++) {
@@ -1562,7 +1564,10 @@ qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, 
   a.final_d = ctx->order == 2 ? 1 : 0;
   double* dout = (double*)(db + ((used + 15) & ~(size_t)15));
   a.out = dout;
-  CUDA_TRY(launch_sweep(a, nrep, ctx->stream));
+  if (ctx->L > RESIDENT_MAX_L)
+    CUDA_TRY(launch_sweep_cluster(a, nrep, ctx->stream));
+  else
+    CUDA_TRY(launch_sweep(a, nrep, ctx->stream));
   ctx->stats.kernel_launches_total++;
   CUDA_TRY(cudaMemcpyAsync(out, dout, (size_t)nrep * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));

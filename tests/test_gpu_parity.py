@@ -411,12 +411,13 @@ def test_strang_parity(q, ctx, orc, n, span, kernel):
     ctx.set_option(q.OPT_ORDER, 1)
 
 
-@pytest.mark.parametrize("n", [6, 8, 12])
+@pytest.mark.parametrize("n", [6, 8, 12, 13, 14, 15, 16])
 @pytest.mark.parametrize("order", [1, 2])
 def test_sweep_parity(q, ctx, orc, n, order):
-    """NEXT F1: batched T sweep (one CTA per replica) against one oracle run per
+    """NEXT F1: batched T sweep (one CTA per replica up to n = 12, one cluster of
+    2^(n-13) CTAs with DSMEM exchange for n = 13..16) against one oracle run per
     replica (configs[1]-style sweep T in {1,2,5,10,20} at dt = 0.05)."""
-    cl, sol = (cnf.load_instance(n) if n != 6 else (cnf.paper_instance()[1], 10))
+    cl = cnf.paper_instance()[1] if n == 6 else instance(n)
     ctx.set_option(q.OPT_ORDER, order)
     ctx.load_instance(n, cl)
     Ts = np.array([1.0, 2.0, 5.0, 10.0, 20.0])
@@ -431,9 +432,9 @@ def test_sweep_parity(q, ctx, orc, n, order):
 
 
 def test_sweep_errors(q, ctx):
-    ctx.load_instance(14, instance(14))
+    ctx.load_instance(17, instance(17))
     with pytest.raises(q.QaaError):
-        ctx.sweep([1.0], [10])  # n > 12
+        ctx.sweep([1.0], [10])  # n > 16
     ctx.load_instance(8, instance(8))
     with pytest.raises(q.QaaError):
         ctx.sweep([1.0], [0])
