@@ -243,7 +243,9 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        group-0 output read back by the group-k sub-pass and evict-first
  *                        for dead data; 1 = no hints; 2 = evict-first only); bit 4: use it
  *                        even below 256 chunks (n < 28), where the two-pass plan is faster
- *                        and is chosen otherwise.
+ *                        and is chosen otherwise; bit 5: hand out the tiles through a
+ *                        global atomic work queue instead of the static round robin
+ *                        (measured 2-4 % slower).
  *  QAA_OPT_ORDER         1 (default) = first-order Lie-Trotter, D then X (R7);
  *                        2 = second-order Strang splitting, D^{1/2} X D^{1/2} per step, at
  *                        the same HBM cost (the half D's of adjacent steps are merged, the

@@ -608,7 +608,11 @@ __device__ void super_issue(const CUtensorMap* kmap, const SuperArgs& a, int64_t
   int kind;
   int64_t c;
   uint32_t i;
-  if (!decode_item(a, atomicAdd(a.queue, 1ull), &kind, &c, &i)) {
+  // queue position: a.queue != nullptr -> dynamic (global atomic counter);
+  // otherwise static round robin, tile J of CTA b = item b + J * gridDim.x
+  const unsigned long long qpos =
+      a.queue ? atomicAdd(a.queue, 1ull) : (unsigned long long)blockIdx.x + (unsigned long long)J * gridDim.x;
+  if (!decode_item(a, qpos, &kind, &c, &i)) {
     meta[s] = SlotMeta{SK_END, 0, 0, 0};
     mbar_arrive_notx(fb);
     return;

@@ -81,6 +81,7 @@ struct qaa_ctx {
   int super_groups = 2;
   int super_hints = 2;
   int super_force = 0;
+  int super_dynamic = 0;
   SuperArgs super_static[4];
   bool super_ok[4] = {false, false, false, false};
   void* clause_recs = nullptr;  // device clause records (A1) of the loaded instance
@@ -277,13 +278,14 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       ctx->order = (int)value;
       return QAA_OK;
     case QAA_OPT_SUPER:
-      if (value < 0 || value > 31) return fail(ctx, QAA_E_USAGE, "super option must be in 0..31");
+      if (value < 0 || value > 63) return fail(ctx, QAA_E_USAGE, "super option must be in 0..63");
       // bit 0: L2-blocked Trotter steps; bit 1: one consumer group per CTA (default two);
       // bits 2-3: L2 eviction hints (0 = evict-last for the group-0 output that the
       // group-k sub-pass reads back + evict-first for dead data; 1 = none; 2 = evict-first only)
       ctx->super_mode = (int)(value & 1);
       ctx->super_groups = (value & 2) ? 1 : 2;
       ctx->super_force = (value & 16) ? 1 : 0;  // also below SUPER_MIN_CHUNKS (tests)
+      ctx->super_dynamic = (value & 32) ? 1 : 0;  // dynamic work queue instead of static round robin
       ctx->super_hints = ((value >> 2) & 3) == 1 ? 0 : (((value >> 2) & 3) == 2 ? 1 : 2);
       return QAA_OK;
     case QAA_OPT_TMA_GROUPS:
@@ -903,7 +905,7 @@ static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_p
     a.g0.seg_len[s] = g0.seg_len[s];
   }
   a.hints = ctx->super_hints;
-  a.queue = (unsigned long long*)ctx->d_super;
+  a.queue = ctx->super_dynamic ? (unsigned long long*)ctx->d_super : nullptr;
   a.done = (unsigned*)((char*)ctx->d_super + 256);
   CUDA_TRY(cudaMemsetAsync(ctx->d_super, 0, 256 + (size_t)a.nchunks * sizeof(unsigned), ctx->stream));
   return launch_superpass(&ctx->tmaps[(size_t)k], a, (gk.rot_local >> 3) & 1, ctx->super_groups, ctx->num_sms,

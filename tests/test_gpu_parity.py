@@ -337,12 +337,13 @@ def test_torch_owned_state(q, orc):
 
 
 @pytest.mark.parametrize("n", [22, 23, 24, 26])
-@pytest.mark.parametrize("sup", [17, 19, 0])
+@pytest.mark.parametrize("sup", [17, 19, 49, 0])
 @pytest.mark.parametrize("K", [1, 2, 5])
 def test_super_pass_parity(q, ctx, orc, n, sup, K):
     """L2-blocked Trotter steps (QAA_OPT_SUPER bit 0; bit 1 = one consumer group;
-    bit 4 = also below 256 chunks, i.e. at these test sizes) against the oracle;
-    0 = the two-pass plan."""
+    bit 4 = also below 256 chunks, i.e. at these test sizes; bit 5 = dynamic work
+    queue instead of the static round robin) against the oracle; 0 = the
+    two-pass plan."""
     ctx.set_option(q.OPT_SUPER, sup)
     cl = instance(n)
     psi0 = cnf.random_state(n, 31 + n)

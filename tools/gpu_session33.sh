@@ -1,0 +1,4 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "super" 2>&1 | tail -2
+for m in 1 33 1 33; do timeout 120 python tools/diag_super2.py $m 20 30; done
+for m in 1 33; do timeout 120 python tools/diag_super2.py $m 50 28; done
