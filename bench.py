@@ -305,9 +305,13 @@ def run_ours(args):
         ctx2.set_option(q.OPT_STEP_SPANNING, args.step_spanning)
         lits = np.ascontiguousarray(np.asarray(cl, dtype=np.int32).reshape(-1))
         pinned = torch.from_numpy(lits).pin_memory().numpy()
-        e2e_steps = max(2, min(args.steps, 4))
+        e2e_steps = max(2, min(args.steps, 10))
         T, s = schedule_window(0, chunk)
-        ctx2.load_instance(n, pinned.reshape(-1, 3))  # warm (allocations)
+        # one untimed warm-up step (allocations, tensor maps, coefficient buffers)
+        ctx2.load_instance(n, pinned.reshape(-1, 3))
+        ctx2.init_uniform()
+        ctx2.evolve(T, chunk, s)
+        ctx2.success_prob()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for i in range(e2e_steps):

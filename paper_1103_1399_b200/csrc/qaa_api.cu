@@ -91,6 +91,7 @@ struct qaa_ctx {
   size_t d_super_cap = 0;
   // TMA state per tile group (built at load)
   std::vector<uint8_t*> Eg;  // per-group permuted energies (Eg[0] = E)
+  std::vector<size_t> Eg_cap;
   std::vector<CUtensorMap> tmaps;
   std::vector<TmaArgs> tma_static;
   std::vector<int> tma_ok;
@@ -322,13 +323,23 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 static qaa_status build_tma(qaa_ctx* ctx) {
-  for (size_t g = 1; g < ctx->Eg.size(); g++)
-    if (ctx->Eg[g]) cudaFree(ctx->Eg[g]);
+  // the permuted tables of the previous load are reused when big enough (a
+  // 1 GiB cudaFree/cudaMalloc pair per load costs more than the permutation)
+  std::vector<uint8_t*> old_eg = ctx->Eg;
+  std::vector<size_t> old_cap = ctx->Eg_cap;
+  auto release_old = [&]() {
+    for (size_t g = 1; g < old_eg.size(); g++)
+      if (old_eg[g]) cudaFree(old_eg[g]);
+  };
   ctx->Eg.clear();
+  ctx->Eg_cap.clear();
   ctx->tmaps.clear();
   ctx->tma_static.clear();
   ctx->tma_ok.clear();
-  if (ctx->L <= RESIDENT_MAX_L) return QAA_OK;
+  if (ctx->L <= RESIDENT_MAX_L) {
+    release_old();
+    return QAA_OK;
+  }
   const int L = ctx->L;
   const size_t N = (size_t)1 << L;
   auto enc = tensor_map_encoder();
@@ -393,7 +404,13 @@ static qaa_status build_tma(qaa_ctx* ctx) {
     if (gi == 0) {
       eg = ctx->E;
     } else if (ok) {
-      cudaError_t e = cudaMalloc(&eg, N);
+      cudaError_t e = cudaSuccess;
+      if (gi < old_eg.size() && old_eg[gi] && old_cap[gi] >= N) {
+        eg = old_eg[gi];
+        old_eg[gi] = nullptr;  // taken over
+      } else {
+        e = cudaMalloc(&eg, N);
+      }
       if (e != cudaSuccess) {
         cudaGetLastError();
         eg = nullptr;
@@ -406,10 +423,12 @@ static qaa_status build_tma(qaa_ctx* ctx) {
     }
     t.Eg = eg;
     ctx->Eg.push_back(eg);
+    ctx->Eg_cap.push_back(gi == 0 || !eg ? 0 : N);
     ctx->tmaps.push_back(map);
     ctx->tma_static.push_back(t);
     ctx->tma_ok.push_back(ok ? 1 : 0);
   }
+  release_old();
   // L2-blocked D passes pair group 0 with group k (k = 1, 2) on chunks that fix
   // every physical bit outside their tile bits (pass_tma.cu qaa_superpass)
   for (int k = 0; k < 4; k++) ctx->super_ok[k] = false;
