@@ -107,10 +107,17 @@ struct SuperArgs {
   uint32_t k_imask, k_cmask;  // group-k tile id = pdep(i, k_imask) | pdep(c, k_cmask)
   uint32_t z_imask, z_cmask;  // group-0 tile id
   int hints;           // L2 eviction hints: 0 none, 1 evict-first for dead data, 2 + evict-last for group-0 output
+  // sharded plan (kernel variant without D): group-k tiles go to the peers' next
+  // shard buffers, tile at local index x -> peers[x >> gshift] at
+  // (x mod 2^gshift) | (rank << gshift) (the layout bit swap)
+  int remote;
+  int gshift;
+  int rank;
+  double2* peers[8];
   unsigned* done;      // [nchunks] group-0 tiles stored per chunk (zeroed before launch)
   unsigned long long* queue;  // global work counter (zeroed before launch)
 };
-cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, int ngroups, int grid,
+cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, int ngroups, bool bd, int grid,
                              cudaStream_t st);
 cudaError_t launch_pass_tma(const CUtensorMap* map, const TmaArgs& a, int prog, bool lane3, int ngroups, int grid,
                             cudaStream_t st);

@@ -581,10 +581,11 @@ struct SlotMeta {
   int pad;
 };
 
-// group-k tile T (tensor-map rows) and its energy slice, completing on bar
+// group-k tile T (tensor-map rows) and, with D, its energy slice, completing on bar
+template <bool BD>
 __device__ __forceinline__ void load_gk(const CUtensorMap* kmap, const SuperArgs& a, uint32_t T, double2* dst,
                                        uint8_t* edst, uint64_t* bar, uint64_t pol) {
-  mbar_expect_tx(bar, TILE * 16u + (uint32_t)TILE);
+  mbar_expect_tx(bar, TILE * 16u + (BD ? (uint32_t)TILE : 0u));
   if (a.gk.contiguous) {
     bulk_g2s_hint(dst, a.gk.psi + tbase(a.gk, T), TILE * 16u, bar, pol);
   } else {
@@ -596,11 +597,11 @@ __device__ __forceinline__ void load_gk(const CUtensorMap* kmap, const SuperArgs
     }
     tma_load_hint(dst, kmap, cc, a.gk.ndims, bar, pol);
   }
-  bulk_g2s_hint(edst, a.gk.Eg + (int64_t)T * TILE, TILE, bar, pol);
+  if (BD) bulk_g2s_hint(edst, a.gk.Eg + (int64_t)T * TILE, TILE, bar, pol);
 }
 
 // fetch the next work item for slot J % 3 (tile J of this CTA) and start its load
-template <int NG>
+template <int NG, bool BD>
 __device__ void super_issue(const CUtensorMap* kmap, const SuperArgs& a, int64_t J, double2* slots, uint8_t* eslots,
                             uint64_t* full, SlotMeta* meta, uint64_t pol_dead) {
   const int s = (int)(J % TMA_SLOTS);
@@ -628,16 +629,20 @@ __device__ void super_issue(const CUtensorMap* kmap, const SuperArgs& a, int64_t
   if (ld_acquire(&a.done[c]) >= (1u << a.tpc_bits)) {
     fence_async_global();  // generic-proxy stores of chunk c -> this async-proxy read
     meta[s] = SlotMeta{SK_B, (int)c, T, 0};
-    load_gk(kmap, a, T, slots + (size_t)s * FAST_XBUF, eslots + (size_t)s * TILE, fb, pol_dead);
+    load_gk<BD>(kmap, a, T, slots + (size_t)s * FAST_XBUF, eslots + (size_t)s * TILE, fb, pol_dead);
   } else {
     meta[s] = SlotMeta{SK_B_DEFERRED, (int)c, T, 0};
     mbar_arrive_notx(fb);
   }
 }
 
-template <bool LANE3, int NG>
+// BD: the group-k sub-pass is rotate/D/rotate (single GPU); otherwise a plain
+// rotate whose tiles may be stored straight into the peers' next shard buffers
+// (a.remote: the layout swap of the sharded plan)
+template <bool LANE3, int NG, bool BD>
 __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_constant__ CUtensorMap kmap,
                                                                  const SuperArgs a) {
+  constexpr int BPROG = BD ? FP_GK_PRE_D_POST : FP_GK_PRE;
   extern __shared__ __align__(128) unsigned char sm[];
   double2* slots = reinterpret_cast<double2*>(sm);
   uint8_t* eslots = sm + TMA_SLOTS * SLOT_BYTES;
@@ -656,12 +661,13 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
     for (int s = 0; s < NG * TMA_SLOTS; s++) mbar_init(&full[s], 1);
     for (int g = 0; g < NG; g++) mbar_init(&late[g], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int64_t J = 0; J < TMA_SLOTS; J++) super_issue<NG>(&kmap, a, J, slots, eslots, full, meta, pol_dead);
+    for (int64_t J = 0; J < TMA_SLOTS; J++) super_issue<NG, BD>(&kmap, a, J, slots, eslots, full, meta, pol_dead);
   }
-  for (int e = tid; e < a.gk.n_phi * PHI_COPIES; e += NG * NTHREADS) phis[e] = a.gk.phi[e / PHI_COPIES];
+  if (BD)
+    for (int e = tid; e < a.gk.n_phi * PHI_COPIES; e += NG * NTHREADS) phis[e] = a.gk.phi[e / PHI_COPIES];
   __syncthreads();
   const int g = warp >> 3, lw = warp & 7, gtid = tid & (NTHREADS - 1);
-  const Off psk = make_off<Info<FP_GK_PRE_D_POST>::store_pat>(a.gk, lane, lw);
+  const Off psk = make_off<Info<BPROG>::store_pat>(a.gk, lane, lw);
   const Off ps0 = make_off<Info<FP_G0_PRE>::store_pat>(a.g0, lane, lw);
   uint32_t late_phase = 0;
   double2 v[RPT];
@@ -673,7 +679,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
       // tile J+3 belongs to the other group and is only ever issued by the
       // finisher of J: pass the end marker on before leaving
       group_bar(g);
-      if (gtid == 0) super_issue<NG>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
+      if (gtid == 0) super_issue<NG, BD>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
       break;
     }
     double2* xb = slots + (size_t)s * FAST_XBUF;
@@ -685,25 +691,35 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
           if (it > (1u << 26)) __trap();
         }
         fence_async_global();
-        load_gk(&kmap, a, m.T, xb, es, &late[g], pol_dead);
+        load_gk<BD>(&kmap, a, m.T, xb, es, &late[g], pol_dead);
       }
       mbar_wait_bounded(&late[g], late_phase & 1);
       late_phase++;
     }
     const bool isb = m.kind != SK_A;
     if (isb) {
-      load_landed<Info<FP_GK_PRE_D_POST>::load_pat>(v, xb, lane, lw);
-      program<FP_GK_PRE_D_POST, LANE3>(a.gk, v, xb, es, phis, lane, lw, g);
+      load_landed<Info<BPROG>::load_pat>(v, xb, lane, lw);
+      program<BPROG, LANE3>(a.gk, v, xb, es, phis, lane, lw, g);
     } else {
       load_landed<Info<FP_G0_PRE>::load_pat>(v, xb, lane, lw);
       program<FP_G0_PRE, false>(a.g0, v, xb, nullptr, phis, lane, lw, g);
     }
     __syncwarp();
-    if (lane == 0 && last_warp_out(&cnt[s])) super_issue<NG>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
+    if (lane == 0 && last_warp_out(&cnt[s])) super_issue<NG, BD>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
     if (isb) {
-      double2* dst = a.gk.psi + tbase(a.gk, m.T);
+      const int64_t tb = tbase(a.gk, m.T);
+      if (!BD && a.remote) {
+        // the bit swap of the sharded layouts: the tile's top local bits (not
+        // tile bits of this group) name the destination rank (pass_fast.cu store)
+        const int64_t j = tb >> a.gshift;
+        double2* dst = a.peers[j] + (tb - (j << a.gshift) + ((int64_t)a.rank << a.gshift));
 #pragma unroll
-      for (int r = 0; r < RPT; r++) st_hint(dst + roff(psk, r), v[r], pol_dead);
+        for (int r = 0; r < RPT; r++) dst[roff(psk, r)] = v[r];
+      } else {
+        double2* dst = a.gk.psi + tb;
+#pragma unroll
+        for (int r = 0; r < RPT; r++) st_hint(dst + roff(psk, r), v[r], pol_dead);
+      }
     } else {
       double2* dst = a.g0.psi + tbase(a.g0, m.T);
 #pragma unroll
@@ -715,12 +731,17 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
       if (gtid == 0) red_release_add(&a.done[m.c], 1u);
     }
   }
+  if (!BD && a.remote) __threadfence_system();
 }
 
 typedef void (*SuperKernel)(const CUtensorMap, const SuperArgs);
-SuperKernel pick_super(bool lane3, int ng) {
-  if (ng == 1) return lane3 ? qaa_superpass<true, 1> : qaa_superpass<false, 1>;
-  return lane3 ? qaa_superpass<true, 2> : qaa_superpass<false, 2>;
+template <bool BD>
+SuperKernel pick_super_bd(bool lane3, int ng) {
+  if (ng == 1) return lane3 ? qaa_superpass<true, 1, BD> : qaa_superpass<false, 1, BD>;
+  return lane3 ? qaa_superpass<true, 2, BD> : qaa_superpass<false, 2, BD>;
+}
+SuperKernel pick_super(bool lane3, int ng, bool bd) {
+  return bd ? pick_super_bd<true>(lane3, ng) : pick_super_bd<false>(lane3, ng);
 }
 
 typedef void (*TmaKernel)(const CUtensorMap, const TmaArgs);
@@ -743,9 +764,9 @@ TmaKernel pick(int prog, bool lane3, int ng) { return ng == 1 ? pick_ng<1>(prog,
 
 
 
-cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, int ngroups, int grid,
+cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, int ngroups, bool bd, int grid,
                              cudaStream_t st) {
-  SuperKernel k = pick_super(lane3, ngroups);
+  SuperKernel k = pick_super(lane3, ngroups, bd);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM_BYTES);
   if (e != cudaSuccess) return e;
   k<<<grid, ngroups * NTHREADS, TMA_SMEM_BYTES, st>>>(*kmap, a);

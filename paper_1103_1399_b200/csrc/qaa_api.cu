@@ -24,7 +24,12 @@ using namespace qaa;
 namespace {
 constexpr int64_t ZLIST_CAP = 1 << 16;  // keep Z as a sorted list up to this size
 constexpr int RESIDENT_MAX_L = TILE_BITS;
-constexpr int SWEEP_MAX_L = 16;  // qaa_sweep: one CTA up to 12, one cluster of <= 8 CTAs up to 16
+constexpr int SWEEP_MAX_L = 16;
+// The L2-blocked step pays from 256 chunks up (n >= 28 on one GPU, measured):
+// below that the strided groups have padded 256-byte rows, the two-pass plan
+// streams at the copy peak and the chunk pipeline is too short (n = 24: 0.44
+// vs 0.19 ms/step).
+constexpr int64_t SUPER_MIN_CHUNKS = 256;  // qaa_sweep: one CTA up to 12, one cluster of <= 8 CTAs up to 16
 
 struct ClauseRecHost {
   uint64_t mhi, vhi;
@@ -81,6 +86,9 @@ struct qaa_ctx {
   int super_groups = 2;
   int super_hints = 2;
   int super_force = 0;
+  bool shard_super_ok = false;  // sharded plan: fused [group 0][group 1 + layout swap] launches
+  SuperArgs shard_super;
+  CUtensorMap shard_kmap[2];    // group 1 over shard buffer 0 / 1
   int super_dynamic = 0;
   SuperArgs super_static[4];
   bool super_ok[4] = {false, false, false, false};
@@ -322,6 +330,126 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+// Tile-group geometry for the TMA kernels: t (contiguous flag, tensor-map
+// dims -> tile-id segments) and, for strided groups, the <= 5-D tensor map of
+// 128-byte rows over the state at `base`. Returns false if not expressible.
+static bool encode_group(qaa_ctx* ctx, const Group& gr, void* base, CUtensorMap* mapp, TmaArgs* tp) {
+  const int L = ctx->L;
+  auto enc = tensor_map_encoder();
+  TmaArgs& t = *tp;
+  CUtensorMap& map = *mapp;
+  memset(&t, 0, sizeof t);
+  memset(&map, 0, sizeof map);
+  bool ok = true;
+  bool in_tile[64] = {false};
+  for (int b = 0; b < TILE_BITS; b++) in_tile[gr.phys[b]] = true;
+  bool contiguous = true;
+  for (int b = 0; b < TILE_BITS; b++) contiguous = contiguous && gr.phys[b] == b;
+  t.contiguous = contiguous ? 1 : 0;
+  if (!contiguous) {
+    // dims: runs of tile bits (split to box-size limits) and gap runs (box 1)
+    cuuint64_t gdim[5], gstride[5];
+    cuuint32_t box[5], estr[5];
+    int nd = 0, gap_index = 0;
+    for (int p = 0; p < L && ok;) {
+      int q = p;
+      while (q + 1 < L && in_tile[q + 1] == in_tile[p]) q++;
+      int bits = q - p + 1;
+      if (in_tile[p]) {
+        int start = p;
+        while (bits > 0 && ok) {
+          const int lim = nd == 0 ? 7 : 8;
+          const int take = bits < lim ? bits : lim;
+          if (nd >= 5) { ok = false; break; }
+          gdim[nd] = (cuuint64_t)1 << (take + (nd == 0 ? 1 : 0));
+          box[nd] = (cuuint32_t)gdim[nd];
+          gstride[nd] = (cuuint64_t)16 << start;
+          t.dim_seg[nd] = -1;
+          nd++;
+          start += take;
+          bits -= take;
+        }
+      } else {
+        if (nd >= 5 || nd == 0) { ok = false; break; }
+        gdim[nd] = (cuuint64_t)1 << bits;
+        box[nd] = 1;
+        gstride[nd] = (cuuint64_t)16 << p;
+        t.dim_seg[nd] = gap_index++;
+        nd++;
+      }
+      p = q + 1;
+    }
+    if (ok && enc) {
+      for (int d = 0; d < nd; d++) estr[d] = 1;
+      CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)nd, base, gdim, gstride + 1,
+                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      ok = r == CUDA_SUCCESS;
+    } else {
+      ok = false;
+    }
+    t.ndims = nd;
+  }
+  return ok;
+}
+
+// Chunk geometry of the L2-blocked pair (group 0, group k): a chunk fixes every
+// physical bit outside both groups' tile bits; false if the two sub-passes do
+// not have the same number of tiles per chunk or k rotates a row bit.
+static bool make_super_args(qaa_ctx* ctx, int k, const TmaArgs& t0, const TmaArgs& tk, SuperArgs* out) {
+  const int L = ctx->L;
+  const Group& g0 = ctx->geom.groups[0];
+  const Group& gk = ctx->geom.groups[(size_t)k];
+  if (gk.rot_local & ~0xFF8u) return false;
+  bool in0[64] = {false}, ink[64] = {false};
+  for (int b = 0; b < TILE_BITS; b++) {
+    in0[g0.phys[b]] = true;
+    ink[gk.phys[b]] = true;
+  }
+  SuperArgs sa;
+  memset(&sa, 0, sizeof sa);
+  // group-k tile-id bits = its non-tile bits in ascending physical order
+  int bit = 0;
+  for (int p = 0; p < L; p++) {
+    if (ink[p]) continue;
+    if (in0[p]) sa.k_imask |= 1u << bit;
+    else sa.k_cmask |= 1u << bit;
+    bit++;
+  }
+  bit = 0;
+  for (int p = 0; p < L; p++) {
+    if (in0[p]) continue;
+    if (ink[p]) sa.z_imask |= 1u << bit;
+    else sa.z_cmask |= 1u << bit;
+    bit++;
+  }
+  const int ik = __builtin_popcount(sa.k_imask), iz = __builtin_popcount(sa.z_imask);
+  const int cb = __builtin_popcount(sa.k_cmask);
+  if (ik != iz || cb != __builtin_popcount(sa.z_cmask)) return false;
+  sa.tpc_bits = ik;
+  sa.nchunks = (int64_t)1 << cb;
+  sa.gk = tk;
+  sa.g0 = t0;
+  *out = sa;
+  return true;
+}
+
+// Sharded plan with three local tile groups: the pass pair [group 0 rotate]
+// [group 1 rotate + layout-swap stores] of every phase runs as one L2-blocked
+// launch (pass_tma.cu qaa_superpass without D, remote group-k stores). Needs
+// group 1's tensor map over both shard buffers.
+static void build_shard_super(qaa_ctx* ctx) {
+  ctx->shard_super_ok = false;
+  if (ctx->geom.groups.size() != 3 || !ctx->bufs[0] || !ctx->bufs[1]) return;
+  TmaArgs t0, t1b[2];
+  CUtensorMap m0;
+  if (!encode_group(ctx, ctx->geom.groups[0], ctx->bufs[0], &m0, &t0) || !t0.contiguous) return;
+  for (int b = 0; b < 2; b++)
+    if (!encode_group(ctx, ctx->geom.groups[1], ctx->bufs[b], &ctx->shard_kmap[b], &t1b[b])) return;
+  if (!make_super_args(ctx, 1, t0, t1b[0], &ctx->shard_super)) return;
+  ctx->shard_super_ok = true;
+}
+
 static qaa_status build_tma(qaa_ctx* ctx) {
   // the permuted tables of the previous load are reused when big enough (a
   // 1 GiB cudaFree/cudaMalloc pair per load costs more than the permutation)
@@ -342,63 +470,11 @@ static qaa_status build_tma(qaa_ctx* ctx) {
   }
   const int L = ctx->L;
   const size_t N = (size_t)1 << L;
-  auto enc = tensor_map_encoder();
   for (size_t gi = 0; gi < ctx->geom.groups.size(); gi++) {
     const Group& gr = ctx->geom.groups[gi];
     TmaArgs t;
-    memset(&t, 0, sizeof t);
     CUtensorMap map;
-    memset(&map, 0, sizeof map);
-    bool ok = true;
-    bool in_tile[64] = {false};
-    for (int b = 0; b < TILE_BITS; b++) in_tile[gr.phys[b]] = true;
-    bool contiguous = true;
-    for (int b = 0; b < TILE_BITS; b++) contiguous = contiguous && gr.phys[b] == b;
-    t.contiguous = contiguous ? 1 : 0;
-    if (!contiguous) {
-      // dims: runs of tile bits (split to box-size limits) and gap runs (box 1)
-      cuuint64_t gdim[5], gstride[5];
-      cuuint32_t box[5], estr[5];
-      int nd = 0, gap_index = 0;
-      for (int p = 0; p < L && ok;) {
-        int q = p;
-        while (q + 1 < L && in_tile[q + 1] == in_tile[p]) q++;
-        int bits = q - p + 1;
-        if (in_tile[p]) {
-          int start = p;
-          while (bits > 0 && ok) {
-            const int lim = nd == 0 ? 7 : 8;
-            const int take = bits < lim ? bits : lim;
-            if (nd >= 5) { ok = false; break; }
-            gdim[nd] = (cuuint64_t)1 << (take + (nd == 0 ? 1 : 0));
-            box[nd] = (cuuint32_t)gdim[nd];
-            gstride[nd] = (cuuint64_t)16 << start;
-            t.dim_seg[nd] = -1;
-            nd++;
-            start += take;
-            bits -= take;
-          }
-        } else {
-          if (nd >= 5 || nd == 0) { ok = false; break; }
-          gdim[nd] = (cuuint64_t)1 << bits;
-          box[nd] = 1;
-          gstride[nd] = (cuuint64_t)16 << p;
-          t.dim_seg[nd] = gap_index++;
-          nd++;
-        }
-        p = q + 1;
-      }
-      if (ok && enc) {
-        for (int d = 0; d < nd; d++) estr[d] = 1;
-        CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)nd, (void*)ctx->state, gdim, gstride + 1,
-                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        ok = r == CUDA_SUCCESS;
-      } else {
-        ok = false;
-      }
-      t.ndims = nd;
-    }
+    bool ok = encode_group(ctx, gr, (void*)ctx->state, &map, &t);
     // permuted energies
     uint8_t* eg = nullptr;
     if (gi == 0) {
@@ -433,45 +509,11 @@ static qaa_status build_tma(qaa_ctx* ctx) {
   // every physical bit outside their tile bits (pass_tma.cu qaa_superpass)
   for (int k = 0; k < 4; k++) ctx->super_ok[k] = false;
   const int P = (int)ctx->geom.groups.size();
-  if (P == 3 && ctx->tma_ok[0]) {
-    const Group& g0 = ctx->geom.groups[0];
-    for (int k = 1; k < P; k++) {
-      if (!ctx->tma_ok[(size_t)k]) continue;
-      const Group& gk = ctx->geom.groups[(size_t)k];
-      if (gk.rot_local & ~0xFF8u) continue;
-      bool in0[64] = {false}, ink[64] = {false};
-      for (int b = 0; b < TILE_BITS; b++) {
-        in0[g0.phys[b]] = true;
-        ink[gk.phys[b]] = true;
-      }
-      SuperArgs sa;
-      memset(&sa, 0, sizeof sa);
-      // group-k tile-id bits = its non-tile bits in ascending physical order
-      int bit = 0;
-      for (int p = 0; p < L; p++) {
-        if (ink[p]) continue;
-        if (in0[p]) sa.k_imask |= 1u << bit;
-        else sa.k_cmask |= 1u << bit;
-        bit++;
-      }
-      bit = 0;
-      for (int p = 0; p < L; p++) {
-        if (in0[p]) continue;
-        if (ink[p]) sa.z_imask |= 1u << bit;
-        else sa.z_cmask |= 1u << bit;
-        bit++;
-      }
-      const int ik = __builtin_popcount(sa.k_imask), iz = __builtin_popcount(sa.z_imask);
-      const int cb = __builtin_popcount(sa.k_cmask);
-      if (ik != iz || cb != __builtin_popcount(sa.z_cmask)) continue;
-      sa.tpc_bits = ik;
-      sa.nchunks = (int64_t)1 << cb;
-      sa.gk = ctx->tma_static[(size_t)k];
-      sa.g0 = ctx->tma_static[0];
-      ctx->super_static[k] = sa;
-      ctx->super_ok[k] = true;
-    }
-  }
+  if (P == 3 && ctx->tma_ok[0])
+    for (int k = 1; k < P; k++)
+      if (ctx->tma_ok[(size_t)k] &&
+          make_super_args(ctx, k, ctx->tma_static[0], ctx->tma_static[(size_t)k], &ctx->super_static[k]))
+        ctx->super_ok[k] = true;
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return QAA_OK;
 }
@@ -712,6 +754,8 @@ qaa_status qaa_load_instance(qaa_ctx* ctx, int n, int m, const int32_t* lits) {
   if (ctx->world == 1) {
     qaa_status st = build_tma(ctx);
     if (st) return st;
+  } else {
+    build_shard_super(ctx);
   }
   ctx->loaded = true;
   return QAA_OK;
@@ -816,11 +860,82 @@ static qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<Step
   fa.n_phi = n_phi;
   fa.gshift = ctx->L - ctx->gbits;
   fa.rank = ctx->rank;
-  for (const ShardPass& sp : plan) {
+  const bool fuse = ctx->shard_super_ok && ctx->super_mode && ctx->kernel_mode == 1 &&
+                    (ctx->super_force || ctx->shard_super.nchunks >= SUPER_MIN_CHUNKS);
+  for (size_t pi = 0; pi < plan.size(); pi++) {
+    const ShardPass& sp = plan[pi];
     if (sp.kind == SK_REMAP) {
       qaa_status st = shard_remap(ctx);
       if (st) return st;
       continue;
+    }
+    if (fuse && pi + 1 < plan.size()) {
+      // [group 0: rotate][group 1: rotate + layout-swap stores] -> one L2-blocked launch
+      const ShardPass& sn = plan[pi + 1];
+      if (sp.kind == SK_PASS && sp.group == 0 && sp.pre_step >= 0 && sp.d_step < 0 && sp.post_step < 0 &&
+          !sp.remote && sn.kind == SK_PASS && sn.group == 1 && sn.pre_step >= 0 && sn.d_step < 0 &&
+          sn.post_step < 0 && sn.remote && sn.layout == sp.layout) {
+        SuperArgs a = ctx->shard_super;
+        const Group& g0 = ctx->geom.groups[0];
+        const Group& g1 = ctx->geom.groups[1];
+        a.g0.psi = ctx->bufs[ctx->cur];
+        a.gk.psi = ctx->bufs[ctx->cur];
+        a.gk.phi = nullptr;
+        a.gk.n_phi = n_phi;
+        for (int b = 0; b < TILE_BITS; b++) {
+          a.g0.t[0][b] = ((sp.pre_local >> b) & 1) ? sc[(size_t)sp.pre_step].coef : 0.0;
+          a.g0.t[1][b] = 0.0;
+          a.g0.phys[b] = g0.phys[b];
+          a.gk.t[0][b] = ((sn.pre_local >> b) & 1) ? sc[(size_t)sn.pre_step].coef : 0.0;
+          a.gk.t[1][b] = 0.0;
+          a.gk.phys[b] = g1.phys[b];
+        }
+        a.g0.ntiles = g0.ntiles;
+        a.gk.ntiles = g1.ntiles;
+        a.g0.nseg = g0.nseg;
+        a.gk.nseg = g1.nseg;
+        for (int q = 0; q < MAX_SEGS; q++) {
+          a.g0.seg_src[q] = g0.seg_src[q];
+          a.g0.seg_dst[q] = g0.seg_dst[q];
+          a.g0.seg_len[q] = g0.seg_len[q];
+          a.gk.seg_src[q] = g1.seg_src[q];
+          a.gk.seg_dst[q] = g1.seg_dst[q];
+          a.gk.seg_len[q] = g1.seg_len[q];
+        }
+        a.hints = ctx->super_hints;
+        a.remote = 1;
+        a.gshift = ctx->L - ctx->gbits;
+        a.rank = ctx->rank;
+        for (int r = 0; r < 8; r++) a.peers[r] = ctx->peers[ctx->cur ^ 1][r];
+        const size_t need = (size_t)a.nchunks * sizeof(unsigned) + 256;
+        if (ctx->d_super_cap < need) {
+          CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+          qaa_status st = ensure_buffer(ctx, &ctx->d_super, &ctx->d_super_cap, need);
+          if (st) return st;
+        }
+        a.queue = ctx->super_dynamic ? (unsigned long long*)ctx->d_super : nullptr;
+        a.done = (unsigned*)((char*)ctx->d_super + 256);
+        CUDA_TRY(cudaMemsetAsync(ctx->d_super, 0, need, ctx->stream));
+        if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
+        CUDA_TRY(launch_superpass(&ctx->shard_kmap[ctx->cur], a, (g1.rot_local >> 3) & 1, ctx->super_groups, false,
+                                  ctx->num_sms, ctx->stream));
+        if (ctx->profile) {
+          CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, ctx->stream));
+          if (ctx->ev_super.size() < ctx->ev_pool.size()) ctx->ev_super.resize(ctx->ev_pool.size(), 0);
+          ctx->ev_super[ctx->ev_used] = 1;
+          ctx->ev_used++;
+        }
+        ctx->stats.pass_launches++;
+        ctx->stats.super_launches++;
+        ctx->stats.kernel_launches_total++;
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        qaa_status st = comm_barrier(ctx);
+        if (st) return st;
+        ctx->cur ^= 1;
+        ctx->state = ctx->bufs[ctx->cur];
+        pi++;
+        continue;
+      }
     }
     const Group& gr = ctx->geom.groups[(size_t)sp.group];
     const bool d = sp.d_step >= 0;
@@ -875,10 +990,6 @@ static qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<Step
 //   [group 0: rotate step j] [group k: rotate step j, D_{j+1}, rotate step j+1]
 // (k alternating 1, 2); each pair becomes ONE launch over L2-resident chunks,
 // so every Trotter step but the first and last is one HBM round trip.
-// It pays from 256 chunks up (n >= 28 on one GPU, measured): below that the
-// strided groups have padded 256-byte rows, the two-pass plan streams at the
-// copy peak and the chunk pipeline is too short (n = 24: 0.44 vs 0.19 ms/step).
-constexpr int64_t SUPER_MIN_CHUNKS = 256;
 static bool super_usable(qaa_ctx* ctx) {
   return ctx->super_mode && ctx->world == 1 && ctx->kernel_mode == 1 && ctx->geom.groups.size() == 3 &&
          ctx->super_ok[1] && ctx->super_ok[2] && (int)ctx->emax + 1 <= TMA_MAX_PHI &&
@@ -927,7 +1038,7 @@ static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_p
   a.queue = ctx->super_dynamic ? (unsigned long long*)ctx->d_super : nullptr;
   a.done = (unsigned*)((char*)ctx->d_super + 256);
   CUDA_TRY(cudaMemsetAsync(ctx->d_super, 0, 256 + (size_t)a.nchunks * sizeof(unsigned), ctx->stream));
-  return launch_superpass(&ctx->tmaps[(size_t)k], a, (gk.rot_local >> 3) & 1, ctx->super_groups, ctx->num_sms,
+  return launch_superpass(&ctx->tmaps[(size_t)k], a, (gk.rot_local >> 3) & 1, ctx->super_groups, true, ctx->num_sms,
                           ctx->stream) == cudaSuccess
              ? QAA_OK
              : fail(ctx, QAA_E_CUDA, "superpass launch failed");

@@ -24,7 +24,7 @@ def comm_worker(rank, world, port, outdir):
     dist.destroy_process_group()
 
 
-def shard_worker(rank, world, port, outdir, n, clauses, T, K, schedule, psi0, s_values):
+def shard_worker(rank, world, port, outdir, n, clauses, T, K, schedule, psi0, s_values, opts=None):
     """GPU: one rank of a sharded evolution (all ranks may share one GPU)."""
     import torch
     dist = _init(rank, world, port)
@@ -32,6 +32,8 @@ def shard_worker(rank, world, port, outdir, n, clauses, T, K, schedule, psi0, s_
     import paper_1103_1399_b200 as q
     comm = q.TorchComm()
     ctx = q.Context(0, rank=rank, world=world, comm=comm)
+    for key, val in (opts or {}).items():
+        ctx.set_option(key, val)
     ctx.load_instance(n, clauses)
     L = n - (world.bit_length() - 1)
     if psi0 is None:
@@ -40,7 +42,8 @@ def shard_worker(rank, world, port, outdir, n, clauses, T, K, schedule, psi0, s_
         ctx.set_state(psi0)  # each rank copies the part it owns
     ctx.evolve(T, K, schedule)
     local = ctx.state(rank << L, 1 << L)
-    res = {"state": local, "success": ctx.success_prob(), "norm2": ctx.norm2(),
+    res = {"state": local, "super_launches": ctx.stats()["super_launches"],
+           "success": ctx.success_prob(), "norm2": ctx.norm2(),
            "sigma_x": ctx.sigma_x(), "energy": np.array([ctx.energy(s) for s in s_values]),
            "nsol": ctx.num_solutions(), "emax": ctx.max_energy(), "E": ctx.energy_table(rank << L, 1 << L)}
     np.save(os.path.join(outdir, f"rank{rank}.npy"), res, allow_pickle=True)
