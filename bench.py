@@ -265,9 +265,13 @@ def run_ours(args):
     peaks = measured_peaks()
     peak = peaks.get("hbm_gbs", 6650.0)
     clocks = clk.summary()
+    # per L2-blocked launch: one step (33 B/amp incl. E, 257 B/amp on chip) on one
+    # GPU; sharded, the fused [group 0][group 1 + layout swap] pair (32 B/amp,
+    # 208 B/amp on chip: no D, one exchange + one lane-shuffle round for group 1)
+    sup_hbm, sup_onchip = (33, 257) if world == 1 else (32, 208)
     if st["super_launches"] > 0 and st["super_kernel_ms"] > 0:
         kname, nl, kms = "qaa_superpass", st["super_launches"], st["super_kernel_ms"]
-        alg_bytes = nl * 33 * amps
+        alg_bytes = nl * sup_hbm * amps
     else:
         kname = "qaa_pass_tma" if (args.kernel == 1 and world == 1) else "qaa_pass_fast"
         nl, kms = npass, st["pass_kernel_ms"]
@@ -290,8 +294,8 @@ def run_ours(args):
         # shared-memory/L1 data path (128 B/clk/SM), 257 B/amp per launch
         sm_hz = (clocks.get("sm_mhz") or 1965.0) * 1e6
         onchip_peak = 128 * 148 * sm_hz / 1e9
-        onchip = 257 * amps / (kms / nl / 1e3) / 1e9
-        roofline["onchip"] = {"bound": "smem/L1 data path", "bytes_per_amp": 257, "achieved": onchip,
+        onchip = sup_onchip * amps / (kms / nl / 1e3) / 1e9
+        roofline["onchip"] = {"bound": "smem/L1 data path", "bytes_per_amp": sup_onchip, "achieved": onchip,
                               "peak": onchip_peak, "unit": "GB/s", "frac": onchip / onchip_peak,
                               "peak_source": "128 B/clk/SM x 148 SMs x median SM clock under load"}
     gpu_launches = st["kernel_launches_total"]

@@ -768,14 +768,19 @@ TmaKernel pick(int prog, bool lane3, int ng) { return ng == 1 ? pick_ng<1>(prog,
 
 cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, int ngroups, bool bd, int grid,
                              cudaStream_t st) {
-  SuperKernel k = pick_super(lane3, ngroups, bd);
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM_BYTES);
-  if (e != cudaSuccess) return e;
+  SuperKernel k = pick_super(lane3, ngroups, bd);  // shared-memory attribute set in pass_tma_setup
   k<<<grid, ngroups * NTHREADS, TMA_SMEM_BYTES, st>>>(*kmap, a);
   return cudaGetLastError();
 }
 
 cudaError_t pass_tma_setup() {
+  for (int l = 0; l < 2; l++)
+    for (int ng = 1; ng <= 2; ng++)
+      for (int bd = 0; bd < 2; bd++) {
+        cudaError_t e = cudaFuncSetAttribute(pick_super(l, ng, bd), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)TMA_SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+      }
   for (int p = 0; p < FP_COUNT; p++)
     for (int l = 0; l < 2; l++)
       for (int ng = 1; ng <= 2; ng++) {
