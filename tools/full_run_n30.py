@@ -35,8 +35,13 @@ out = {"config": "n=30 unique-solution 3-SAT, T=200, K=1e4 (dt=0.02), midpoint s
 idx = np.random.default_rng(7).integers(0, 1 << n, 256)
 
 
+# libqaa enqueues on this (non-default) stream; the timing events go on the same stream
+stream = torch.cuda.Stream(device=0)
+torch.cuda.set_stream(stream)
+
+
 def run(record):
-    with q.Context(0) as c:
+    with q.Context(0, stream=stream.cuda_stream) as c:
         c.load_instance(n, cl)
         c.init_uniform()
         norms, t_dev = [], 0.0
@@ -44,9 +49,9 @@ def run(record):
             s = sched[w * args.window:(w + 1) * args.window]
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
-            ev0.record()
+            ev0.record(stream)
             c.evolve(dt * args.window, args.window, s)
-            ev1.record()
+            ev1.record(stream)
             torch.cuda.synchronize()
             t_dev += ev0.elapsed_time(ev1) / 1e3
             if record:
@@ -81,7 +86,7 @@ if args.oracle_steps > 0 and avail > 1.5 * need:
     t1 = time.time()
     E = oracle.energy_table(n, cl)
     want = oracle.evolve(n, E, oracle.init_uniform(n), dt * k0, k0, sched[:k0])
-    with q.Context(0) as c:
+    with q.Context(0, stream=stream.cuda_stream) as c:
         c.load_instance(n, cl)
         c.init_uniform()
         c.evolve(dt * k0, k0, sched[:k0])
