@@ -563,6 +563,11 @@ struct ClauseRec {
   uint32_t spread[4];
 };
 
+// Each thread handles NB groups of 16 assignments (grid-stride apart, so every
+// store instruction stays coalesced) per pass over the clause list: one clause
+// record load (a shared-memory broadcast) serves NB tests. W32: every
+// assignment fits 32 bits (n <= 32), so the test is one AND + one compare.
+template <bool W32, int NB>
 __global__ void __launch_bounds__(256) energy_table_kernel(uint8_t* E, int64_t N, uint64_t x_offset,
                                                             const ClauseRec* recs, int m, unsigned* d_max,
                                                             unsigned long long* d_zeros, int lowbits, int hishift) {
@@ -575,29 +580,42 @@ __global__ void __launch_bounds__(256) energy_table_kernel(uint8_t* E, int64_t N
   unsigned mx = 0;
   unsigned long long zeros = 0;
   const int64_t ngroups = N >> 4;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups; g += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t p0 = (uint64_t)g << 4;
-    const uint64_t x0 = (p0 & lowmask) | x_offset | ((p0 >> lowbits) << hishift);
-    uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
-    for (int c = 0; c < m; c++) {
-      const ClauseRec r = sr[c];
-      if ((x0 & r.mhi) == r.vhi) {
-        c0 += r.spread[0];
-        c1 += r.spread[1];
-        c2 += r.spread[2];
-        c3 += r.spread[3];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g0 < ngroups; g0 += NB * stride) {
+    uint64_t x0[NB];
+    uint32_t c[NB][4];
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+      const uint64_t p0 = (uint64_t)(g0 + b * stride) << 4;
+      x0[b] = (p0 & lowmask) | x_offset | ((p0 >> lowbits) << hishift);
+      c[b][0] = c[b][1] = c[b][2] = c[b][3] = 0;
+    }
+    for (int k = 0; k < m; k++) {
+      const ClauseRec r = sr[k];
+#pragma unroll
+      for (int b = 0; b < NB; b++) {
+        const bool hit = W32 ? (((uint32_t)x0[b] & (uint32_t)r.mhi) == (uint32_t)r.vhi) : ((x0[b] & r.mhi) == r.vhi);
+        if (hit) {
+          c[b][0] += r.spread[0];
+          c[b][1] += r.spread[1];
+          c[b][2] += r.spread[2];
+          c[b][3] += r.spread[3];
+        }
       }
     }
-    reinterpret_cast<uint4*>(E)[g] = make_uint4(c0, c1, c2, c3);
-    const uint32_t w[4] = {c0, c1, c2, c3};
 #pragma unroll
-    for (int q = 0; q < 4; q++)
+    for (int b = 0; b < NB; b++) {
+      if (g0 + b * stride >= ngroups) break;
+      reinterpret_cast<uint4*>(E)[g0 + b * stride] = make_uint4(c[b][0], c[b][1], c[b][2], c[b][3]);
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const unsigned b = (w[q] >> (8 * j)) & 0xff;
-        mx = b > mx ? b : mx;
-        zeros += b == 0;
-      }
+      for (int q = 0; q < 4; q++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const unsigned v = (c[b][q] >> (8 * j)) & 0xff;
+          mx = v > mx ? v : mx;
+          zeros += v == 0;
+        }
+    }
   }
   // block reduce (integers: order-independent)
   for (int o = 16; o > 0; o >>= 1) {
@@ -637,7 +655,14 @@ cudaError_t launch_energy_table(uint8_t* E, int64_t N, uint64_t x_offset, const 
     int64_t grid = (groups + 255) / 256;
     const int64_t cap = (int64_t)num_sms * 8;
     if (grid > cap) grid = cap;
-    energy_table_kernel<<<(int)grid, 256, 0, st>>>(E, N, x_offset, recs, m, d_max, d_zeros, lowbits, hishift);
+    // every assignment x < x_offset + N fits 32 bits when the highest one does
+    const uint64_t xmax = (uint64_t)(N - 1) | x_offset | (hishift < 64 && lowbits < 64 ?
+                              (((uint64_t)(N - 1) >> lowbits) << hishift) : 0ull);
+    const bool w32 = (xmax >> 32) == 0;
+    if (w32)
+      energy_table_kernel<true, 4><<<(int)grid, 256, 0, st>>>(E, N, x_offset, recs, m, d_max, d_zeros, lowbits, hishift);
+    else
+      energy_table_kernel<false, 4><<<(int)grid, 256, 0, st>>>(E, N, x_offset, recs, m, d_max, d_zeros, lowbits, hishift);
   }
   return cudaGetLastError();
 }
