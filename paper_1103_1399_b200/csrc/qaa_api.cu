@@ -509,7 +509,7 @@ static qaa_status build_tma(qaa_ctx* ctx) {
   // every physical bit outside their tile bits (pass_tma.cu qaa_superpass)
   for (int k = 0; k < 4; k++) ctx->super_ok[k] = false;
   const int P = (int)ctx->geom.groups.size();
-  if (P == 3 && ctx->tma_ok[0])
+  if ((P == 3 || P == 4) && ctx->tma_ok[0])
     for (int k = 1; k < P; k++)
       if (ctx->tma_ok[(size_t)k] &&
           make_super_args(ctx, k, ctx->tma_static[0], ctx->tma_static[(size_t)k], &ctx->super_static[k]))
@@ -990,16 +990,24 @@ static qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<Step
 //   [group 0: rotate step j] [group k: rotate step j, D_{j+1}, rotate step j+1]
 // (k alternating 1, 2); each pair becomes ONE launch over L2-resident chunks,
 // so every Trotter step but the first and last is one HBM round trip.
+// Three tile groups (n <= 30 on one GPU): every pass pair [group 0][group k
+// rotate/D/rotate] fuses. Four groups (n = 31..33): per step [group 0] [group b]
+// [group a rotate/D/rotate]; the plain pair [group 0][group b] fuses (the
+// kernel variant without D), so a step is two HBM round trips instead of three.
 static bool super_usable(qaa_ctx* ctx) {
-  return ctx->super_mode && ctx->world == 1 && ctx->kernel_mode == 1 && ctx->geom.groups.size() == 3 &&
-         ctx->super_ok[1] && ctx->super_ok[2] && (int)ctx->emax + 1 <= TMA_MAX_PHI &&
-         (ctx->super_force ||
-          std::min(ctx->super_static[1].nchunks, ctx->super_static[2].nchunks) >= SUPER_MIN_CHUNKS);
+  const size_t P = ctx->geom.groups.size();
+  if (!(ctx->super_mode && ctx->world == 1 && ctx->kernel_mode == 1 && (P == 3 || P == 4) &&
+        (int)ctx->emax + 1 <= TMA_MAX_PHI))
+    return false;
+  for (size_t k = 1; k < P; k++)
+    if (!ctx->super_ok[k] || (!ctx->super_force && ctx->super_static[k].nchunks < SUPER_MIN_CHUNKS)) return false;
+  return true;
 }
 
 static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_pre, double t_post,
                                     const double2* phi, int n_phi) {
-  const int64_t nch = std::max(ctx->super_static[1].nchunks, ctx->super_static[2].nchunks);
+  int64_t nch = 0;
+  for (size_t g = 1; g < ctx->geom.groups.size() && g < 4; g++) nch = std::max(nch, ctx->super_static[g].nchunks);
   const size_t need = (size_t)nch * sizeof(unsigned) + 256;
   if (ctx->d_super_cap < need) {
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
@@ -1038,8 +1046,9 @@ static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_p
   a.queue = ctx->super_dynamic ? (unsigned long long*)ctx->d_super : nullptr;
   a.done = (unsigned*)((char*)ctx->d_super + 256);
   CUDA_TRY(cudaMemsetAsync(ctx->d_super, 0, 256 + (size_t)a.nchunks * sizeof(unsigned), ctx->stream));
-  return launch_superpass(&ctx->tmaps[(size_t)k], a, (gk.rot_local >> 3) & 1, ctx->super_groups, true, ctx->num_sms,
-                          ctx->stream) == cudaSuccess
+  // phi == nullptr: the plain pair of a four-group plan (kernel variant without D)
+  return launch_superpass(&ctx->tmaps[(size_t)k], a, (gk.rot_local >> 3) & 1, ctx->super_groups, phi != nullptr,
+                          ctx->num_sms, ctx->stream) == cudaSuccess
              ? QAA_OK
              : fail(ctx, QAA_E_CUDA, "superpass launch failed");
 }
@@ -1172,13 +1181,15 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
     if (sup && pi + 1 < plan.size()) {
       // [group 0: pre j] [group k: pre j, D_{j+1}, post j+1] -> one L2-blocked launch
       const PassPlan& pn = plan[pi + 1];
+      const bool with_d = pn.d_step >= 0 && pn.post_step >= 0;
+      const bool plain = pn.d_step < 0 && pn.post_step < 0 && ctx->geom.groups.size() == 4;
       if (pp.group == 0 && pp.pre_step >= 0 && pp.d_step < 0 && pp.post_step < 0 && pn.group >= 1 &&
-          pn.pre_step == pp.pre_step && pn.d_step >= 0 && pn.post_step >= 0 &&
-          ctx->super_ok[(size_t)pn.group] && sc[(size_t)pp.pre_step].form == 0 &&
-          sc[(size_t)pn.post_step].form == 0) {
+          pn.pre_step == pp.pre_step && (with_d || plain) && ctx->super_ok[(size_t)pn.group] &&
+          sc[(size_t)pp.pre_step].form == 0 && (!with_d || sc[(size_t)pn.post_step].form == 0)) {
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
         qaa_status st = launch_super_pair(ctx, pn.group, sc[(size_t)pp.pre_step].coef, sc[(size_t)pn.pre_step].coef,
-                                          sc[(size_t)pn.post_step].coef, dphi + (size_t)pn.d_step * n_phi, n_phi);
+                                          with_d ? sc[(size_t)pn.post_step].coef : 0.0,
+                                          with_d ? dphi + (size_t)pn.d_step * n_phi : nullptr, n_phi);
         if (st) return st;
         if (ctx->profile) {
           CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, ctx->stream));
@@ -1733,7 +1744,7 @@ qaa_status qaa_get_stats(qaa_ctx* ctx, qaa_stats* out) {
   s.row_bits = ctx->row_bits;
   const int P = s.groups;
   s.passes_per_step_num = (ctx->step_spanning && P > 1) ? P - 1 : P;
-  if (ctx->L > RESIDENT_MAX_L && super_usable(ctx) && ctx->step_spanning == 2) s.passes_per_step_num = 1;
+  if (ctx->L > RESIDENT_MAX_L && super_usable(ctx) && ctx->step_spanning == 2) s.passes_per_step_num = P - 2;
   if (ctx->world > 1) s.passes_per_step_num = P;  // sharded: one phase of P passes per step (§7)
   s.passes_per_step_den = 1;
   s.bytes_per_pass = s.amps_local * 32;
