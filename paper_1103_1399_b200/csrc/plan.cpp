@@ -179,8 +179,12 @@ bool build_shard_schedule(const Geometry& geo, int gbits, int64_t K, std::vector
     const int layout = (int)(k & 1);
     ShardPass f{SK_PASS, P - 1, k >= 1 ? k - 1 : -1, k >= 1 ? carried : 0u, k, k, top.rot_local, 0, layout};
     out->push_back(f);
-    for (int g = 0; g <= P - 2; g++)
+    // groups 1..P-3, then 0, then P-2 (remote): group 0 right before the
+    // layout-swap pass, so the pair [0][P-2] can run as one L2-blocked launch
+    for (int i = 0; i <= P - 2; i++) {
+      const int g = i < P - 3 ? i + 1 : (i == P - 3 ? 0 : P - 2);
       out->push_back({SK_PASS, g, k, geo.groups[(size_t)g].rot_local, -1, -1, 0u, g == P - 2 ? 1 : 0, layout});
+    }
   }
   const int lay = (int)(K & 1);
   out->push_back({SK_PASS, P - 1, K - 1, carried, -1, -1, 0u, 0, lay});

@@ -102,8 +102,8 @@ void build_pass_schedule(int ngroups, int64_t K, int step_spanning, std::vector<
 // storing its tiles straight into the peers' next buffers.
 // Step k runs as one phase in layout k % 2:
 //   [top group: rotate the g carried bits for step k-1, D_k, rotate all of
-//    its bits for step k], then groups 0..P-2 rotate for step k, the last of
-//    them storing remotely (layout flips).
+//    its bits for step k], then groups 1..P-3, 0 and P-2 rotate for step k,
+//    the last (P-2) storing remotely (layout flips).
 // After the last phase the carried bits get their step K-1 rotation and, if
 // the state is in layout B, a plain remap returns it to layout A.
 enum ShardKind : int { SK_PASS = 0, SK_REMAP = 1 };

@@ -440,13 +440,15 @@ static bool make_super_args(qaa_ctx* ctx, int k, const TmaArgs& t0, const TmaArg
 // group 1's tensor map over both shard buffers.
 static void build_shard_super(qaa_ctx* ctx) {
   ctx->shard_super_ok = false;
-  if (ctx->geom.groups.size() != 3 || !ctx->bufs[0] || !ctx->bufs[1]) return;
-  TmaArgs t0, t1b[2];
+  const int P = (int)ctx->geom.groups.size();
+  if (P < 3 || !ctx->bufs[0] || !ctx->bufs[1]) return;
+  const int k = P - 2;  // the remote (layout-swap) group, right after group 0 in every phase
+  TmaArgs t0, tkb[2];
   CUtensorMap m0;
   if (!encode_group(ctx, ctx->geom.groups[0], ctx->bufs[0], &m0, &t0) || !t0.contiguous) return;
   for (int b = 0; b < 2; b++)
-    if (!encode_group(ctx, ctx->geom.groups[1], ctx->bufs[b], &ctx->shard_kmap[b], &t1b[b])) return;
-  if (!make_super_args(ctx, 1, t0, t1b[0], &ctx->shard_super)) return;
+    if (!encode_group(ctx, ctx->geom.groups[(size_t)k], ctx->bufs[b], &ctx->shard_kmap[b], &tkb[b])) return;
+  if (!make_super_args(ctx, k, t0, tkb[0], &ctx->shard_super)) return;
   ctx->shard_super_ok = true;
 }
 
@@ -873,11 +875,11 @@ static qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<Step
       // [group 0: rotate][group 1: rotate + layout-swap stores] -> one L2-blocked launch
       const ShardPass& sn = plan[pi + 1];
       if (sp.kind == SK_PASS && sp.group == 0 && sp.pre_step >= 0 && sp.d_step < 0 && sp.post_step < 0 &&
-          !sp.remote && sn.kind == SK_PASS && sn.group == 1 && sn.pre_step >= 0 && sn.d_step < 0 &&
+          !sp.remote && sn.kind == SK_PASS && sn.group == P - 2 && sn.pre_step >= 0 && sn.d_step < 0 &&
           sn.post_step < 0 && sn.remote && sn.layout == sp.layout) {
         SuperArgs a = ctx->shard_super;
         const Group& g0 = ctx->geom.groups[0];
-        const Group& g1 = ctx->geom.groups[1];
+        const Group& g1 = ctx->geom.groups[(size_t)(P - 2)];
         a.g0.psi = ctx->bufs[ctx->cur];
         a.gk.psi = ctx->bufs[ctx->cur];
         a.gk.phi = nullptr;

@@ -50,3 +50,29 @@ def shard_worker(rank, world, port, outdir, n, clauses, T, K, schedule, psi0, s_
     ctx.close()
     dist.barrier()
     dist.destroy_process_group()
+
+
+def shard_closed_form_worker(rank, world, port, outdir, n, clauses, T, K, opts=None):
+    """GPU: sharded s = 1 run at a large size; returns sampled local amplitudes
+    (global indices) and the norm after a few general steps -- no full copy."""
+    import torch
+    dist = _init(rank, world, port)
+    torch.cuda.set_device(0)
+    import paper_1103_1399_b200 as q
+    comm = q.TorchComm()
+    ctx = q.Context(0, rank=rank, world=world, comm=comm)
+    for key, val in (opts or {}).items():
+        ctx.set_option(key, val)
+    ctx.load_instance(n, clauses)
+    L = n - (world.bit_length() - 1)
+    ctx.init_uniform()
+    ctx.evolve(T, K, np.ones(K))
+    rng = np.random.default_rng(n + rank)
+    starts = [int((rank << L) + s) for s in rng.integers(0, (1 << L) - 32, 8)]
+    samples = {s: ctx.state(s, 32) for s in starts}
+    ctx.evolve(0.06, 3)
+    res = {"samples": samples, "norm2": ctx.norm2(), "super_launches": ctx.stats()["super_launches"]}
+    np.save(os.path.join(outdir, f"rank{rank}.npy"), res, allow_pickle=True)
+    ctx.close()
+    dist.barrier()
+    dist.destroy_process_group()

@@ -82,3 +82,32 @@ def test_sharded_uniform_start_paper_config():
     want = oracle.evolve(n, oracle.energy_table(n, cl), oracle.init_uniform(n), T, K)
     assert np.max(np.abs(got - want)) < 1e-10
     assert abs(res[0]["success"] - abs(want[sol]) ** 2) < 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,world", [(32, 2)])
+def test_sharded_four_groups_closed_form(n, world):
+    """Sharded with four local tile groups (2^31 amplitudes per rank, the
+    per-GPU size of the n = 32/33/34 multi-GPU configs), both ranks on one GPU:
+    s = 1 closed form psi_K(x) = 2^{-n/2} e^{-i T E(x)} on sampled x (E from the
+    oracle) through the fused [group 0][group 2 + layout swap] launches, and the
+    norm after general steps."""
+    import torch
+    from oracle import oracle
+    free, _ = torch.cuda.mem_get_info()
+    need = world * (2 * 16 + 6) * (1 << (n - 1)) + (8 << 30)
+    if free < need:
+        pytest.skip(f"needs {need >> 30} GiB free on one GPU, have {free >> 30}")
+    cl = cnf.load_instance(n)[0]
+    T, K = 0.23, 3
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(W.shard_closed_form_worker, args=(world, free_port(), d, n, cl, T, K, None),
+                 nprocs=world, join=True)
+        res = [np.load(os.path.join(d, f"rank{r}.npy"), allow_pickle=True).item() for r in range(world)]
+    for r in res:
+        assert r["super_launches"] > 0
+        assert abs(r["norm2"] - 1.0) < 1e-12
+        for s0, got in r["samples"].items():
+            xs = np.arange(s0, s0 + 32, dtype=np.uint64)
+            want = 2.0 ** (-n / 2) * np.exp(-1j * T * oracle.energy_at(n, cl, xs).astype(float))
+            assert np.max(np.abs(got - want)) < 1e-15
