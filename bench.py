@@ -16,6 +16,12 @@ step loads the instance from host memory, initialises, evolves one window and
 reads P_succ back (H2D/D2H inside the timed region).
 
 `--impl reference` times the CPU oracle (oracle/, as it stands) instead.
+
+With N > 1 GPUs (torchrun) the state is n = 30 + log2 N, 2^30 amplitudes per GPU
+(weak scaling), and `value` is the whole-job aggregate in shard-steps/s: N x the
+Trotter steps/s of the N-GPU state (each GPU advances its 2^30-amplitude shard
+once per step), so at N = 1 it is the plain Trotter steps/s and perfect weak
+scaling gives N x value(1); the raw steps/s of the state is `state_steps_per_s`.
 """
 from __future__ import annotations
 
@@ -153,6 +159,9 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    # the oracle on all of the box's host cores (torchrun exports OMP_NUM_THREADS=1);
+    # set before liboracle (and with it the OpenMP runtime) is first loaded
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())
     n = args.n or (N_DEFAULT + (args.gpus.bit_length() - 1))
     ns = args.cpu_sample_n
     for _ in range(args.warmup):
@@ -162,10 +171,13 @@ def run_reference(args):
         dt, scaled, cores = oracle_sample(n, ns, 1)
         per.append(scaled)
     t_step = float(np.mean(per))
-    val = 1.0 / t_step
+    # whole-job units as in the GPU arm: Trotter steps of 2^30-amplitude shards
+    units = 2.0 ** (n - N_DEFAULT) if args.gpus > 1 else 1.0
+    val = units / t_step
     sample = (f"oracle Trotter step on a seeded n={ns} instance, 1 step per bench step, scaled by "
               f"2^{n - ns}*(n+1)/(n_s+1) to n={n}")
-    line = {"impl": "reference", "metric": "trotter_steps_per_s", "value": val, "unit": "steps/s",
+    line = {"impl": "reference", "metric": "trotter_steps_per_s", "value": val,
+            "unit": "steps/s" if args.gpus == 1 else "shard-steps/s (2^30 amplitudes per shard)",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": f"n={n} unique-solution 3-SAT, T=200, K=1e4 (dt=0.02)",
@@ -252,7 +264,12 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=comm_group)
         ms = float(t.item())
     trotter = args.steps * chunk
-    value = trotter / (ms / 1e3)
+    # whole-job aggregate: N GPUs each advance their 2^L-amplitude shard one
+    # Trotter step per step of the n = 30 + log2 N state, so the units are
+    # shard-steps (= Trotter steps of the n = 30 state at N = 1)
+    shards = world
+    state_steps_per_s = trotter / (ms / 1e3)
+    value = shards * state_steps_per_s
     # roofline of the dominant kernel: algorithmic bytes per launch = 32 B/amp
     # (read + write psi) + 1 B/amp (E) on D launches. With L2-blocked steps
     # (default) the dominant kernel is qaa_superpass: one launch = one Trotter
@@ -334,12 +351,14 @@ def run_ours(args):
             e2e_s = float(t.item())
         h2d = 32 * len(cl) + chunk * ((emax + 1) * 16 + 12)
         d2h = 16 + 8
-        e2e = {"value": e2e_steps * chunk / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": h2d,
+        e2e = {"value": world * e2e_steps * chunk / e2e_s,
+               "unit": "steps/s" if world == 1 else "shard-steps/s (2^30 amplitudes per shard)",
+               "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                "includes": "load_instance (H2D clauses, energy table, Z) + init + evolve(window) + success_prob (D2H)"}
 
     cpu = None
-    if not args.no_cpu_baseline and rank == 0:
+    if not args.no_cpu_baseline and rank == 0 and world == 1:  # contract: rank 0 at N = 1 only
         try:
             dt, scaled, cores = oracle_sample(n, args.cpu_sample_n, 2)
             cpu = {"value": 1.0 / scaled, "unit": "steps/s", "cores": cores, "kind": "oracle",
@@ -349,7 +368,9 @@ def run_ours(args):
             cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": f"failed: {e}"}
     if rank == 0:
-        line = {"metric": "trotter_steps_per_s", "value": value, "unit": "steps/s", "n_gpus": world,
+        line = {"metric": "trotter_steps_per_s", "value": value,
+                "unit": "steps/s" if world == 1 else "shard-steps/s (2^30 amplitudes per shard)",
+                "state_steps_per_s": state_steps_per_s, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
@@ -358,7 +379,7 @@ def run_ours(args):
                            "n": n, "m": len(cl), "chunk": chunk, "row_bits": args.row_bits,
                            "step_spanning": args.step_spanning,
                            "kernel": ("tma" if args.kernel else "register") if world == 1 else
-                           "register + fused peer-store layout swap (sharded)",
+                           "L2-blocked [group 0][group P-2 + peer-store layout swap] + register D pass (sharded)",
                            "shared_gpu_functional_test": bool(args.share_gpu),
                            "passes_per_step":
                                st["passes_per_step_num"] / st["passes_per_step_den"], "tile_groups": st["groups"],
