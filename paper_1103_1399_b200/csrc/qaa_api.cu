@@ -86,9 +86,14 @@ struct qaa_ctx {
   int super_groups = 2;
   int super_hints = 2;
   int super_force = 0;
-  bool shard_super_ok = false;  // sharded plan: fused [group 0][group 1 + layout swap] launches
+  bool shard_super_ok = false;  // sharded plan: fused [group 0][group P-2 + layout swap] launches
   SuperArgs shard_super;
-  CUtensorMap shard_kmap[2];    // group 1 over shard buffer 0 / 1
+  CUtensorMap shard_kmap[2];    // group P-2 over shard buffer 0 / 1
+  bool shard_top_ok = false;    // sharded top-group D passes on the TMA kernel
+  CUtensorMap shard_top_map[2]; // top group over shard buffer 0 / 1
+  TmaArgs shard_top;            // its geometry
+  uint8_t* shard_top_eg[2] = {nullptr, nullptr};  // its permuted energies, layout A / B
+  size_t shard_top_eg_cap = 0;
   int super_dynamic = 0;
   SuperArgs super_static[4];
   bool super_ok[4] = {false, false, false, false};
@@ -248,6 +253,8 @@ void qaa_destroy(qaa_ctx* ctx) {
     if (ctx->bufs[b]) cudaFree(ctx->bufs[b]);
   }
   if (ctx->E_B) cudaFree(ctx->E_B);
+  for (int b = 0; b < 2; b++)
+    if (ctx->shard_top_eg[b]) cudaFree(ctx->shard_top_eg[b]);
   if (ctx->coef_done) cudaEventDestroy(ctx->coef_done);
   for (auto& p : ctx->ev_pool) {
     cudaEventDestroy(p.first);
@@ -438,6 +445,44 @@ static bool make_super_args(qaa_ctx* ctx, int k, const TmaArgs& t0, const TmaArg
 // [group 1 rotate + layout-swap stores] of every phase runs as one L2-blocked
 // launch (pass_tma.cu qaa_superpass without D, remote group-k stores). Needs
 // group 1's tensor map over both shard buffers.
+// Sharded top group (rotate carried bits, D, rotate all) on the TMA kernel:
+// its tensor map over both shard buffers and its energy slices permuted from
+// the layout-A and layout-B tables. Falls back to the register kernel if a map
+// cannot be encoded or the tables do not fit.
+static qaa_status build_shard_top(qaa_ctx* ctx) {
+  ctx->shard_top_ok = false;
+  const int P = (int)ctx->geom.groups.size();
+  if (P < 2 || !ctx->bufs[0] || !ctx->bufs[1] || !ctx->E_B) return QAA_OK;
+  const Group& gt = ctx->geom.groups[(size_t)P - 1];
+  if (gt.rot_local & ~0xFF8u) return QAA_OK;
+  TmaArgs tb[2];
+  for (int b = 0; b < 2; b++)
+    if (!encode_group(ctx, gt, ctx->bufs[b], &ctx->shard_top_map[b], &tb[b]) || tb[b].contiguous) return QAA_OK;
+  const size_t N = (size_t)1 << ctx->L;
+  if (ctx->shard_top_eg_cap < N) {
+    for (int b = 0; b < 2; b++) {
+      if (ctx->shard_top_eg[b]) cudaFree(ctx->shard_top_eg[b]);
+      ctx->shard_top_eg[b] = nullptr;
+    }
+    ctx->shard_top_eg_cap = 0;
+    for (int b = 0; b < 2; b++)
+      if (cudaMalloc(&ctx->shard_top_eg[b], N) != cudaSuccess) {
+        cudaGetLastError();
+        return QAA_OK;  // register-kernel fallback
+      }
+    ctx->shard_top_eg_cap = N;
+  }
+  for (int b = 0; b < 2; b++) {
+    CUDA_TRY(launch_permute_energy(b ? ctx->E_B : ctx->E, ctx->shard_top_eg[b], gt.phys, gt.nseg, gt.seg_src,
+                                   gt.seg_dst, gt.seg_len, gt.ntiles, (gt.rot_local >> 3) & 1, ctx->num_sms,
+                                   ctx->stream));
+    ctx->stats.kernel_launches_total++;
+  }
+  ctx->shard_top = tb[0];
+  ctx->shard_top_ok = true;
+  return QAA_OK;
+}
+
 static void build_shard_super(qaa_ctx* ctx) {
   ctx->shard_super_ok = false;
   const int P = (int)ctx->geom.groups.size();
@@ -758,6 +803,8 @@ qaa_status qaa_load_instance(qaa_ctx* ctx, int n, int m, const int32_t* lits) {
     if (st) return st;
   } else {
     build_shard_super(ctx);
+    qaa_status st = build_shard_top(ctx);
+    if (st) return st;
   }
   ctx->loaded = true;
   return QAA_OK;
@@ -948,6 +995,38 @@ static qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<Step
       fp = d ? FP_GK_PRE_D_POST : FP_GK_PRE;
     if (sp.group == 0 && (d || sp.post_step >= 0)) return fail(ctx, QAA_E_USAGE, "internal: unexpected shard pass");
     if (sp.group > 0 && (gr.rot_local & ~0xFF8u)) return fail(ctx, QAA_E_USAGE, "sharded plan needs row_bits >= 3");
+    if (d && sp.group == P - 1 && !sp.remote && ctx->shard_top_ok && ctx->kernel_mode == 1 &&
+        n_phi <= TMA_MAX_PHI) {
+      // top group: carried bits of step k-1, D_k, all its bits of step k -- TMA kernel
+      TmaArgs ta = ctx->shard_top;
+      ta.psi = ctx->bufs[ctx->cur];
+      ta.Eg = ctx->shard_top_eg[sp.layout];
+      ta.phi = dphi + (size_t)sp.d_step * n_phi;
+      ta.n_phi = n_phi;
+      for (int b = 0; b < TILE_BITS; b++) {
+        ta.t[0][b] = (sp.pre_step >= 0 && ((sp.pre_local >> b) & 1)) ? sc[(size_t)sp.pre_step].coef : 0.0;
+        ta.t[1][b] = (sp.post_step >= 0 && ((sp.post_local >> b) & 1)) ? sc[(size_t)sp.post_step].coef : 0.0;
+        ta.phys[b] = gr.phys[b];
+      }
+      ta.ntiles = gr.ntiles;
+      ta.nseg = gr.nseg;
+      for (int q = 0; q < MAX_SEGS; q++) {
+        ta.seg_src[q] = gr.seg_src[q];
+        ta.seg_dst[q] = gr.seg_dst[q];
+        ta.seg_len[q] = gr.seg_len[q];
+      }
+      const int tgrid = (int)std::min<int64_t>(gr.ntiles / 2, ctx->num_sms);
+      if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
+      CUDA_TRY(launch_pass_tma(&ctx->shard_top_map[ctx->cur], ta, FP_GK_PRE_D_POST, (gr.rot_local >> 3) & 1,
+                               ctx->tma_groups ? ctx->tma_groups : 2, tgrid, ctx->stream));
+      if (ctx->profile) {
+        CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, ctx->stream));
+        ctx->ev_used++;
+      }
+      ctx->stats.pass_launches++;
+      ctx->stats.kernel_launches_total++;
+      continue;
+    }
     fa.psi = ctx->bufs[ctx->cur];
     fa.E = sp.layout ? ctx->E_B : ctx->E;
     fa.phi = d ? dphi + (size_t)sp.d_step * n_phi : nullptr;
