@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--step-spanning", type=int, default=2,
                     help="2 = D only on strided groups (default), 1 = cyclic, 0 = no spanning")
     ap.add_argument("--ctas-per-sm", type=int, default=1)
-    ap.add_argument("--kernel", type=int, default=1, help="1 = TMA warp-specialised pass, 0 = register pass")
+    ap.add_argument("--kernel", type=int, default=2,
+                    help="QAA_OPT_KERNEL: 2 = auto (default; TMA kernels at the bench sizes), 1 = TMA, 0 = register")
     ap.add_argument("--tma-groups", type=int, default=0, help="0 = auto, 1 or 2 consumer groups per TMA CTA")
     ap.add_argument("--super", type=int, default=1,
                     help="QAA_OPT_SUPER bits (1 = L2-blocked Trotter steps, default; 0 = two HBM passes per step)")
@@ -290,7 +291,7 @@ def run_ours(args):
         kname, nl, kms = "qaa_superpass", st["super_launches"], st["super_kernel_ms"]
         alg_bytes = nl * sup_hbm * amps
     else:
-        kname = "qaa_pass_tma" if (args.kernel == 1 and world == 1) else "qaa_pass_fast"
+        kname = "qaa_pass_fast" if (args.kernel == 0 or (args.kernel == 2 and L <= 19)) else "qaa_pass_tma"
         nl, kms = npass, st["pass_kernel_ms"]
         alg_bytes = npass * 32 * amps + n_d * amps
     achieved = alg_bytes / (kms / 1e3) / 1e9 if kms > 0 else None
@@ -378,7 +379,8 @@ def run_ours(args):
                                        f"{chunk} Trotter steps + P_succ per bench step",
                            "n": n, "m": len(cl), "chunk": chunk, "row_bits": args.row_bits,
                            "step_spanning": args.step_spanning,
-                           "kernel": ("tma" if args.kernel else "register") if world == 1 else
+                           "kernel": ("register" if args.kernel == 0 or (args.kernel == 2 and L <= 19) else "tma")
+                           if world == 1 else
                            "L2-blocked [group 0][group P-2 + peer-store layout swap] + register D pass (sharded)",
                            "shared_gpu_functional_test": bool(args.share_gpu),
                            "passes_per_step":

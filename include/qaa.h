@@ -228,9 +228,11 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        0 = one D per step in the first pass only (P passes/step).
  *  QAA_OPT_CTAS_PER_SM   register-kernel variant: 1 = one CTA per SM with register
  *                        double-buffered prefetch, 2 = two CTAs per SM, no prefetch.
- *  QAA_OPT_KERNEL        1 (default) = warp-specialised TMA pass kernel (producer warp +
- *                        two consumer groups, mbarrier ring of 3 shared-memory slots),
- *                        0 = register-prefetch pass kernel.
+ *  QAA_OPT_KERNEL        2 (default) = auto: the register-prefetch kernel up to 19 local
+ *                        qubits (latency-bound passes), the TMA kernels above;
+ *                        1 = always the TMA pass kernels (mbarrier ring of 3 shared-memory
+ *                        slots, 1-2 consumer groups; the L2-blocked step needs them);
+ *                        0 = always the register-prefetch pass kernel.
  *  QAA_OPT_TMA_GROUPS    consumer groups (8 warps each) per TMA CTA: 0 = auto (1 for
  *                        passes without D: two tiles in flight; 2 for D passes: two
  *                        groups overlap their transposes and FMAs), or force 1 / 2.

@@ -80,7 +80,7 @@ struct qaa_ctx {
   int order = 1;  // 1: Lie-Trotter (D then X, R7); 2: Strang (half D, X, half D; NEXT F4)
   double drv_x = 0.0, drv_z = 0.0;  // driving term s(1-s)(g_x H_B + g_z H_P) (NEXT F4, R3)
   int ctas_per_sm = 1;
-  int kernel_mode = 1;  // 1: TMA warp-specialised pass, 0: register-prefetch pass
+  int kernel_mode = 2;  // 1: TMA pass kernels, 0: register-prefetch pass, 2: auto (register up to L = 19)
   int tma_groups = 0;   // consumer groups per TMA CTA: 0 = auto (1 without D, 2 with D)
   int super_mode = 1;   // L2-blocked D passes (qaa_superpass) when the plan has 3 tile groups
   int super_groups = 2;
@@ -309,7 +309,7 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       ctx->tma_groups = (int)value;
       return QAA_OK;
     case QAA_OPT_KERNEL:
-      if (value < 0 || value > 1) return fail(ctx, QAA_E_USAGE, "kernel mode must be 0 or 1");
+      if (value < 0 || value > 2) return fail(ctx, QAA_E_USAGE, "kernel mode must be 0, 1 or 2 (auto)");
       ctx->kernel_mode = (int)value;
       return QAA_OK;
     case QAA_OPT_CTAS_PER_SM:
@@ -891,6 +891,15 @@ static qaa_status ensure_events(qaa_ctx* ctx, size_t need) {
 // Sharded evolve (plan.hpp ShardPass): every phase ends with a
 // pass whose tiles are stored straight into the peers' other shard buffer
 // (the bit swap of the top local and the rank qubits), then one host barrier.
+// Pass-kernel choice. Auto: the register-prefetch kernel while the state is
+// small enough for a pass to be latency-bound (L <= 19: a few dozen tiles, the
+// LDG path has the shorter tile latency, measured 30 % faster at n = 13..19),
+// the TMA kernels above (n = 23..27: 20-30 % faster; the L2-blocked step from 28).
+constexpr int AUTO_REGISTER_MAX_L = 19;
+static bool use_tma(const qaa_ctx* ctx) {
+  return ctx->kernel_mode == 1 || (ctx->kernel_mode == 2 && ctx->L > AUTO_REGISTER_MAX_L);
+}
+
 static qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<StepCoef>& sc, const double2* dphi,
                                  int n_phi) {
   for (int64_t k = 0; k < K; k++)
@@ -909,7 +918,7 @@ static qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<Step
   fa.n_phi = n_phi;
   fa.gshift = ctx->L - ctx->gbits;
   fa.rank = ctx->rank;
-  const bool fuse = ctx->shard_super_ok && ctx->super_mode && ctx->kernel_mode == 1 &&
+  const bool fuse = ctx->shard_super_ok && ctx->super_mode && use_tma(ctx) &&
                     (ctx->super_force || ctx->shard_super.nchunks >= SUPER_MIN_CHUNKS);
   for (size_t pi = 0; pi < plan.size(); pi++) {
     const ShardPass& sp = plan[pi];
@@ -995,7 +1004,7 @@ static qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<Step
       fp = d ? FP_GK_PRE_D_POST : FP_GK_PRE;
     if (sp.group == 0 && (d || sp.post_step >= 0)) return fail(ctx, QAA_E_USAGE, "internal: unexpected shard pass");
     if (sp.group > 0 && (gr.rot_local & ~0xFF8u)) return fail(ctx, QAA_E_USAGE, "sharded plan needs row_bits >= 3");
-    if (d && sp.group == P - 1 && !sp.remote && ctx->shard_top_ok && ctx->kernel_mode == 1 &&
+    if (d && sp.group == P - 1 && !sp.remote && ctx->shard_top_ok && use_tma(ctx) &&
         n_phi <= TMA_MAX_PHI) {
       // top group: carried bits of step k-1, D_k, all its bits of step k -- TMA kernel
       TmaArgs ta = ctx->shard_top;
@@ -1077,7 +1086,7 @@ static qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<Step
 // kernel variant without D), so a step is two HBM round trips instead of three.
 static bool super_usable(qaa_ctx* ctx) {
   const size_t P = ctx->geom.groups.size();
-  if (!(ctx->super_mode && ctx->world == 1 && ctx->kernel_mode == 1 && (P == 3 || P == 4) &&
+  if (!(ctx->super_mode && ctx->world == 1 && use_tma(ctx) && (P == 3 || P == 4) &&
         (int)ctx->emax + 1 <= TMA_MAX_PHI))
     return false;
   for (size_t k = 1; k < P; k++)
@@ -1297,7 +1306,7 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
       else if (d && post) fp = FP_GK_PRE_D_POST;  // without pre: its t0 row is all zeros
     }
     if ((pre && sc[(size_t)pp.pre_step].form != 0) || (post && sc[(size_t)pp.post_step].form != 0)) fp = -1;
-    if (fp >= 0 && ctx->kernel_mode == 1 && ctx->tma_ok[(size_t)pp.group] && n_phi <= TMA_MAX_PHI) {
+    if (fp >= 0 && use_tma(ctx) && ctx->tma_ok[(size_t)pp.group] && n_phi <= TMA_MAX_PHI) {
       TmaArgs ta = ctx->tma_static[(size_t)pp.group];
       ta.psi = ctx->state;
       ta.phi = d ? dphi + (size_t)pp.d_step * n_phi : nullptr;
