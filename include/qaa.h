@@ -156,8 +156,8 @@ qaa_status qaa_sigma_x(qaa_ctx* ctx, double* out);
  * of the loaded instance, replica r for total time T[r] in K[r] steps of the
  * midpoint schedule (splitting order of QAA_OPT_ORDER), all in ONE launch with
  * the state resident in shared memory (no HBM traffic): one CTA per replica for
- * n <= 12, one thread-block cluster of 2^(n-13) CTAs (2^13 amplitudes each,
- * cluster qubits exchanged through distributed shared memory) for 13 <= n <= 16;
+ * n <= 13, one thread-block cluster of 2^(n-13) CTAs (2^13 amplitudes each,
+ * cluster qubits exchanged through distributed shared memory) for 14 <= n <= 16;
  * out[r] = P_succ of replica r (host array of nrep doubles). The context's own
  * state is not touched. Synchronises.
  * Errors: USAGE (world > 1, n > 16, nrep < 1, NULL arrays, T[r] < 0 or not

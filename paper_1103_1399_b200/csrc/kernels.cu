@@ -396,7 +396,7 @@ cudaError_t launch_sweep(const SweepArgs& a, int nrep, cudaStream_t st) {
 // barriers per step instead of two per bit) was measured 4x slower at n = 16. Shared memory holds amplitude x at x ^ ((x>>4)&7):
 // every phase's quarter-warp then hits 8 distinct 16-byte bank groups.
 namespace cg = cooperative_groups;
-constexpr int SWEEP_LB = 13;  // local bits per CTA
+constexpr int SWEEP_LB = 13;  // max local bits per CTA (2^13 amplitudes, 128 KiB)
 
 __device__ __forceinline__ int sw_pos(int x) { return x ^ ((x >> 4) & 7); }
 __device__ __forceinline__ uint32_t dsmem_map(const void* p, uint32_t rank) {
@@ -412,11 +412,12 @@ __device__ __forceinline__ double2 ld_dsmem(uint32_t addr) {
   return v;
 }
 // amplitude index of register r of thread t in the phase whose register bits
-// are R[0..3] (the 9 thread bits fill the other local bits in increasing order)
+// are R[0..3] (the LB-4 thread bits fill the other local bits in increasing order)
+template <int LB>
 __device__ __forceinline__ int sw_index(int t, int r, const int (&R)[4]) {
   int x = 0, tb = 0;
 #pragma unroll
-  for (int b = 0; b < SWEEP_LB; b++) {
+  for (int b = 0; b < LB; b++) {
     int rb = -1;
 #pragma unroll
     for (int i = 0; i < 4; i++)
@@ -429,14 +430,16 @@ __device__ __forceinline__ int sw_index(int t, int r, const int (&R)[4]) {
   return x;
 }
 
-template <int FORM>
+// one register phase: 16 amplitudes per thread whose indices differ in the
+// register bits R; the first nrot of them are rotated (D fused when phi != 0)
+template <int FORM, int LB>
 __device__ __forceinline__ void sw_phase(double2* s, const uint8_t* e, const double2* phi, int t, int nrot,
                                          const int (&R)[4], double c) {
   double2 v[16];
   int pos[16];
 #pragma unroll
   for (int r = 0; r < 16; r++) {
-    const int x = sw_index(t, r, R);
+    const int x = sw_index<LB>(t, r, R);
     pos[r] = sw_pos(x);
     v[r] = s[pos[r]];
     if (phi) {  // D_k (first phase): psi[x] <- Phi_k[E[x]] psi[x]
@@ -454,17 +457,25 @@ __device__ __forceinline__ void sw_phase(double2* s, const uint8_t* e, const dou
   for (int r = 0; r < 16; r++) s[pos[r]] = v[r];
 }
 
-template <int FORM>
+// one Trotter step of a replica: D fused into the first of the register
+// phases over the LB local bits ({0-3} {4-7} {8-11} {12}; the last phase of an
+// LB < 12 state re-uses lower bits unrotated), then one DSMEM phase per cluster bit
+template <int FORM, int LB>
 __device__ __forceinline__ void sw_step(double2* s, const uint8_t* e, const double2* phi, int t, double c,
                                         cg::cluster_group& cl, int cb, int q) {
-  const int R0[4] = {0, 1, 2, 3}, R1[4] = {4, 5, 6, 7}, R2[4] = {8, 9, 10, 11}, R3[4] = {12, 9, 10, 11};
-  sw_phase<FORM>(s, e, phi, t, 4, R0, c);
+  constexpr int NT = 1 << (LB - 4);
+  const int R0[4] = {0, 1, 2, 3}, R1[4] = {4, 5, 6, 7};
+  const int R2[4] = {8, LB > 9 ? 9 : 4, LB > 10 ? 10 : 5, LB > 11 ? 11 : (LB > 10 ? 7 : 6)};
+  const int R3[4] = {12, 9, 10, 11};
+  sw_phase<FORM, LB>(s, e, phi, t, 4, R0, c);
   __syncthreads();
-  sw_phase<FORM>(s, e, nullptr, t, 4, R1, c);
+  sw_phase<FORM, LB>(s, e, nullptr, t, 4, R1, c);
   __syncthreads();
-  sw_phase<FORM>(s, e, nullptr, t, 4, R2, c);
-  __syncthreads();
-  sw_phase<FORM>(s, e, nullptr, t, 1, R3, c);
+  sw_phase<FORM, LB>(s, e, nullptr, t, LB >= 12 ? 4 : LB - 8, R2, c);
+  if (LB == 13) {
+    __syncthreads();
+    sw_phase<FORM, LB>(s, e, nullptr, t, 1, R3, c);
+  }
   for (int b = 0; b < cb; b++) {
     cl.sync();  // every CTA's phase writes are visible
     // partner CTA's copy of my positions, through the shared::cluster window
@@ -472,50 +483,52 @@ __device__ __forceinline__ void sw_step(double2* s, const uint8_t* e, const doub
     double2 v[16];
 #pragma unroll
     for (int i = 0; i < 16; i++) {
-      const int p = t + 512 * i;  // any bijection: own and partner amplitude share the position
+      const int p = t + NT * i;  // any bijection: own and partner amplitude share the position
       const double2 a = s[p], w = ld_dsmem(rbase + 16u * (uint32_t)p);
       v[i] = FORM == 0 ? make_double2(fma(-c, w.y, a.x), fma(c, w.x, a.y))
                        : make_double2(fma(c, a.x, -w.y), fma(c, a.y, w.x));
     }
     cl.sync();  // the partner has read my old values
 #pragma unroll
-    for (int i = 0; i < 16; i++) s[t + 512 * i] = v[i];
+    for (int i = 0; i < 16; i++) s[t + NT * i] = v[i];
   }
   __syncthreads();  // the next step's first phase reads other threads' amplitudes
 }
 
-__global__ void __launch_bounds__(512, 1) qaa_sweep_cluster_kernel(const SweepArgs a) {
+template <int LB>
+__global__ void __launch_bounds__(1 << (LB - 4), 1) qaa_sweep_cluster_kernel(const SweepArgs a) {
+  constexpr int NT = 1 << (LB - 4), N = 1 << LB;
   cg::cluster_group cl = cg::this_cluster();
   const int C = (int)cl.num_blocks(), q = (int)cl.block_rank();
-  const int cb = a.L - SWEEP_LB, r = blockIdx.x / C, t = threadIdx.x;
+  const int cb = a.L - LB, r = blockIdx.x / C, t = threadIdx.x;
   extern __shared__ double2 smem[];
   double2* s = smem;
-  uint8_t* e = reinterpret_cast<uint8_t*>(smem + (1 << SWEEP_LB));
+  uint8_t* e = reinterpret_cast<uint8_t*>(smem + N);
   __shared__ double red[32];
   __shared__ double part;
   const int64_t K = a.K[r], off = a.row_off[r];
-  for (int x = t; x < (1 << SWEEP_LB); x += 512) {
+  for (int x = t; x < N; x += NT) {
     s[x] = make_double2(a.amp0, 0.0);
-    e[x] = a.E[((int64_t)q << SWEEP_LB) | x];
+    e[x] = a.E[((int64_t)q << LB) | x];
   }
   __syncthreads();
   for (int64_t k = 0; k < K; k++) {
     const double2* phi = a.phi_all + (off + k) * a.n_phi;
     if (a.form[off + k] == 0)
-      sw_step<0>(s, e, phi, t, a.coef[off + k], cl, cb, q);
+      sw_step<0, LB>(s, e, phi, t, a.coef[off + k], cl, cb, q);
     else
-      sw_step<1>(s, e, phi, t, a.coef[off + k], cl, cb, q);
+      sw_step<1, LB>(s, e, phi, t, a.coef[off + k], cl, cb, q);
   }
   if (a.final_d) {  // Strang: closing half step D(s_{K-1})^{1/2}
     const double2* phi = a.phi_all + (off + K) * a.n_phi;
-    for (int x = t; x < (1 << SWEEP_LB); x += 512) {
+    for (int x = t; x < N; x += NT) {
       const double2 f = phi[e[x]], v = s[sw_pos(x)];
       s[sw_pos(x)] = make_double2(fma(f.x, v.x, -f.y * v.y), fma(f.x, v.y, f.y * v.x));
     }
     __syncthreads();
   }
   double acc[1] = {0.0};
-  for (int x = t; x < (1 << SWEEP_LB); x += 512)
+  for (int x = t; x < N; x += NT)
     if (e[x] == 0) {
       const double2 v = s[sw_pos(x)];
       acc[0] += fma(v.x, v.x, v.y * v.y);
@@ -531,14 +544,16 @@ __global__ void __launch_bounds__(512, 1) qaa_sweep_cluster_kernel(const SweepAr
   cl.sync();  // keep every CTA's shared memory alive until rank 0 has read it
 }
 
-cudaError_t launch_sweep_cluster(const SweepArgs& a, int nrep, cudaStream_t st) {
-  const size_t smem = (sizeof(double2) + 1) * ((size_t)1 << SWEEP_LB);
-  cudaError_t e = cudaFuncSetAttribute(qaa_sweep_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int LB>
+static cudaError_t launch_sweep_lb(const SweepArgs& a, int nrep, cudaStream_t st) {
+  const size_t smem = (sizeof(double2) + 1) * ((size_t)1 << LB);
+  cudaError_t e =
+      cudaFuncSetAttribute(qaa_sweep_cluster_kernel<LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int C = 1 << (a.L - SWEEP_LB);
+  const int C = 1 << (a.L - LB);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(nrep * C));
-  cfg.blockDim = dim3(512);
+  cfg.blockDim = dim3(1u << (LB - 4));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -548,9 +563,19 @@ cudaError_t launch_sweep_cluster(const SweepArgs& a, int nrep, cudaStream_t st) 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, qaa_sweep_cluster_kernel, a);
+  e = cudaLaunchKernelEx(&cfg, qaa_sweep_cluster_kernel<LB>, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_cluster(const SweepArgs& a, int nrep, cudaStream_t st) {
+  switch (a.L < SWEEP_LB ? a.L : SWEEP_LB) {
+    case 10: return launch_sweep_lb<10>(a, nrep, st);
+    case 11: return launch_sweep_lb<11>(a, nrep, st);
+    case 12: return launch_sweep_lb<12>(a, nrep, st);
+    case 13: return launch_sweep_lb<13>(a, nrep, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 // ------------------------------------------------------------------ energy table

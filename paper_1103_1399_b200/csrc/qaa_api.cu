@@ -1797,7 +1797,7 @@ qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, 
   a.final_d = ctx->order == 2 ? 1 : 0;
   double* dout = (double*)(db + ((used + 15) & ~(size_t)15));
   a.out = dout;
-  if (ctx->L > RESIDENT_MAX_L)
+  if (ctx->L >= 10)  // register phases, one CTA (n <= 13) or one cluster (n = 14..16) per replica
     CUDA_TRY(launch_sweep_cluster(a, nrep, ctx->stream));
   else
     CUDA_TRY(launch_sweep(a, nrep, ctx->stream));

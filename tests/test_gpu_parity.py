@@ -414,11 +414,12 @@ def test_strang_parity(q, ctx, orc, n, span, kernel):
     ctx.set_option(q.OPT_ORDER, 1)
 
 
-@pytest.mark.parametrize("n", [6, 8, 12, 13, 14, 15, 16])
+@pytest.mark.parametrize("n", [6, 8, 10, 11, 12, 13, 14, 15, 16])
 @pytest.mark.parametrize("order", [1, 2])
 def test_sweep_parity(q, ctx, orc, n, order):
-    """NEXT F1: batched T sweep (one CTA per replica up to n = 12, one cluster of
-    2^(n-13) CTAs with DSMEM exchange for n = 13..16) against one oracle run per
+    """NEXT F1: batched T sweep (one CTA per replica up to n = 13 -- per-qubit
+    loop below n = 10, 16-amplitude register phases from 10 --, one cluster of
+    2^(n-13) CTAs with DSMEM exchange for n = 14..16) against one oracle run per
     replica (configs[1]-style sweep T in {1,2,5,10,20} at dt = 0.05)."""
     cl = cnf.paper_instance()[1] if n == 6 else instance(n)
     ctx.set_option(q.OPT_ORDER, order)

@@ -4,8 +4,8 @@ python - <<'PY'
 import sys, time; sys.path.insert(0,'.')
 import numpy as np, torch, paper_1103_1399_b200 as q
 from inputs import cnf
-for n in (12, 14, 16):
-    cl = cnf.load_instance(n)[0]
+for n in (8, 10, 12, 13, 14, 16):
+    cl = cnf.load_instance(n)[0] if n in (8,10,12,13,14,16) else None
     with q.Context(0) as c:
         c.load_instance(n, cl)
         Ts = np.array([1, 2, 5, 10, 20, 50, 100, 200, 1, 2, 5, 10, 20, 50, 100, 200], dtype=float)
