@@ -290,6 +290,8 @@ def run_ours(args):
     if st["super_launches"] > 0 and st["super_kernel_ms"] > 0:
         kname, nl, kms = "qaa_superpass", st["super_launches"], st["super_kernel_ms"]
         alg_bytes = nl * sup_hbm * amps
+        if world == 1:  # one launch per evolve call is the closing pair, without D
+            alg_bytes -= args.steps * amps
     else:
         kname = "qaa_pass_fast" if (args.kernel == 0 or (args.kernel == 2 and L <= 19)) else "qaa_pass_tma"
         nl, kms = npass, st["pass_kernel_ms"]

@@ -240,7 +240,7 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        tile groups (22 <= n <= 30 on one GPU) and schedule mode 2: each pass
  *                        pair [group 0 rotate][group k rotate, D, rotate] runs as ONE launch
  *                        over 32 MiB chunks resident in L2, one HBM round trip per step
- *                        (K + 2 launches for K steps); bit 1: one consumer group per CTA
+ *                        (K + 1 launches for K steps: the closing plain pair fuses too); bit 1: one consumer group per CTA
  *                        (default two); bits 2-3: L2 eviction hints (0 = evict-last for the
  *                        group-0 output read back by the group-k sub-pass and evict-first
  *                        for dead data; 1 = no hints; 2 = evict-first only); bit 4: use it

@@ -1272,7 +1272,8 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
       // [group 0: pre j] [group k: pre j, D_{j+1}, post j+1] -> one L2-blocked launch
       const PassPlan& pn = plan[pi + 1];
       const bool with_d = pn.d_step >= 0 && pn.post_step >= 0;
-      const bool plain = pn.d_step < 0 && pn.post_step < 0 && ctx->geom.groups.size() == 4;
+      // plain pair: every step of a four-group plan, and the closing pair of a call
+      const bool plain = pn.d_step < 0 && pn.post_step < 0;
       if (pp.group == 0 && pp.pre_step >= 0 && pp.d_step < 0 && pp.post_step < 0 && pn.group >= 1 &&
           pn.pre_step == pp.pre_step && (with_d || plain) && ctx->super_ok[(size_t)pn.group] &&
           sc[(size_t)pp.pre_step].form == 0 && (!with_d || sc[(size_t)pn.post_step].form == 0)) {

@@ -352,8 +352,8 @@ def test_super_pass_parity(q, ctx, orc, n, sup, K):
     assert_close(got, want)
     st = ctx.stats()
     if sup & 1:
-        assert st["pass_launches"] == K + 2  # first pass, K-1 fused pairs, final two passes
-        assert st["super_launches"] == K - 1
+        assert st["pass_launches"] == K + 1  # first pass, K-1 fused pairs, the fused closing pair
+        assert st["super_launches"] == K
 
 
 @pytest.mark.parametrize("n", [22, 24, 27, 30, 31])
@@ -375,9 +375,9 @@ def test_super_bitwise_equals_two_pass(q, n):
         c.init_uniform()
         c.evolve(1.7, K, sched)
         st = c.stats()
-        # three tile groups: K - 1 fused [G0][Gk D] pairs; four (n = 31): one fused
-        # plain pair [G0][Gb] per step
-        assert (st["super_launches"] == (K if n >= 31 else K - 1)) if sup else (st["super_launches"] == 0)
+        # three tile groups: K - 1 fused [G0][Gk D] pairs + the fused closing pair;
+        # four (n = 31): one fused plain pair [G0][Gb] per step
+        assert (st["super_launches"] == K) if sup else (st["super_launches"] == 0)
         if sup:  # the default (bit 4 clear) picks the L2-blocked step only from n = 28 up
             c2 = q.Context(0)
             c2.load_instance(n, cl)
