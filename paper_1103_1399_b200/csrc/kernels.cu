@@ -544,6 +544,59 @@ __global__ void __launch_bounds__(1 << (LB - 4), 1) qaa_sweep_cluster_kernel(con
   cl.sync();  // keep every CTA's shared memory alive until rank 0 has read it
 }
 
+// Single evolution resident in one CTA for 10 <= L <= 12 (qaa_evolve): the
+// sweep's register phases over a swizzled shared-memory copy of the state,
+// loaded from and stored back to psi (SURVEY §7 hard part 5).
+template <int LB>
+__global__ void __launch_bounds__(1 << (LB - 4), 1) qaa_resident_phase_kernel(const ResidentArgs a) {
+  constexpr int NT = 1 << (LB - 4), N = 1 << LB;
+  cg::cluster_group cl = cg::this_cluster();  // a cluster of one: sw_step's cluster phase is empty
+  extern __shared__ double2 smem[];
+  double2* s = smem;
+  uint8_t* e = reinterpret_cast<uint8_t*>(smem + N);
+  const int t = threadIdx.x;
+  for (int x = t; x < N; x += NT) {
+    s[sw_pos(x)] = a.psi[x];
+    e[x] = a.E[x];
+  }
+  __syncthreads();
+  for (int64_t k = 0; k < a.K; k++) {
+    const double2* phi = a.phi_all + k * a.n_phi;
+    if (a.form[k] == 0)
+      sw_step<0, LB>(s, e, phi, t, a.coef[k], cl, 0, 0);
+    else
+      sw_step<1, LB>(s, e, phi, t, a.coef[k], cl, 0, 0);
+  }
+  if (a.final_d) {  // Strang: closing half step D(s_{K-1})^{1/2}
+    const double2* phi = a.phi_all + a.K * a.n_phi;
+    for (int x = t; x < N; x += NT) {
+      const double2 f = phi[e[x]], v = s[sw_pos(x)];
+      s[sw_pos(x)] = make_double2(fma(f.x, v.x, -f.y * v.y), fma(f.x, v.y, f.y * v.x));
+    }
+    __syncthreads();
+  }
+  for (int x = t; x < N; x += NT) a.psi[x] = s[sw_pos(x)];
+}
+
+template <int LB>
+static cudaError_t launch_resident_lb(const ResidentArgs& a, cudaStream_t st) {
+  const size_t smem = (sizeof(double2) + 1) * ((size_t)1 << LB);
+  cudaError_t e =
+      cudaFuncSetAttribute(qaa_resident_phase_kernel<LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  qaa_resident_phase_kernel<LB><<<1, 1 << (LB - 4), smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_resident_phases(const ResidentArgs& a, cudaStream_t st) {
+  switch (a.L) {
+    case 10: return launch_resident_lb<10>(a, st);
+    case 11: return launch_resident_lb<11>(a, st);
+    case 12: return launch_resident_lb<12>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <int LB>
 static cudaError_t launch_sweep_lb(const SweepArgs& a, int nrep, cudaStream_t st) {
   const size_t smem = (sizeof(double2) + 1) * ((size_t)1 << LB);

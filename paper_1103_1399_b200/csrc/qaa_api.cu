@@ -1234,7 +1234,10 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
       if (st) return st;
       CUDA_TRY(cudaEventRecord(ctx->ev_pool[ev].first, ctx->stream));
     }
-    CUDA_TRY(launch_resident(ra, ctx->stream));
+    if (ctx->L >= 10)
+      CUDA_TRY(launch_resident_phases(ra, ctx->stream));
+    else
+      CUDA_TRY(launch_resident(ra, ctx->stream));
     if (ctx->profile) {
       CUDA_TRY(cudaEventRecord(ctx->ev_pool[ev].second, ctx->stream));
       ctx->ev_used = ev + 1;
