@@ -501,14 +501,18 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_pass_tma(const __grid_co
 // tiles of the chunk (128-byte strided rows) then hit L2, and their dirty
 // lines leave L2 as write-backs.
 //
-// Work is one global queue: A(0), then for c = 0..nch-1: [A(c+1)] B(c), where
-// A(c) = the group-0 tiles of chunk c and B(c) = its group-k tiles. B(c) needs
-// every A(c) tile stored (done[c] == 2^tpc_bits); the one-segment lag keeps two
-// chunks live in L2. The issuing thread never waits: an unmet dependency marks
-// the slot "deferred", and the owning group -- whose own later items were all
-// fetched after it, so hold nothing chunk c needs -- waits and loads it itself.
-// A group's items are fetched in order (item J is fetched when J-3 is freed,
-// and J-3, J-1 belong to the same group), so its first END is its last item.
+// Work is one sequence: A(0), then for c = 0..nch-1: [A(c+1)] B(c), where
+// A(c) = the group-0 tiles of chunk c and B(c) = its group-k tiles, dealt
+// round robin (tile J of CTA b = item b + J gridDim.x; optionally through a
+// global atomic counter). B(c) needs every A(c) tile stored (done[c] ==
+// 2^tpc_bits); the one-segment lag keeps two chunks live in L2. The issuing
+// thread never waits: an unmet dependency marks the slot "deferred", and the
+// owning group -- whose own later items all come later in the sequence, so hold
+// nothing chunk c needs -- waits and loads it itself. A group's items are taken
+// in sequence order (item J is fetched when J-3 is freed, and J-3, J-1 belong
+// to the same group), so its first END is its last item. Without D (BD = false)
+// the group-k sub-pass is a plain rotate, optionally storing into the peers'
+// next shard buffers (the sharded plan's layout swap).
 // ============================================================================
 __device__ __forceinline__ uint32_t pdep32(uint32_t x, uint32_t mask) {
   uint32_t r = 0;
