@@ -248,6 +248,8 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        and is chosen otherwise; bit 5: hand out the tiles through a
  *                        global atomic work queue instead of the static round robin
  *                        (measured 2-4 % slower).
+ *  QAA_OPT_ENERGY_W64    test hook: 1 = the 64-bit energy-table kernel even when every
+ *                        assignment fits 32 bits (default 0: 32-bit kernel for n <= 32).
  *  QAA_OPT_ORDER         1 (default) = first-order Lie-Trotter, D then X (R7);
  *                        2 = second-order Strang splitting, D^{1/2} X D^{1/2} per step, at
  *                        the same HBM cost (the half D's of adjacent steps are merged, the
@@ -260,7 +262,8 @@ enum {
   QAA_OPT_KERNEL = 5,
   QAA_OPT_TMA_GROUPS = 6,
   QAA_OPT_SUPER = 7,
-  QAA_OPT_ORDER = 8
+  QAA_OPT_ORDER = 8,
+  QAA_OPT_ENERGY_W64 = 9
 };
 qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value);
 

@@ -724,7 +724,8 @@ __global__ void energy_table_small_kernel(uint8_t* E, int64_t N, uint64_t x_offs
 }
 
 cudaError_t launch_energy_table(uint8_t* E, int64_t N, uint64_t x_offset, const uint64_t* MV, int m, unsigned* d_max,
-                                unsigned long long* d_zeros, int num_sms, cudaStream_t st, int lowbits, int hishift) {
+                                unsigned long long* d_zeros, int num_sms, cudaStream_t st, int lowbits, int hishift,
+                                bool force_w64) {
   const ClauseRec* recs = reinterpret_cast<const ClauseRec*>(MV);
   if (N < 16) {
     energy_table_small_kernel<<<1, 32, 0, st>>>(E, N, x_offset, recs, m, d_max, d_zeros);
@@ -736,7 +737,7 @@ cudaError_t launch_energy_table(uint8_t* E, int64_t N, uint64_t x_offset, const 
     // every assignment x < x_offset + N fits 32 bits when the highest one does
     const uint64_t xmax = (uint64_t)(N - 1) | x_offset | (hishift < 64 && lowbits < 64 ?
                               (((uint64_t)(N - 1) >> lowbits) << hishift) : 0ull);
-    const bool w32 = (xmax >> 32) == 0;
+    const bool w32 = (xmax >> 32) == 0 && !force_w64;
     if (w32)
       energy_table_kernel<true, 4><<<(int)grid, 256, 0, st>>>(E, N, x_offset, recs, m, d_max, d_zeros, lowbits, hishift);
     else

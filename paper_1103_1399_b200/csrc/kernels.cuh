@@ -182,7 +182,7 @@ cudaError_t launch_sweep_cluster(const SweepArgs& a, int nrep, cudaStream_t st);
 // max(E) and the zero count into the given device counters.
 cudaError_t launch_energy_table(uint8_t* E, int64_t N, uint64_t x_offset, const uint64_t* MV, int m,
                                 unsigned* d_max, unsigned long long* d_zeros, int num_sms, cudaStream_t st,
-                                int lowbits = 63, int hishift = 0);
+                                int lowbits = 63, int hishift = 0, bool force_w64 = false);
 // Z compaction (A3): writes x_offset + x for every E[x] == 0 (order unspecified).
 cudaError_t launch_compact_zeros(const uint8_t* E, int64_t N, uint64_t x_offset, uint64_t* Z,
                                  unsigned long long* d_count, int num_sms, cudaStream_t st);

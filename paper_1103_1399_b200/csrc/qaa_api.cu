@@ -86,6 +86,7 @@ struct qaa_ctx {
   int super_groups = 2;
   int super_hints = 2;
   int super_force = 0;
+  int energy_w64 = 0;  // test hook: 64-bit energy-table kernel even when x fits 32 bits
   bool shard_super_ok = false;  // sharded plan: fused [group 0][group P-2 + layout swap] launches
   SuperArgs shard_super;
   CUtensorMap shard_kmap[2];    // group P-2 over shard buffer 0 / 1
@@ -288,6 +289,10 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
     case QAA_OPT_STEP_SPANNING:
       if (value < 0 || value > 2) return fail(ctx, QAA_E_USAGE, "step_spanning must be 0, 1 or 2");
       ctx->step_spanning = (int)value;
+      return QAA_OK;
+    case QAA_OPT_ENERGY_W64:
+      if (value < 0 || value > 1) return fail(ctx, QAA_E_USAGE, "energy_w64 must be 0 or 1");
+      ctx->energy_w64 = (int)value;
       return QAA_OK;
     case QAA_OPT_ORDER:
       if (value != 1 && value != 2) return fail(ctx, QAA_E_USAGE, "splitting order must be 1 or 2");
@@ -747,7 +752,8 @@ qaa_status qaa_load_instance(qaa_ctx* ctx, int n, int m, const int32_t* lits) {
   CUDA_TRY(cudaMemsetAsync(ctx->d_counters, 0, 16, ctx->stream));
   const uint64_t x_offset = (uint64_t)ctx->rank << L;
   CUDA_TRY(launch_energy_table(ctx->E, N, x_offset, (const uint64_t*)ctx->clause_recs, (int)recs.size(), ctx->d_counters,
-                               (unsigned long long*)(ctx->d_counters + 2), ctx->num_sms, ctx->stream));
+                               (unsigned long long*)(ctx->d_counters + 2), ctx->num_sms, ctx->stream, 63, 0,
+                               ctx->energy_w64 != 0));
   ctx->stats.kernel_launches_total++;
   unsigned hc[4];
   CUDA_TRY(cudaMemcpyAsync(hc, ctx->d_counters, 16, cudaMemcpyDeviceToHost, ctx->stream));
@@ -766,7 +772,7 @@ qaa_status qaa_load_instance(qaa_ctx* ctx, int n, int m, const int32_t* lits) {
     if (st) return st;
     CUDA_TRY(launch_energy_table(ctx->E_B, N, (uint64_t)ctx->rank << (L - ctx->gbits), (const uint64_t*)ctx->clause_recs,
                                  (int)recs.size(), ctx->d_counters, (unsigned long long*)(ctx->d_counters + 2),
-                                 ctx->num_sms, ctx->stream, L - ctx->gbits, L));
+                                 ctx->num_sms, ctx->stream, L - ctx->gbits, L, ctx->energy_w64 != 0));
     ctx->stats.kernel_launches_total++;
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     // global |Z| and max E over ranks
@@ -1711,12 +1717,12 @@ qaa_status qaa_time_energy_table(qaa_ctx* ctx, int reps, double* ms) {
   // warm-up, then `reps` timed launches recomputing E in place (same values)
   CUDA_TRY(launch_energy_table(ctx->E, N, (uint64_t)ctx->rank << ctx->L, (const uint64_t*)ctx->clause_recs,
                                ctx->n_recs, ctx->d_counters, (unsigned long long*)(ctx->d_counters + 2), ctx->num_sms,
-                               ctx->stream));
+                               ctx->stream, 63, 0, ctx->energy_w64 != 0));
   CUDA_TRY(cudaEventRecord(a, ctx->stream));
   for (int r = 0; r < reps; r++)
     CUDA_TRY(launch_energy_table(ctx->E, N, (uint64_t)ctx->rank << ctx->L, (const uint64_t*)ctx->clause_recs,
                                  ctx->n_recs, ctx->d_counters, (unsigned long long*)(ctx->d_counters + 2),
-                                 ctx->num_sms, ctx->stream));
+                                 ctx->num_sms, ctx->stream, 63, 0, ctx->energy_w64 != 0));
   CUDA_TRY(cudaEventRecord(b, ctx->stream));
   CUDA_TRY(cudaEventSynchronize(b));
   float t = 0.f;

@@ -19,7 +19,7 @@ __all__ = [
     "qaa_init_basis", "qaa_evolve", "qaa_sweep", "qaa_time_energy_table", "qaa_set_driver", "qaa_spectrum", "qaa_success_prob", "qaa_energy", "qaa_norm2", "qaa_sigma_x",
     "qaa_num_solutions", "qaa_max_energy", "qaa_copy_state", "qaa_set_state", "qaa_copy_energy_table",
     "qaa_state_ptr", "qaa_set_option", "qaa_get_stats", "qaa_reset_stats", "qaa_plan_describe",
-    "qaa_version", "OPT_ROW_BITS", "OPT_PROFILE", "OPT_STEP_SPANNING", "OPT_CTAS_PER_SM", "OPT_KERNEL", "OPT_TMA_GROUPS", "OPT_SUPER", "OPT_ORDER",
+    "qaa_version", "OPT_ROW_BITS", "OPT_PROFILE", "OPT_STEP_SPANNING", "OPT_CTAS_PER_SM", "OPT_KERNEL", "OPT_TMA_GROUPS", "OPT_SUPER", "OPT_ORDER", "OPT_ENERGY_W64",
     "PLAN_RECORD", "SHARD_RECORD", "TorchComm", "qaa_plan_describe_sharded",
 ]
 
@@ -30,6 +30,7 @@ STATUS = {0: "QAA_OK", 1: "QAA_E_USAGE", 2: "QAA_E_INPUT", 3: "QAA_E_CAP", 4: "Q
           5: "QAA_E_CUDA", 6: "QAA_E_NCCL"}
 OPT_ROW_BITS, OPT_PROFILE, OPT_STEP_SPANNING, OPT_CTAS_PER_SM, OPT_KERNEL, OPT_TMA_GROUPS, OPT_SUPER, OPT_ORDER = \
     1, 2, 3, 4, 5, 6, 7, 8
+OPT_ENERGY_W64 = 9
 PLAN_RECORD = 10
 SHARD_RECORD = 10
 

@@ -53,9 +53,12 @@ def instance(n, seed=None):
 
 
 # ------------------------------------------------------------------ K1 / K2
+@pytest.mark.parametrize("w64", [0, 1])
 @pytest.mark.parametrize("n", [3, 4, 6, 8, 11, 12, 13, 16, 20, 24])
-def test_energy_table_exact(ctx, orc, n):
+def test_energy_table_exact(q, ctx, orc, n, w64):
+    """w64 = 1: the 64-bit kernel (used for n > 32) on the same tables."""
     cl = instance(n)
+    ctx.set_option(q.OPT_ENERGY_W64, w64)
     ctx.load_instance(n, cl)
     Eg = ctx.energy_table()
     Eo = orc.energy_table(n, cl)
