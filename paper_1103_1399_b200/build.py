@@ -12,8 +12,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libqaa.so")
-SOURCES = ["qaa_api.cu", "kernels.cu", "pass_fast.cu", "pass_tma.cu", "spectrum.cu", "plan.cpp"]
-HEADERS = ["kernels.cuh", "plan.hpp"]
+SOURCES = ["api_context.cu", "api_tma.cu", "api_shard.cu", "api_evolve.cu", "api_observe.cu", "api_extras.cu", "kernels.cu", "pass_fast.cu", "pass_tma.cu", "spectrum.cu", "plan.cpp"]
+HEADERS = ["api_internal.hpp", "kernels.cuh", "plan.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
@@ -31,7 +31,7 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", LIB, *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
+    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-Xlinker", "--no-undefined", "-o", LIB, *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(PKG, "build.log")
     with open(log, "w") as f:

@@ -1,0 +1,247 @@
+// api_extras.cu -- NEXT rows: spectrum (F3), energy-table timing (F2), batched sweep (F1), plan description.
+#include "api_internal.hpp"
+
+extern "C" {
+
+qaa_status qaa_spectrum(qaa_ctx* ctx, double s, int kmax, int nev, double* evals, double* overlap, int* iters) {
+  CHECK_CTX();
+  if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "spectrum before load_instance");
+  if (!(s >= 0.0 && s <= 1.0)) return fail(ctx, QAA_E_USAGE, "s = %g outside [0, 1]", s);
+  if (kmax < 2 || kmax > 512 || nev < 1 || nev > kmax || !evals)
+    return fail(ctx, QAA_E_USAGE, "need 2 <= kmax <= 512, 1 <= nev <= kmax, evals != NULL");
+  if (ctx->world != 1 || ctx->L > 24) return fail(ctx, QAA_E_CAP, "spectrum: single GPU, n <= 24");
+  if (overlap && !ctx->initialized) return fail(ctx, QAA_E_STATE, "overlap needs an initialised state");
+  const size_t vec = ((size_t)1 << ctx->L) * sizeof(double2);
+  void* basis = nullptr;
+  cudaError_t e = cudaMalloc(&basis, vec * (size_t)(kmax + 1));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ctx, QAA_E_CAP, "Lanczos basis of %d vectors does not fit", kmax + 1);
+  }
+  qaa_status st = ensure_part(ctx, (size_t)ctx->num_sms * 8 + 16);
+  if (st) {
+    cudaFree(basis);
+    return st;
+  }
+  LanczosArgs p;
+  p.n = ctx->L;
+  p.num_sms = ctx->num_sms;
+  p.E = ctx->E;
+  p.wb = weight_b(ctx, s);
+  p.wp = weight_p(ctx, s);
+  p.kmax = kmax;
+  p.nev = nev;
+  p.basis = (double2*)basis;
+  p.scratch = ctx->d_part;
+  p.state = overlap ? ctx->state : nullptr;
+  int it = 0;
+  e = lanczos_spectrum(p, ctx->stream, evals, overlap, &it);
+  cudaFree(basis);
+  if (e != cudaSuccess) return fail(ctx, QAA_E_CUDA, "Lanczos failed: %s", cudaGetErrorString(e));
+  ctx->stats.kernel_launches_total += 4 * (int64_t)it * (it + 1);
+  if (iters) *iters = it;
+  return QAA_OK;
+}
+
+qaa_status qaa_time_energy_table(qaa_ctx* ctx, int reps, double* ms) {
+  CHECK_CTX();
+  if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "time_energy_table before load_instance");
+  if (reps < 1 || !ms) return fail(ctx, QAA_E_USAGE, "reps must be >= 1 and ms non-NULL");
+  if (!ctx->clause_recs) return fail(ctx, QAA_E_STATE, "no clause records");
+  const int64_t N = (int64_t)1 << ctx->L;
+  cudaEvent_t a, b;
+  CUDA_TRY(cudaEventCreate(&a));
+  CUDA_TRY(cudaEventCreate(&b));
+  // warm-up, then `reps` timed launches recomputing E in place (same values)
+  CUDA_TRY(launch_energy_table(ctx->E, N, (uint64_t)ctx->rank << ctx->L, (const uint64_t*)ctx->clause_recs,
+                               ctx->n_recs, ctx->d_counters, (unsigned long long*)(ctx->d_counters + 2), ctx->num_sms,
+                               ctx->stream, 63, 0, ctx->energy_w64 != 0));
+  CUDA_TRY(cudaEventRecord(a, ctx->stream));
+  for (int r = 0; r < reps; r++)
+    CUDA_TRY(launch_energy_table(ctx->E, N, (uint64_t)ctx->rank << ctx->L, (const uint64_t*)ctx->clause_recs,
+                                 ctx->n_recs, ctx->d_counters, (unsigned long long*)(ctx->d_counters + 2),
+                                 ctx->num_sms, ctx->stream, 63, 0, ctx->energy_w64 != 0));
+  CUDA_TRY(cudaEventRecord(b, ctx->stream));
+  CUDA_TRY(cudaEventSynchronize(b));
+  float t = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&t, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  ctx->stats.kernel_launches_total += reps + 1;
+  *ms = (double)t / reps;
+  return QAA_OK;
+}
+
+qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, double* out) {
+  CHECK_CTX();
+  if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "sweep before load_instance");
+  if (ctx->world != 1 || ctx->L > SWEEP_MAX_L)
+    return fail(ctx, QAA_E_USAGE, "sweep needs world = 1 and n <= %d (state resident in one CTA or cluster)",
+                SWEEP_MAX_L);
+  if (nrep < 1 || !T || !K || !out) return fail(ctx, QAA_E_USAGE, "sweep needs nrep >= 1 and non-NULL arrays");
+  int64_t rows = 0;
+  for (int r = 0; r < nrep; r++) {
+    if (!(T[r] >= 0.0) || !std::isfinite(T[r])) return fail(ctx, QAA_E_USAGE, "T[%d] = %g invalid", r, T[r]);
+    if (K[r] < 1) return fail(ctx, QAA_E_USAGE, "K[%d] = %lld < 1", r, (long long)K[r]);
+    rows += K[r] + (ctx->order == 2 ? 1 : 0);
+  }
+  const int n_phi = (int)ctx->emax + 1;
+  const size_t phi_bytes = (size_t)rows * n_phi * sizeof(double2);
+  const size_t tail = (size_t)rows * (sizeof(double) + sizeof(int32_t)) + (size_t)nrep * 2 * sizeof(int64_t);
+  const size_t total = phi_bytes + tail + (size_t)nrep * sizeof(double) + 512;
+  if (ctx->coef_pending) {
+    CUDA_TRY(cudaEventSynchronize(ctx->coef_done));
+    ctx->coef_pending = false;
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  qaa_status st = ensure_host(ctx, &ctx->h_coef, &ctx->h_coef_cap, total);
+  if (st) return st;
+  st = ensure_buffer(ctx, &ctx->d_coef, &ctx->d_coef_cap, total);
+  if (st) return st;
+  char* hb = (char*)ctx->h_coef;
+  double2* hphi = (double2*)hb;
+  double* hcoef = (double*)(hb + phi_bytes);
+  int32_t* hform = (int32_t*)(hcoef + rows);
+  int64_t* hK = (int64_t*)(((uintptr_t)(hform + rows) + 15) & ~(uintptr_t)15);
+  int64_t* hoff = hK + nrep;
+  int64_t row = 0;
+  for (int r = 0; r < nrep; r++) {
+    hK[r] = K[r];
+    hoff[r] = row;
+    const double dt = T[r] / (double)K[r];
+    for (int64_t k = 0; k < K[r]; k++) {
+      const double s = ((double)k + 0.5) / (double)K[r];
+      double theta = dt * weight_p(ctx, s);
+      if (ctx->order == 2)
+        theta = 0.5 * dt * (weight_p(ctx, k == 0 ? 0.0 : ((double)k - 0.5) / (double)K[r]) + weight_p(ctx, s));
+      StepCoef c;
+      build_step(T[r], K[r], weight_b(ctx, s), theta, ctx->n, n_phi, hphi + (size_t)(row + k) * n_phi, &c);
+      hcoef[row + k] = c.coef;
+      hform[row + k] = c.form;
+    }
+    row += K[r];
+    if (ctx->order == 2) {
+      const double theta = 0.5 * dt * weight_p(ctx, ((double)K[r] - 0.5) / (double)K[r]);
+      for (int e = 0; e < n_phi; e++)
+        hphi[(size_t)row * n_phi + e] = make_double2(std::cos(theta * (double)e), -std::sin(theta * (double)e));
+      hcoef[row] = 0.0;
+      hform[row] = 0;
+      row++;
+    }
+  }
+  const size_t used = (size_t)((char*)(hoff + nrep) - hb);
+  CUDA_TRY(cudaMemcpyAsync(ctx->d_coef, ctx->h_coef, used, cudaMemcpyHostToDevice, ctx->stream));
+  char* db = (char*)ctx->d_coef;
+  SweepArgs a;
+  a.E = ctx->E;
+  a.L = ctx->L;
+  a.amp0 = 1.0 / std::sqrt(std::ldexp(1.0, ctx->n));
+  a.phi_all = (const double2*)db;
+  a.n_phi = n_phi;
+  a.coef = (const double*)(db + phi_bytes);
+  a.form = (const int32_t*)(db + ((char*)hform - hb));
+  a.K = (const int64_t*)(db + ((char*)hK - hb));
+  a.row_off = (const int64_t*)(db + ((char*)hoff - hb));
+  a.final_d = ctx->order == 2 ? 1 : 0;
+  double* dout = (double*)(db + ((used + 15) & ~(size_t)15));
+  a.out = dout;
+  if (ctx->L >= 10)  // register phases, one CTA (n <= 13) or one cluster (n = 14..16) per replica
+    CUDA_TRY(launch_sweep_cluster(a, nrep, ctx->stream));
+  else
+    CUDA_TRY(launch_sweep(a, nrep, ctx->stream));
+  ctx->stats.kernel_launches_total++;
+  CUDA_TRY(cudaMemcpyAsync(out, dout, (size_t)nrep * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return QAA_OK;
+}
+
+qaa_status qaa_plan_describe(int n_local, int row_bits, int step_spanning, int64_t K, int32_t* rec, int64_t cap,
+                             int64_t* count) {
+  if (!count || n_local < 1 || n_local > 40 || K < 1 || (cap > 0 && !rec)) return QAA_E_USAGE;
+  if (n_local <= RESIDENT_MAX_L) {
+    const uint64_t mask = (n_local >= 64) ? ~0ull : ((1ull << n_local) - 1);
+    for (int64_t k = 0; k < K && k < cap; k++) {
+      int32_t* r = rec + k * QAA_PLAN_RECORD;
+      r[0] = 0;
+      r[1] = -1;
+      r[2] = (int32_t)k;
+      r[3] = (int32_t)k;
+      r[4] = 0;
+      r[5] = 0;
+      r[6] = (int32_t)(mask & 0xffffffffu);
+      r[7] = (int32_t)(mask >> 32);
+      r[8] = 0;
+      r[9] = 0;
+    }
+    *count = K;
+    return QAA_OK;
+  }
+  Geometry g;
+  std::string e;
+  if (!build_geometry(n_local, row_bits, &g, &e)) return QAA_E_USAGE;
+  std::vector<PassPlan> plan;
+  build_pass_schedule((int)g.groups.size(), K, step_spanning, &plan);
+  *count = (int64_t)plan.size();
+  for (int64_t i = 0; i < (int64_t)plan.size() && i < cap; i++) {
+    const PassPlan& pp = plan[(size_t)i];
+    const Group& gr = g.groups[pp.group];
+    Program prog;
+    if (!build_program(pp.pre_step >= 0 ? gr.rot_local : 0u, pp.d_step >= 0, pp.post_step >= 0 ? gr.rot_local : 0u,
+                       &prog))
+      return QAA_E_USAGE;
+    const uint64_t pre = pp.pre_step >= 0 ? gr.rot_phys : 0, post = pp.post_step >= 0 ? gr.rot_phys : 0;
+    int32_t* r = rec + i * QAA_PLAN_RECORD;
+    r[0] = pp.group;
+    r[1] = (int32_t)pp.pre_step;
+    r[2] = (int32_t)pp.d_step;
+    r[3] = (int32_t)pp.post_step;
+    r[4] = (int32_t)(pre & 0xffffffffu);
+    r[5] = (int32_t)(pre >> 32);
+    r[6] = (int32_t)(post & 0xffffffffu);
+    r[7] = (int32_t)(post >> 32);
+    r[8] = prog.n_exch;
+    r[9] = prog.n_shfl;
+  }
+  return QAA_OK;
+}
+
+}  // extern "C"
+
+
+extern "C" qaa_status qaa_plan_describe_sharded(int n, int world, int row_bits, int64_t K, int32_t* rec, int64_t cap,
+                                                int64_t* count) {
+  if (!count || K < 1 || (cap > 0 && !rec)) return QAA_E_USAGE;
+  if (world != 2 && world != 4 && world != 8) return QAA_E_USAGE;
+  const int g = world == 2 ? 1 : (world == 4 ? 2 : 3);
+  const int L = n - g;
+  if (n < 1 || n > 40 || L <= RESIDENT_MAX_L) return QAA_E_CAP;
+  Geometry geo;
+  std::string e;
+  if (!build_geometry(L, row_bits, &geo, &e)) return QAA_E_USAGE;
+  std::vector<ShardPass> plan;
+  if (!build_shard_schedule(geo, g, K, &plan, &e)) return QAA_E_CAP;
+  *count = (int64_t)plan.size();
+  for (int64_t i = 0; i < (int64_t)plan.size() && i < cap; i++) {
+    const ShardPass& sp = plan[(size_t)i];
+    int32_t* r = rec + i * QAA_SHARD_RECORD;
+    uint32_t pre = 0, post = 0;
+    if (sp.kind == SK_PASS) {
+      const Group& gr = geo.groups[(size_t)sp.group];
+      for (int b = 0; b < TILE_BITS; b++) {
+        if ((sp.pre_local >> b) & 1) pre |= 1u << gr.phys[b];
+        if ((sp.post_local >> b) & 1) post |= 1u << gr.phys[b];
+      }
+    }
+    r[0] = sp.kind;
+    r[1] = sp.group;
+    r[2] = (int32_t)sp.pre_step;
+    r[3] = (int32_t)sp.d_step;
+    r[4] = (int32_t)sp.post_step;
+    r[5] = sp.remote;
+    r[6] = sp.layout;
+    r[7] = (int32_t)pre;
+    r[8] = (int32_t)post;
+    r[9] = 0;
+  }
+  return QAA_OK;
+}

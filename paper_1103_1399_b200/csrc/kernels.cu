@@ -632,7 +632,7 @@ cudaError_t launch_sweep_cluster(const SweepArgs& a, int nrep, cudaStream_t st) 
 }
 
 // ------------------------------------------------------------------ energy table
-// Clause record (host-built, qaa_api.cu): {M_hi, V_hi, spread[4]}: the clause
+// Clause record (host-built, api_context.cu): {M_hi, V_hi, spread[4]}: the clause
 // is violated by x iff (x & M) == V. For 16 consecutive x = x0 | i the high
 // part (bits >= 4) is one test, and spread[] holds, byte i, the outcome of the
 // low part for x0 | i, so one predicated 4-word add counts 16 assignments.

@@ -1,5 +1,5 @@
 // kernels.cuh -- device-side entry points of libqaa (launch wrappers). The
-// C-ABI in qaa_api.cu is the only caller.
+// C-ABI units api_*.cu are the only callers.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>

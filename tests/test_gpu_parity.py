@@ -152,6 +152,25 @@ def test_pass_parity_row_bits(q, ctx, orc, c):
     ctx.set_option(q.OPT_ROW_BITS, 3)
 
 
+@pytest.mark.parametrize("n,c", [(20, 4), (22, 5), (21, 4)])
+def test_row_bits_after_load(q, ctx, orc, n, c):
+    """QAA_OPT_ROW_BITS set AFTER load_instance rebuilds the tensor maps, the
+    permuted energy tables and the chunk plans before the next evolve
+    (n = 21 at c = 4 changes the tile-group count: 2 -> 3 groups)."""
+    ctx.set_option(q.OPT_KERNEL, 1)  # TMA kernels (the ones with per-group tables)
+    cl = instance(n)
+    psi0 = cnf.random_state(n, 11)
+    ctx.load_instance(n, cl)
+    ctx.set_state(psi0)
+    ctx.set_option(q.OPT_ROW_BITS, c)
+    ctx.evolve(1.3, 3)
+    got = ctx.state()
+    want = orc.evolve(n, orc.energy_table(n, cl), psi0, 1.3, 3)
+    assert_close(got, want)
+    ctx.set_option(q.OPT_ROW_BITS, 3)
+    ctx.set_option(q.OPT_KERNEL, 2)
+
+
 def test_cot_form_large_beta(q, ctx, orc):
     """|beta| > pi/4 selects the cot form (u psi0 + i psi1) on both kernels."""
     for n in (10, 17):
