@@ -247,7 +247,18 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        even below 256 chunks (n < 28), where the two-pass plan is faster
  *                        and is chosen otherwise; bit 5: hand out the tiles through a
  *                        global atomic work queue instead of the static round robin
- *                        (measured 2-4 % slower).
+ *                        (measured 2-4 % slower); bit 6: the tensor-memory variant
+ *                        (pass_tmem.cu: register-pattern changes through tcgen05.st/ld
+ *                        instead of shared memory; measured 3-10 % slower);
+ *                        bits 7-10 and 13: its A/B switches and diagnostics counters
+ *                        (SuperArgs.tm_flags); bits 11-12: chunk lag - 1 (default lag 1:
+ *                        two chunks live in L2; 2-3 measured slower). Values 0..16383.
+ *  QAA_OPT_SUPER_GRID    CTAs of an L2-blocked launch (0 = one per SM, default; else 1..SMs):
+ *                        a tuning hook -- a chunk's 2^tpc tiles are dealt round robin, so a
+ *                        grid dividing them evenly balances the per-chunk work.
+ *  QAA_OPT_SUPER_SPLIT   split roles in the L2-blocked launch: this many CTAs run only the
+ *                        group-0 tiles (from HBM), the others only the group-k tiles, each
+ *                        side in chunk order (0 = one interleaved sequence, default).
  *  QAA_OPT_ENERGY_W64    test hook: 1 = the 64-bit energy-table kernel even when every
  *                        assignment fits 32 bits (default 0: 32-bit kernel for n <= 32).
  *  QAA_OPT_ORDER         1 (default) = first-order Lie-Trotter, D then X (R7);
@@ -263,7 +274,9 @@ enum {
   QAA_OPT_TMA_GROUPS = 6,
   QAA_OPT_SUPER = 7,
   QAA_OPT_ORDER = 8,
-  QAA_OPT_ENERGY_W64 = 9
+  QAA_OPT_ENERGY_W64 = 9,
+  QAA_OPT_SUPER_GRID = 10,
+  QAA_OPT_SUPER_SPLIT = 11
 };
 qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value);
 
@@ -282,6 +295,11 @@ typedef struct {
   int64_t super_launches;    /* of pass_launches: L2-blocked launches (QAA_OPT_SUPER) */
   double super_kernel_ms;    /* of pass_kernel_ms: their event-timed durations */
   int64_t super_kernels_timed;
+  int64_t tm_launches;       /* of super_launches: tensor-memory exchange variant (pass_tmem.cu) */
+  uint64_t tm_diag[8];       /* diagnostics (QAA_OPT_SUPER bit 10), summed over warps' lane 0 since the
+                                context's first such launch: [0] cycles in slot-landed waits, [1] items,
+                                [2] deferred group-k items, [3] cycles in deferred waits, [4] / [5]
+                                cycles in group-0 / group-k tile programs; zeros otherwise */
 } qaa_stats;
 qaa_status qaa_get_stats(qaa_ctx* ctx, qaa_stats* out);
 qaa_status qaa_reset_stats(qaa_ctx* ctx);

@@ -12,8 +12,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libqaa.so")
-SOURCES = ["api_context.cu", "api_tma.cu", "api_shard.cu", "api_evolve.cu", "api_observe.cu", "api_extras.cu", "kernels.cu", "pass_fast.cu", "pass_tma.cu", "spectrum.cu", "plan.cpp"]
-HEADERS = ["api_internal.hpp", "kernels.cuh", "plan.hpp"]
+SOURCES = ["api_context.cu", "api_tma.cu", "api_shard.cu", "api_evolve.cu", "api_observe.cu", "api_extras.cu", "kernels.cu", "pass_fast.cu", "pass_tma.cu", "pass_tmem.cu", "spectrum.cu", "plan.cpp"]
+HEADERS = ["api_internal.hpp", "kernels.cuh", "pass_common.cuh", "plan.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
@@ -29,18 +29,40 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit in parallel (one nvcc per file), then link."""
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-Xlinker", "--no-undefined", "-o", LIB, *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, src + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, "-c", "-o", obj, os.path.join(CSRC, src)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        return obj, cmd, r
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    link = [NVCC, *ARCH, "-cudart", "static", "-shared", "-Xlinker", "--no-undefined", "-o", LIB,
+            *[o for o, _, _ in results], "-ldl"]
+    lres = subprocess.run(link, capture_output=True, text=True) if all(r.returncode == 0 for _, _, r in results) \
+        else None
     log = os.path.join(PKG, "build.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
+        for _, cmd, r in results:
+            f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        if lres is not None:
+            f.write(" ".join(link) + "\n" + lres.stdout + lres.stderr)
+    if lres is None or lres.returncode != 0:
+        for _, _, r in results:
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+        if lres is not None:
+            sys.stderr.write(lres.stdout + lres.stderr)
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
-        print(res.stdout + res.stderr)
+        print(open(log).read())
     return LIB
 
 

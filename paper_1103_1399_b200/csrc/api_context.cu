@@ -48,6 +48,7 @@ qaa_status qaa_create(const qaa_config* cfg, qaa_ctx** out) {
   CUDA_TRY(pass_kernel_setup());
   CUDA_TRY(pass_fast_setup());
   CUDA_TRY(pass_tma_setup());
+  CUDA_TRY(superpass_tm_setup());
   return QAA_OK;
 }
 
@@ -76,6 +77,10 @@ void qaa_destroy(qaa_ctx* ctx) {
   if (ctx->E_B) cudaFree(ctx->E_B);
   for (int b = 0; b < 2; b++)
     if (ctx->shard_top_eg[b]) cudaFree(ctx->shard_top_eg[b]);
+  for (int k = 0; k < 4; k++)
+    if (ctx->Eg_tm[k]) cudaFree(ctx->Eg_tm[k]);
+  if (ctx->d_pos_tm) cudaFree(ctx->d_pos_tm);
+  if (ctx->d_tm_diag) cudaFree(ctx->d_tm_diag);
   if (ctx->coef_done) cudaEventDestroy(ctx->coef_done);
   for (auto& p : ctx->ev_pool) {
     cudaEventDestroy(p.first);
@@ -120,6 +125,14 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       ctx->row_bits = (int)value;
       ctx->progs.clear();
       return QAA_OK;
+    case QAA_OPT_SUPER_GRID:
+      if (value < 0 || value > ctx->num_sms) return fail(ctx, QAA_E_USAGE, "super grid must be in 0..%d", ctx->num_sms);
+      ctx->super_grid = (int)value;
+      return QAA_OK;
+    case QAA_OPT_SUPER_SPLIT:
+      if (value < 0 || value >= ctx->num_sms) return fail(ctx, QAA_E_USAGE, "super split must be in 0..%d", ctx->num_sms - 1);
+      ctx->super_split = (int)value;
+      return QAA_OK;
     case QAA_OPT_PROFILE:
       ctx->profile = value != 0;
       return QAA_OK;
@@ -136,7 +149,7 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       ctx->order = (int)value;
       return QAA_OK;
     case QAA_OPT_SUPER:
-      if (value < 0 || value > 63) return fail(ctx, QAA_E_USAGE, "super option must be in 0..63");
+      if (value < 0 || value > 16383) return fail(ctx, QAA_E_USAGE, "super option must be in 0..16383");
       // bit 0: L2-blocked Trotter steps; bit 1: one consumer group per CTA (default two);
       // bits 2-3: L2 eviction hints (0 = evict-last for the group-0 output that the
       // group-k sub-pass reads back + evict-first for dead data; 1 = none; 2 = evict-first only)
@@ -144,6 +157,9 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       ctx->super_groups = (value & 2) ? 1 : 2;
       ctx->super_force = (value & 16) ? 1 : 0;  // also below SUPER_MIN_CHUNKS (tests)
       ctx->super_dynamic = (value & 32) ? 1 : 0;  // dynamic work queue instead of static round robin
+      ctx->super_tm = (value & 64) ? 1 : 0;       // 64: tensor-memory exchanges (pass_tmem.cu; measured slower)
+      ctx->super_tm_flags = (int)((value >> 7) & 15) | (int)((value >> 9) & 16);  // bits 7-10, 13: pass_tmem.cu switches
+      ctx->super_lag = 1 + (int)((value >> 11) & 3);    // bits 11-12: chunk lag - 1 (SuperArgs.lag)
       ctx->super_hints = ((value >> 2) & 3) == 1 ? 0 : (((value >> 2) & 3) == 2 ? 1 : 2);
       return QAA_OK;
     case QAA_OPT_TMA_GROUPS:
@@ -372,6 +388,10 @@ qaa_status qaa_get_stats(qaa_ctx* ctx, qaa_stats* out) {
     ctx->ev_used = 0;
   }
   qaa_stats s = ctx->stats;
+  if (ctx->d_tm_diag) {
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(cudaMemcpy(s.tm_diag, ctx->d_tm_diag, sizeof s.tm_diag, cudaMemcpyDeviceToHost));
+  }
   s.n = ctx->n;
   s.n_local = ctx->L;
   s.amps_local = ctx->loaded ? ((int64_t)1 << ctx->L) : 0;

@@ -66,7 +66,7 @@ static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_p
                                     const double2* phi, int n_phi) {
   int64_t nch = 0;
   for (size_t g = 1; g < ctx->geom.groups.size() && g < 4; g++) nch = std::max(nch, ctx->super_static[g].nchunks);
-  const size_t need = (size_t)nch * sizeof(unsigned) + 256;
+  const size_t need = 2 * (size_t)nch * sizeof(unsigned) + 256;
   if (ctx->d_super_cap < need) {
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     qaa_status st = ensure_buffer(ctx, &ctx->d_super, &ctx->d_super_cap, need);
@@ -101,14 +101,38 @@ static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_p
     a.g0.seg_len[s] = g0.seg_len[s];
   }
   a.hints = ctx->super_hints;
+  a.lag = ctx->super_lag;
   a.queue = ctx->super_dynamic ? (unsigned long long*)ctx->d_super : nullptr;
   a.done = (unsigned*)((char*)ctx->d_super + 256);
-  CUDA_TRY(cudaMemsetAsync(ctx->d_super, 0, 256 + (size_t)a.nchunks * sizeof(unsigned), ctx->stream));
+  a.doneB = a.done + a.nchunks;
+  a.split_a = ctx->super_split;
+  CUDA_TRY(cudaMemsetAsync(ctx->d_super, 0, 256 + 2 * (size_t)a.nchunks * sizeof(unsigned), ctx->stream));
   // phi == nullptr: the plain pair of a four-group plan (kernel variant without D)
-  return launch_superpass(&ctx->tmaps[(size_t)k], a, (gk.rot_local >> 3) & 1, ctx->super_groups, phi != nullptr,
-                          ctx->num_sms, ctx->stream) == cudaSuccess
-             ? QAA_OK
-             : fail(ctx, QAA_E_CUDA, "superpass launch failed");
+  const bool bd = phi != nullptr;
+  cudaError_t e;
+  if (ctx->super_tm && ctx->tm_ok[k] && (!bd || ctx->Eg_tm[k])) {
+    if (bd) a.gk.Eg = ctx->Eg_tm[k];
+    a.done_shift = 3;  // per-warp publish
+    a.split_a = 0;     // split roles: shared-memory kernel only
+    a.tm_flags = ctx->super_tm_flags;
+    if (a.tm_flags & 8) {  // diagnostics: wait / program cycle counters, read by qaa_get_stats
+      if (!ctx->d_tm_diag) {
+        CUDA_TRY(cudaMalloc(&ctx->d_tm_diag, 8 * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMemsetAsync(ctx->d_tm_diag, 0, 8 * sizeof(unsigned long long), ctx->stream));
+      }
+      a.dbg = ctx->d_tm_diag;
+    }
+    // the swizzled map splits the rows off as their own dimension: its own coordinates
+    a.gk.ndims = ctx->tm_geo[k].ndims;
+    for (int d = 0; d < 5; d++) a.gk.dim_seg[d] = ctx->tm_geo[k].dim_seg[d];
+    e = launch_superpass_tm(&ctx->tmaps_sw[k], a, ctx->super_groups, bd, ctx->super_grid ? ctx->super_grid : ctx->num_sms,
+                            ctx->stream);
+    ctx->stats.tm_launches++;
+  } else {
+    e = launch_superpass(&ctx->tmaps[(size_t)k], a, (gk.rot_local >> 3) & 1, ctx->super_groups, bd,
+                         ctx->super_grid ? ctx->super_grid : ctx->num_sms, ctx->stream);
+  }
+  return e == cudaSuccess ? QAA_OK : fail(ctx, QAA_E_CUDA, "superpass launch failed: %s", cudaGetErrorString(e));
 }
 
 static const Program* get_program(qaa_ctx* ctx, int g, bool pre, bool d, bool post) {

@@ -98,6 +98,18 @@ struct qaa_ctx {
   uint8_t* shard_top_eg[2] = {nullptr, nullptr};  // its permuted energies, layout A / B
   size_t shard_top_eg_cap = 0;
   int super_dynamic = 0;
+  int super_tm = 0;             // tensor-memory exchanges in the L2-blocked step (pass_tmem.cu)
+  int super_tm_flags = 0;
+  int super_lag = 1;
+  int super_grid = 0;  // 0: one CTA per SM
+  int super_split = 0;  // split roles: CTAs running group-0 tiles only (0 = interleaved sequence)
+  unsigned long long* d_tm_diag = nullptr;  // pass_tmem.cu diagnostics counters (QAA_OPT_SUPER bit 10)
+  int tm_ok[4] = {0, 0, 0, 0};  // per paired group: swizzled map (+ K3-packed energies) ready
+  CUtensorMap tmaps_sw[4];
+  TmaArgs tm_geo[4];             // its tensor-map dims (ndims, dim_seg) for the load coordinates
+  uint8_t* Eg_tm[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t Eg_tm_cap[4] = {0, 0, 0, 0};
+  uint16_t* d_pos_tm = nullptr;  // byte position of each tile-local index in a K3-packed slice
   SuperArgs super_static[4];
   bool super_ok[4] = {false, false, false, false};
   void* clause_recs = nullptr;  // device clause records (A1) of the loaded instance
@@ -211,6 +223,7 @@ inline bool use_tma(const qaa_ctx* ctx) {
 qaa_status build_tma(qaa_ctx* ctx);
 void build_shard_super(qaa_ctx* ctx);
 qaa_status build_shard_top(qaa_ctx* ctx);
+qaa_status build_tm(qaa_ctx* ctx);
 // api_shard.cu: host collectives through the caller's qaa_comm, shard buffers, sharded evolve
 qaa_status comm_barrier(qaa_ctx* ctx);
 qaa_status comm_allgather(qaa_ctx* ctx, const void* send, void* recv, size_t bytes);

@@ -20,7 +20,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // Tile-group geometry for the TMA kernels: t (contiguous flag, tensor-map
 // dims -> tile-id segments) and, for strided groups, the <= 5-D tensor map of
 // 128-byte rows over the state at `base`. Returns false if not expressible.
-static bool encode_group(qaa_ctx* ctx, const Group& gr, void* base, CUtensorMap* mapp, TmaArgs* tp) {
+static bool encode_group(qaa_ctx* ctx, const Group& gr, void* base, CUtensorMap* mapp, TmaArgs* tp,
+                         bool swz128 = false) {
   const int L = ctx->L;
   auto enc = tensor_map_encoder();
   TmaArgs& t = *tp;
@@ -45,7 +46,8 @@ static bool encode_group(qaa_ctx* ctx, const Group& gr, void* base, CUtensorMap*
       if (in_tile[p]) {
         int start = p;
         while (bits > 0 && ok) {
-          const int lim = nd == 0 ? 7 : 8;
+          // 128-byte swizzle: the inner box dim is exactly one 128-byte row (3 bits)
+          const int lim = nd == 0 ? (swz128 ? 3 : 7) : 8;
           const int take = bits < lim ? bits : lim;
           if (nd >= 5) { ok = false; break; }
           gdim[nd] = (cuuint64_t)1 << (take + (nd == 0 ? 1 : 0));
@@ -69,7 +71,8 @@ static bool encode_group(qaa_ctx* ctx, const Group& gr, void* base, CUtensorMap*
     if (ok && enc) {
       for (int d = 0; d < nd; d++) estr[d] = 1;
       CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)nd, base, gdim, gstride + 1,
-                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       ok = r == CUDA_SUCCESS;
     } else {
@@ -241,6 +244,52 @@ qaa_status build_tma(qaa_ctx* ctx) {
       if (ctx->tma_ok[(size_t)k] &&
           make_super_args(ctx, k, ctx->tma_static[0], ctx->tma_static[(size_t)k], &ctx->super_static[k]))
         ctx->super_ok[k] = true;
+  qaa_status st = build_tm(ctx);
+  if (st) return st;
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return QAA_OK;
+}
+
+// Tensor-memory L2-blocked step (pass_tmem.cu): per paired group k a tensor map
+// with the 128-byte swizzle (the landed tile is read conflict-free in pattern
+// K1) and, when the pair carries D (three-group plans), the energy slices
+// packed for pattern K3. Needs the group's tile bits 0..2 to be the three
+// 128-byte-row bits (row_bits = 3; unrotated padding bits above them are
+// fine). Missing pieces leave tm_ok[k] = 0 (legacy kernel).
+qaa_status build_tm(qaa_ctx* ctx) {
+  for (int k = 0; k < 4; k++) ctx->tm_ok[k] = 0;
+  const int P = (int)ctx->geom.groups.size();
+  const size_t N = (size_t)1 << ctx->L;
+  if (!(P == 3 || P == 4)) return QAA_OK;
+  if (!ctx->d_pos_tm) {
+    std::vector<uint16_t> pos(TILE);
+    superpass_tm_energy_positions(pos.data());
+    CUDA_TRY(cudaMalloc(&ctx->d_pos_tm, TILE * sizeof(uint16_t)));
+    CUDA_TRY(cudaMemcpy(ctx->d_pos_tm, pos.data(), TILE * sizeof(uint16_t), cudaMemcpyHostToDevice));
+  }
+  for (int k = 1; k < P; k++) {
+    if (!ctx->super_ok[k]) continue;
+    const Group& gr = ctx->geom.groups[(size_t)k];
+    if (gr.phys[0] != 0 || gr.phys[1] != 1 || gr.phys[2] != 2) continue;  // 128-byte rows
+    TmaArgs& t = ctx->tm_geo[k];
+    if (!encode_group(ctx, gr, (void*)ctx->state, &ctx->tmaps_sw[k], &t, true) || t.contiguous) continue;
+    if (P == 3) {  // the pair carries D: packed energies for pattern K3
+      if (ctx->Eg_tm_cap[k] < N) {
+        if (ctx->Eg_tm[k]) cudaFree(ctx->Eg_tm[k]);
+        ctx->Eg_tm[k] = nullptr;
+        ctx->Eg_tm_cap[k] = 0;
+        if (cudaMalloc(&ctx->Eg_tm[k], N) != cudaSuccess) {
+          cudaGetLastError();
+          ctx->Eg_tm[k] = nullptr;
+          continue;
+        }
+        ctx->Eg_tm_cap[k] = N;
+      }
+      CUDA_TRY(launch_permute_energy(ctx->E, ctx->Eg_tm[k], gr.phys, gr.nseg, gr.seg_src, gr.seg_dst, gr.seg_len,
+                                     gr.ntiles, 0, ctx->num_sms, ctx->stream, ctx->d_pos_tm));
+      ctx->stats.kernel_launches_total++;
+    }
+    ctx->tm_ok[k] = 1;
+  }
   return QAA_OK;
 }

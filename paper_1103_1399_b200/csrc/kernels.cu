@@ -918,7 +918,8 @@ struct PermArgs {
   int64_t ntiles;
   int pb3;
 };
-__global__ void __launch_bounds__(256) permute_energy_kernel(const uint8_t* E, uint8_t* Eg, const PermArgs a) {
+__global__ void __launch_bounds__(256) permute_energy_kernel(const uint8_t* E, uint8_t* Eg, const PermArgs a,
+                                                             const uint16_t* pos) {
   for (int64_t T = blockIdx.x; T < a.ntiles; T += gridDim.x) {
     int64_t base = 0;
 #pragma unroll
@@ -939,13 +940,13 @@ __global__ void __launch_bounds__(256) permute_energy_kernel(const uint8_t* E, u
         r = ((l >> 4) & 7) | (((l >> 3) & 1) << 3);
       }
       const int warp = l >> 9;
-      Eg[T * TILE + (((lane + 32 * warp) << 4) | r)] = E[o];
+      Eg[T * TILE + (pos ? (int)pos[l] : (((lane + 32 * warp) << 4) | r))] = E[o];
     }
   }
 }
 cudaError_t launch_permute_energy(const uint8_t* E, uint8_t* Eg, const int (&phys)[TILE_BITS], int nseg,
                                   const int* seg_src, const int* seg_dst, const int* seg_len, int64_t ntiles,
-                                  int pb3, int num_sms, cudaStream_t st) {
+                                  int pb3, int num_sms, cudaStream_t st, const uint16_t* pos) {
   PermArgs a;
   a.pb3 = pb3;
   for (int b = 0; b < TILE_BITS; b++) a.phys[b] = phys[b];
@@ -957,7 +958,7 @@ cudaError_t launch_permute_energy(const uint8_t* E, uint8_t* Eg, const int (&phy
   }
   a.ntiles = ntiles;
   int64_t grid = ntiles < (int64_t)num_sms * 8 ? ntiles : (int64_t)num_sms * 8;
-  permute_energy_kernel<<<(int)grid, 256, 0, st>>>(E, Eg, a);
+  permute_energy_kernel<<<(int)grid, 256, 0, st>>>(E, Eg, a, pos);
   return cudaGetLastError();
 }
 }  // namespace qaa

@@ -115,6 +115,17 @@ struct SuperArgs {
   int rank;
   double2* peers[8];
   unsigned* done;      // [nchunks] group-0 tiles stored per chunk (zeroed before launch)
+  int lag;             // chunks between A(c) and B(c) in the work sequence (0 = 1)
+  // split roles (split_a > 0): CTAs [0, split_a) run only group-0 tiles, the rest
+  // only group-k tiles, each in chunk order; B(c) waits for done[c], A(c) for
+  // doneB[c - lag - 1] == 2^tpc_bits (all B(c - lag - 1) issued: bounds the L2 live set)
+  int split_a;
+  unsigned* doneB;     // [nchunks] group-k tiles issued per chunk (zeroed before launch)
+  int done_shift;      // done[c] counts 2^done_shift arrivals per tile (3: one per warp, pass_tmem.cu)
+  int tm_flags;        // pass_tmem.cu A/B switches: 1 = group-0 slot released at the tile's end,
+                       // 2 = publish right after the stores, 4 = spin (no suspend hint) in waits,
+                       // 8 = count waits into dbg (diagnostics), 16 = no early retry of deferred loads
+  unsigned long long* dbg;  // [8] diagnostics counters (tm_flags & 8)
   unsigned long long* queue;  // global work counter (zeroed before launch)
 };
 cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, int ngroups, bool bd, int grid,
@@ -123,9 +134,17 @@ cudaError_t launch_pass_tma(const CUtensorMap* map, const TmaArgs& a, int prog, 
                             cudaStream_t st);
 // gather a group's energy layout: Eg[T*4096 + pack(l)] = E[tbase(T) + off(l)], pack =
 // the thread-major order of register pattern PB (16 bytes per thread, one LDS.128)
+// pos != nullptr: byte position pos[l] of tile-local index l instead (pass_tmem.cu pattern K3)
 cudaError_t launch_permute_energy(const uint8_t* E, uint8_t* Eg, const int (&phys)[TILE_BITS], int nseg,
                                   const int* seg_src, const int* seg_dst, const int* seg_len, int64_t ntiles,
-                                  int pb3, int num_sms, cudaStream_t st);
+                                  int pb3, int num_sms, cudaStream_t st, const uint16_t* pos = nullptr);
+// L2-blocked Trotter step with tensor-memory pattern changes (pass_tmem.cu):
+// same SuperArgs; kmap = the group-k map with the 128-byte swizzle, gk.Eg = the
+// K3-packed energy slices (bd). Cooperative launch (co-residency guaranteed).
+cudaError_t superpass_tm_setup();
+void superpass_tm_energy_positions(uint16_t* pos);  // host: TILE entries
+cudaError_t launch_superpass_tm(const CUtensorMap* kmap, const SuperArgs& a, int ngroups, bool bd, int grid,
+                                cudaStream_t st);
 
 // Whole-evolution kernel for L <= 12 local qubits: one CTA keeps the state in
 // shared memory for all K steps (SURVEY §7 hard part 5; latency-bound sizes).

@@ -20,94 +20,13 @@
 
 #include <cstdint>
 
-#include "kernels.cuh"
+#include "pass_common.cuh"
 
 namespace qaa {
 namespace {
 
-#define FULLM 0xffffffffu
-
-__device__ __forceinline__ constexpr int padA(int l) { return l + (l >> 4); }
-
-template <int P>
-__device__ __forceinline__ int pat_tl(int lane, int warp) {
-  if (P == PA) return lane | (warp << 5);
-  if (P == PB) return (lane & 15) | ((lane >> 4) << 8) | (warp << 9);
-  return (lane << 4) | (warp << 9);
-}
-template <int P>
-__device__ __forceinline__ constexpr int reg_shift() {
-  return P == PA ? 8 : (P == PB ? 4 : 0);
-}
-template <int P>
-__device__ __forceinline__ constexpr int lane_local(int i) {
-  return P == PA ? i : (P == PB ? (i < 4 ? i : 8) : 4 + i);
-}
-
-struct Off {
-  int64_t thr;
-  int64_t s[4];
-};
-
-template <int P>
-__device__ __forceinline__ Off make_off(const FastArgs& a, int lane, int warp) {
-  Off o;
-  const int tl = pat_tl<P>(lane, warp);
-  int64_t t = 0;
-#pragma unroll
-  for (int b = 0; b < TILE_BITS; b++)
-    if ((tl >> b) & 1) t += (int64_t)1 << a.phys[b];
-  o.thr = t;
-#pragma unroll
-  for (int i = 0; i < 4; i++) o.s[i] = (int64_t)1 << a.phys[reg_shift<P>() + i];
-  return o;
-}
-
-__device__ __forceinline__ int64_t roff(const Off& o, int r) {
-  int64_t x = o.thr;
-  if (r & 1) x += o.s[0];
-  if (r & 2) x += o.s[1];
-  if (r & 4) x += o.s[2];
-  if (r & 8) x += o.s[3];
-  return x;
-}
-
-__device__ __forceinline__ int64_t tbase(const FastArgs& a, int64_t T) {
-  int64_t b = 0;
-#pragma unroll
-  for (int s = 0; s < MAX_SEGS; s++)
-    if (s < a.nseg) b += ((T >> a.seg_src[s]) & (((int64_t)1 << a.seg_len[s]) - 1)) << a.seg_dst[s];
-  return b;
-}
-
-// (x, y) <- (x + i t y, y + i t x)
-__device__ __forceinline__ void rot2(double2& x, double2& y, double t) {
-  const double2 nx = make_double2(fma(-t, y.y, x.x), fma(t, y.x, x.y));
-  const double2 ny = make_double2(fma(-t, x.y, y.x), fma(t, x.x, y.y));
-  x = nx;
-  y = ny;
-}
-
-// rotate the 4 register bits of pattern P with per-local-bit coefficients t[slot][.]
-template <int P>
-__device__ __forceinline__ void rot_regs(double2 (&v)[RPT], const double (&t)[TILE_BITS]) {
-#pragma unroll
-  for (int i = 0; i < 4; i++) {
-    const double c = t[reg_shift<P>() + i];
-#pragma unroll
-    for (int r = 0; r < RPT; r++)
-      if (!(r & (1 << i))) rot2(v[r], v[r | (1 << i)], c);
-  }
-}
-
-__device__ __forceinline__ void rot_lane(double2 (&v)[RPT], int lanebit, double t) {
-#pragma unroll
-  for (int r = 0; r < RPT; r++) {
-    const double px = __shfl_xor_sync(FULLM, v[r].x, 1 << lanebit);
-    const double py = __shfl_xor_sync(FULLM, v[r].y, 1 << lanebit);
-    v[r] = make_double2(fma(-t, py, v[r].x), fma(t, px, v[r].y));
-  }
-}
+using namespace pc;
+#define FULLM QAA_FULLM
 
 template <int FROM, int TO>
 __device__ __forceinline__ void xchg(double2* xb, double2 (&v)[RPT], int lane, int warp) {

@@ -16,226 +16,13 @@
 
 #include <cstdint>
 
-#include "kernels.cuh"
+#include "pass_common.cuh"
 
 namespace qaa {
 namespace {
 
-#define FULLM 0xffffffffu
-constexpr int TMA_SLOTS = 3;
-constexpr int SLOT_BYTES = FAST_XBUF * 16;  // 69632: padded exchange layout
-constexpr int TMA_MAX_GROUPS = 2;
-constexpr int PHI_COPIES = 8;  // bank-group copies of the D table (diag below)
-// dynamic shared memory: 3 slots (padded exchange layout), 3 energy slices, the
-// D table copies, mbarriers (full, late), slot metadata, slot counters (last 32 B)
-constexpr size_t TMA_SMEM_BYTES = (size_t)TMA_SLOTS * SLOT_BYTES + (size_t)TMA_SLOTS * TILE +
-                                   (size_t)TMA_MAX_PHI * PHI_COPIES * 16 + TMA_MAX_GROUPS * TMA_SLOTS * 8 +
-                                   TMA_MAX_GROUPS * 8 + TMA_SLOTS * 16 + 32;
-__device__ __forceinline__ unsigned* slot_counters(unsigned char* sm) {
-  return reinterpret_cast<unsigned*>(sm + TMA_SMEM_BYTES - 32);
-}
-
-__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(sa(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(dst)),
-      "l"(src), "r"(bytes), "r"(sa(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, const int (&c)[5], int rank,
-                                         uint64_t* bar) {
-  const uint64_t m = reinterpret_cast<uint64_t>(map);
-  switch (rank) {
-    case 2:
-      asm volatile(
-          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-          "[%4];" ::"r"(sa(dst)),
-          "l"(m), "r"(c[0]), "r"(c[1]), "r"(sa(bar))
-          : "memory");
-      break;
-    case 3:
-      asm volatile(
-          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-          "%4}], [%5];" ::"r"(sa(dst)),
-          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(sa(bar))
-          : "memory");
-      break;
-    case 4:
-      asm volatile(
-          "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-          "%4, %5}], [%6];" ::"r"(sa(dst)),
-          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(sa(bar))
-          : "memory");
-      break;
-    default:
-      asm volatile(
-          "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-          "%4, %5, %6}], [%7];" ::"r"(sa(dst)),
-          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(sa(bar))
-          : "memory");
-      break;
-  }
-}
-// L2 eviction-priority hints (createpolicy + .L2::cache_hint), used by the
-// L2-blocked pass to keep the chunk data that is read again and stream out the rest
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_normal() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                              uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
-          "r"(sa(dst)),
-      "l"(src), "r"(bytes), "r"(sa(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_hint(void* dst, const CUtensorMap* map, const int (&c)[5], int rank,
-                                              uint64_t* bar, uint64_t pol) {
-  const uint64_t m = reinterpret_cast<uint64_t>(map);
-  switch (rank) {
-    case 2:
-      asm volatile(
-          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
-          "[%1, {%2, %3}], [%4], %5;" ::"r"(sa(dst)),
-          "l"(m), "r"(c[0]), "r"(c[1]), "r"(sa(bar)), "l"(pol)
-          : "memory");
-      break;
-    case 3:
-      asm volatile(
-          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
-          "[%1, {%2, %3, %4}], [%5], %6;" ::"r"(sa(dst)),
-          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(sa(bar)), "l"(pol)
-          : "memory");
-      break;
-    case 4:
-      asm volatile(
-          "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
-          "[%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(sa(dst)),
-          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(sa(bar)), "l"(pol)
-          : "memory");
-      break;
-    default:
-      asm volatile(
-          "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
-          "[%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(sa(dst)),
-          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(sa(bar)), "l"(pol)
-          : "memory");
-      break;
-  }
-}
-__device__ __forceinline__ void st_hint(double2* p, double2 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
-               : "memory");
-}
-// tile j uses slot j % 3 and consumer group j % NG: each (slot, group)
-// barrier sees one phase per lcm(3, NG) tiles
-template <int NG>
-__device__ __forceinline__ constexpr int period() {
-  return NG % TMA_SLOTS == 0 ? NG : NG * TMA_SLOTS;
-}
-__device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void group_bar(int g) {
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(NTHREADS) : "memory");
-}
-
-__device__ __forceinline__ constexpr int padA(int l) { return l + (l >> 4); }
-
-template <int P>
-__device__ __forceinline__ int pat_tl(int lane, int warp) {
-  if (P == PA) return lane | (warp << 5);
-  if (P == PB) return (lane & 15) | ((lane >> 4) << 8) | (warp << 9);
-  return (lane << 4) | (warp << 9);
-}
-template <int P>
-__device__ __forceinline__ constexpr int reg_shift() {
-  return P == PA ? 8 : (P == PB ? 4 : 0);
-}
-
-struct Off {
-  int64_t thr;
-  int64_t s[4];
-};
-template <int P>
-__device__ __forceinline__ Off make_off(const TmaArgs& a, int lane, int warp) {
-  Off o;
-  const int tl = pat_tl<P>(lane, warp);
-  int64_t t = 0;
-#pragma unroll
-  for (int b = 0; b < TILE_BITS; b++)
-    if ((tl >> b) & 1) t += (int64_t)1 << a.phys[b];
-  o.thr = t;
-#pragma unroll
-  for (int i = 0; i < 4; i++) o.s[i] = (int64_t)1 << a.phys[reg_shift<P>() + i];
-  return o;
-}
-__device__ __forceinline__ int64_t roff(const Off& o, int r) {
-  int64_t x = o.thr;
-  if (r & 1) x += o.s[0];
-  if (r & 2) x += o.s[1];
-  if (r & 4) x += o.s[2];
-  if (r & 8) x += o.s[3];
-  return x;
-}
-__device__ __forceinline__ int64_t tbase(const TmaArgs& a, int64_t T) {
-  int64_t b = 0;
-#pragma unroll
-  for (int s = 0; s < MAX_SEGS; s++)
-    if (s < a.nseg) b += ((T >> a.seg_src[s]) & (((int64_t)1 << a.seg_len[s]) - 1)) << a.seg_dst[s];
-  return b;
-}
-
-__device__ __forceinline__ void rot2(double2& x, double2& y, double t) {
-  const double2 nx = make_double2(fma(-t, y.y, x.x), fma(t, y.x, x.y));
-  const double2 ny = make_double2(fma(-t, x.y, y.x), fma(t, x.x, y.y));
-  x = nx;
-  y = ny;
-}
-template <int P>
-__device__ __forceinline__ void rot_regs(double2 (&v)[RPT], const double (&t)[TILE_BITS]) {
-#pragma unroll
-  for (int i = 0; i < 4; i++) {
-    const double c = t[reg_shift<P>() + i];
-#pragma unroll
-    for (int r = 0; r < RPT; r++)
-      if (!(r & (1 << i))) rot2(v[r], v[r | (1 << i)], c);
-  }
-}
-__device__ __forceinline__ void rot_lane(double2 (&v)[RPT], int lanebit, double t) {
-#pragma unroll
-  for (int r = 0; r < RPT; r++) {
-    const double px = __shfl_xor_sync(FULLM, v[r].x, 1 << lanebit);
-    const double py = __shfl_xor_sync(FULLM, v[r].y, 1 << lanebit);
-    v[r] = make_double2(fma(-t, py, v[r].x), fma(t, px, v[r].y));
-  }
-}
+using namespace pc;
+#define FULLM QAA_FULLM
 // Cross-warp exchange through the padded layout. The leading barrier is the
 // write-after-read guard (every warp of the group has finished reading the
 // buffer: the landed tile or the previous exchange), placed after the caller's
@@ -266,14 +53,6 @@ __device__ __forceinline__ void rot_regs_pb3(double2 (&v)[RPT], const double (&t
       if (!(r & (1 << i))) rot2(v[r], v[r | (1 << i)], c);
   }
 }
-// rotate one register bit
-template <int I>
-__device__ __forceinline__ void rot_regbit(double2 (&v)[RPT], double c) {
-#pragma unroll
-  for (int r = 0; r < RPT; r++)
-    if (!(r & (1 << I))) rot2(v[r], v[r | (1 << I)], c);
-}
-
 template <int FROM, int TO>
 __device__ __forceinline__ void xchg(double2* xb, double2 (&v)[RPT], int lane, int warp, int g) {
   const int bs = padA(pat_tl<FROM>(lane, warp));
@@ -378,17 +157,6 @@ __device__ __forceinline__ void program(const TmaArgs& a, double2 (&v)[RPT], dou
   }
 }
 
-// "Last warp out refills": each warp, once its values of slot s are consumed,
-// bumps the slot's counter (acq_rel at CTA scope); the 8th warp of the group
-// resets it and refills the slot -- no group barrier before the refill.
-__device__ __forceinline__ bool last_warp_out(unsigned* cnt) {
-  unsigned old;
-  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(sa(cnt)) : "memory");
-  if (old != (NTHREADS / 32) - 1) return false;
-  *cnt = 0;
-  fence_async_shared();  // generic-proxy accesses of the slot before the async-proxy refill
-  return true;
-}
 template <int PROG>
 struct Info {
   static constexpr bool has_d = PROG == FP_G0_DPOST || PROG == FP_G0_PRE_D_POST || PROG == FP_GK_PRE_D_POST;
@@ -514,132 +282,6 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_pass_tma(const __grid_co
 // the group-k sub-pass is a plain rotate, optionally storing into the peers'
 // next shard buffers (the sharded plan's layout swap).
 // ============================================================================
-__device__ __forceinline__ uint32_t pdep32(uint32_t x, uint32_t mask) {
-  uint32_t r = 0;
-  for (uint32_t m = mask; m; m &= m - 1) {
-    if (x & 1u) r |= m & (~m + 1u);
-    x >>= 1;
-  }
-  return r;
-}
-
-enum SuperKind : int { SK_END = 0, SK_A = 1, SK_B = 2, SK_B_DEFERRED = 3 };
-
-__device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// bounded wait: a lost arrival becomes a trap (launch error) instead of a hang
-__device__ __forceinline__ void mbar_wait_bounded(uint64_t* b, uint32_t parity) {
-  for (uint32_t it = 0;; it++) {
-    uint32_t ok;
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(sa(b)), "r"(parity)
-        : "memory");
-    if (ok) return;
-    if (it > (1u << 26)) __trap();
-  }
-}
-__device__ __forceinline__ void mbar_arrive_notx(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(b)) : "memory");
-}
-
-// queue position q -> (kind, chunk, intra index); false past the end
-__device__ __forceinline__ bool decode_item(const SuperArgs& a, unsigned long long q, int* kind, int64_t* c,
-                                            uint32_t* i) {
-  const unsigned long long tpc = 1ull << a.tpc_bits;
-  const unsigned long long nch = (unsigned long long)a.nchunks;
-  if (q >= 2 * nch * tpc) return false;
-  if (q < tpc) {
-    *kind = SK_A;
-    *c = 0;
-    *i = (uint32_t)q;
-    return true;
-  }
-  const unsigned long long r0 = q - tpc, u = r0 / (2 * tpc), r = r0 % (2 * tpc);
-  if (u + 1 < nch && r < tpc) {
-    *kind = SK_A;
-    *c = (int64_t)(u + 1);
-    *i = (uint32_t)r;
-  } else {
-    *kind = SK_B;
-    *c = (int64_t)u;
-    *i = (uint32_t)(u + 1 < nch ? r - tpc : r);
-  }
-  return true;
-}
-
-struct SlotMeta {
-  int kind;
-  int c;
-  uint32_t T;
-  int pad;
-};
-
-// group-k tile T (tensor-map rows) and, with D, its energy slice, completing on bar
-template <bool BD>
-__device__ __forceinline__ void load_gk(const CUtensorMap* kmap, const SuperArgs& a, uint32_t T, double2* dst,
-                                       uint8_t* edst, uint64_t* bar, uint64_t pol) {
-  mbar_expect_tx(bar, TILE * 16u + (BD ? (uint32_t)TILE : 0u));
-  if (a.gk.contiguous) {
-    bulk_g2s_hint(dst, a.gk.psi + tbase(a.gk, T), TILE * 16u, bar, pol);
-  } else {
-    int cc[5];
-#pragma unroll
-    for (int d = 0; d < 5; d++) {
-      const int sg = a.gk.dim_seg[d];
-      cc[d] = sg < 0 ? 0 : (int)((T >> a.gk.seg_src[sg]) & ((1u << a.gk.seg_len[sg]) - 1));
-    }
-    tma_load_hint(dst, kmap, cc, a.gk.ndims, bar, pol);
-  }
-  if (BD) bulk_g2s_hint(edst, a.gk.Eg + (int64_t)T * TILE, TILE, bar, pol);
-}
-
-// fetch the next work item for slot J % 3 (tile J of this CTA) and start its load
-template <int NG, bool BD>
-__device__ void super_issue(const CUtensorMap* kmap, const SuperArgs& a, int64_t J, double2* slots, uint8_t* eslots,
-                            uint64_t* full, SlotMeta* meta, uint64_t pol_dead) {
-  const int s = (int)(J % TMA_SLOTS);
-  uint64_t* fb = &full[NG * s + (int)(J % NG)];
-  int kind;
-  int64_t c;
-  uint32_t i;
-  // queue position: a.queue != nullptr -> dynamic (global atomic counter);
-  // otherwise static round robin, tile J of CTA b = item b + J * gridDim.x
-  const unsigned long long qpos =
-      a.queue ? atomicAdd(a.queue, 1ull) : (unsigned long long)blockIdx.x + (unsigned long long)J * gridDim.x;
-  if (!decode_item(a, qpos, &kind, &c, &i)) {
-    meta[s] = SlotMeta{SK_END, 0, 0, 0};
-    mbar_arrive_notx(fb);
-    return;
-  }
-  if (kind == SK_A) {
-    const uint32_t T = pdep32(i, a.z_imask) | pdep32((uint32_t)c, a.z_cmask);
-    meta[s] = SlotMeta{SK_A, (int)c, T, 0};
-    mbar_expect_tx(fb, TILE * 16u);
-    bulk_g2s_hint(slots + (size_t)s * FAST_XBUF, a.g0.psi + tbase(a.g0, T), TILE * 16u, fb, pol_dead);
-    return;
-  }
-  const uint32_t T = pdep32(i, a.k_imask) | pdep32((uint32_t)c, a.k_cmask);
-  if (ld_acquire(&a.done[c]) >= (1u << a.tpc_bits)) {
-    fence_async_global();  // generic-proxy stores of chunk c -> this async-proxy read
-    meta[s] = SlotMeta{SK_B, (int)c, T, 0};
-    load_gk<BD>(kmap, a, T, slots + (size_t)s * FAST_XBUF, eslots + (size_t)s * TILE, fb, pol_dead);
-  } else {
-    meta[s] = SlotMeta{SK_B_DEFERRED, (int)c, T, 0};
-    mbar_arrive_notx(fb);
-  }
-}
-
 // BD: the group-k sub-pass is rotate/D/rotate (single GPU); otherwise a plain
 // rotate whose tiles may be stored straight into the peers' next shard buffers
 // (a.remote: the layout swap of the sharded plan)
@@ -699,8 +341,25 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
       }
       mbar_wait_bounded(&late[g], late_phase & 1);
       late_phase++;
+    } else if (m.kind == SK_A_DEFERRED) {
+      // split roles: the group-0 side ran ahead; wait until the group-k side has
+      // issued chunk c - L (a throttle on the L2 live set, not a data dependency)
+      if (gtid == 0) {
+        const int L = 1 + (a.lag > 1 ? a.lag : 1);
+        for (uint32_t it = 0;; it++) {
+          unsigned nb;
+          asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(nb) : "l"(&a.doneB[m.c - L]) : "memory");
+          if (nb >= (1u << a.tpc_bits)) break;
+          __nanosleep(64);
+          if (it > (1u << 26)) __trap();
+        }
+        mbar_expect_tx(&late[g], TILE * 16u);
+        bulk_g2s_hint(xb, a.g0.psi + tbase(a.g0, m.T), TILE * 16u, &late[g], pol_dead);
+      }
+      mbar_wait_bounded(&late[g], late_phase & 1);
+      late_phase++;
     }
-    const bool isb = m.kind != SK_A;
+    const bool isb = m.kind != SK_A && m.kind != SK_A_DEFERRED;
     if (isb) {
       load_landed<Info<BPROG>::load_pat>(v, xb, lane, lw);
       program<BPROG, LANE3>(a.gk, v, xb, es, phis, lane, lw, g);
@@ -773,8 +432,19 @@ TmaKernel pick(int prog, bool lane3, int ng) { return ng == 1 ? pick_ng<1>(prog,
 cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, int ngroups, bool bd, int grid,
                              cudaStream_t st) {
   SuperKernel k = pick_super(lane3, ngroups, bd);  // shared-memory attribute set in pass_tma_setup
-  k<<<grid, ngroups * NTHREADS, TMA_SMEM_BYTES, st>>>(*kmap, a);
-  return cudaGetLastError();
+  // cooperative launch: the chunk dependencies spin across CTAs, so every CTA
+  // must be co-resident -- the launch fails instead of deadlocking
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)(ngroups * NTHREADS));
+  cfg.dynamicSmemBytes = TMA_SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, *kmap, a);
 }
 
 cudaError_t pass_tma_setup() {

@@ -42,7 +42,7 @@ def shard_worker(rank, world, port, outdir, n, clauses, T, K, schedule, psi0, s_
         ctx.set_state(psi0)  # each rank copies the part it owns
     ctx.evolve(T, K, schedule)
     local = ctx.state(rank << L, 1 << L)
-    res = {"state": local, "super_launches": ctx.stats()["super_launches"],
+    res = {"state": local, "super_launches": ctx.stats()["super_launches"], "groups": ctx.stats()["groups"],
            "success": ctx.success_prob(), "norm2": ctx.norm2(),
            "sigma_x": ctx.sigma_x(), "energy": np.array([ctx.energy(s) for s in s_values]),
            "nsol": ctx.num_solutions(), "emax": ctx.max_energy(), "E": ctx.energy_table(rank << L, 1 << L)}

@@ -69,6 +69,39 @@ def test_sharded_evolution_parity(n, world, K, fused):
 
 
 @pytest.mark.gpu
+def test_sharded_four_groups_full_state():
+    """The FOUR-local-tile-group sharded plan -- the geometry the n = 32/33/34
+    multi-GPU configs use (fused [group 0][group P-2 + layout swap] launches, the
+    top group's D pass over both shard buffers) -- at a size whose full state the
+    host holds: n = 28 over 2 ranks with 32-amplitude (512-byte) rows, so L = 27
+    splits into 4 tile groups. The whole gathered state and the observables
+    against the oracle."""
+    from oracle import oracle
+    import paper_1103_1399_b200 as q
+    n, world, K, T = 28, 2, 3, 1.9
+    cl = cnf.random_instance(n, int(round(4.3 * n)), 2028)
+    sched = np.random.default_rng(n).uniform(0, 1, K)
+    with tempfile.TemporaryDirectory() as d:
+        opts = {q.OPT_ROW_BITS: 5, q.OPT_SUPER: 17}
+        mp.spawn(W.shard_worker, args=(world, free_port(), d, n, cl, T, K, sched, None, [0.5], opts),
+                 nprocs=world, join=True)
+        res = [np.load(os.path.join(d, f"rank{r}.npy"), allow_pickle=True).item() for r in range(world)]
+    for r in res:
+        assert r["groups"] == 4
+        assert r["super_launches"] == K  # one fused layout-swap launch per phase
+    got = np.concatenate([r["state"] for r in res])
+    E = oracle.energy_table(n, cl)
+    want = oracle.evolve(n, E, oracle.init_uniform(n), T, K, sched)
+    assert np.max(np.abs(got - want)) < 1e-10
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-11
+    ob = oracle.observables(n, E, want)
+    for r in res:
+        assert abs(r["norm2"] - ob["norm2"]) < 1e-12
+        assert abs(r["success"] - ob["success"]) < 1e-13
+        assert np.allclose(r["sigma_x"], ob["sigma_x"], atol=1e-12, rtol=0)
+
+
+@pytest.mark.gpu
 def test_sharded_uniform_start_paper_config():
     """configs[0]-like run sharded over 2 ranks: n = 16 instance, uniform start."""
     from oracle import oracle
