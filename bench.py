@@ -15,7 +15,9 @@ flush is needed between steps.
 step loads the instance from host memory, initialises, evolves one window and
 reads P_succ back (H2D/D2H inside the timed region).
 
-`--impl reference` times the CPU oracle (oracle/, as it stands) instead.
+`--impl reference` times the CPU oracle (oracle/, as it stands) instead, on the
+same workload: one oracle Trotter step of the bench schedule at n = 30 per bench
+step, in place, on all host cores (cpu_baseline: the first 2 steps, rank 0 at N = 1).
 
 With N > 1 GPUs (torchrun) the state is n = 30 + log2 N, 2^30 amplitudes per GPU
 (weak scaling), and `value` is the whole-job aggregate in shard-steps/s: N x the
@@ -63,7 +65,6 @@ def parse():
                     help="QAA_OPT_SUPER bits (1 = L2-blocked Trotter steps, default; 0 = two HBM passes per step)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample-n", type=int, default=26)
     ap.add_argument("--share-gpu", action="store_true",
                     help="map every rank to cuda:0 (functional test of --gpus N on a 1-GPU box; not a perf number)")
     return ap.parse_args()
@@ -140,50 +141,93 @@ def traffic_from_profiles():
 
 
 # --------------------------------------------------------------------- CPU oracle timing
-def oracle_sample(n_target: int, n_sample: int, steps: int = 2):
-    """Time the oracle's Trotter step (O-5..O-7) on a seeded instance of n_sample
-    qubits and scale per amplitude-qubit to n_target (cost ~ (n+1) 2^n)."""
-    from oracle import oracle
-    oracle.build()
-    cl = cnf.random_instance(n_sample, int(round(4.5 * n_sample)), 1000 + n_sample)
-    E = oracle.energy_table(n_sample, cl)
-    psi = oracle.init_uniform(n_sample)
-    T, s = schedule_window(0, steps)
-    t0 = time.perf_counter()
-    oracle.evolve(n_sample, E, psi, T, steps, s)
-    dt = (time.perf_counter() - t0) / steps
-    scale = (2.0 ** (n_target - n_sample)) * (n_target + 1) / (n_sample + 1)
-    return dt, dt * scale, oracle.num_threads()
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def set_omp_threads(k: int) -> int:
+    """Threads of the oracle's OpenMP runtime (already loaded): omp_set_num_threads."""
+    import ctypes
+    try:
+        gomp = ctypes.CDLL("libgomp.so.1")
+        gomp.omp_set_num_threads(int(k))
+        return int(k)
+    except OSError:
+        return os.cpu_count() or 1
+
+
+class OracleAtConfig:
+    """The oracle (oracle/, as it stands) on the bench workload itself: the
+    checked-in n-qubit instance, its O-2 energy table and the uniform state,
+    advanced step by step along the bench schedule IN PLACE (O-5..O-7 through
+    oracle_evolve, one step per call; building the table and the state is setup,
+    not timed)."""
+
+    def __init__(self, n: int, cl):
+        from oracle import oracle
+        oracle.build()
+        self.oracle, self.n = oracle, n
+        self.E = np.ascontiguousarray(oracle.energy_table(n, cl), dtype=np.uint16)
+        self.psi = oracle.init_uniform(n)
+        self.k = 0
+
+    def step(self) -> float:
+        """One Trotter step k of the bench schedule; returns its wall time (s)."""
+        o = self.oracle
+        T, s = schedule_window(self.k, 1)
+        sch = np.ascontiguousarray(s, dtype=np.float64)
+        t0 = time.perf_counter()
+        o._check(o.lib().oracle_evolve(self.n, o._ptr(self.E), o._ptr(self.psi), float(T), 1, o._ptr(sch)), "evolve")
+        dt = time.perf_counter() - t0
+        self.k += 1
+        return dt
+
+
+def single_thread_record():
+    """The 1-thread oracle step at n = 30, measured once by tools/oracle_threads.py on
+    the GPU box's host (3 min per step: outside the default bench run)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "r02_oracle_threads.json")))
+    except Exception:
+        return None
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    # the oracle on all of the box's host cores (torchrun exports OMP_NUM_THREADS=1);
-    # set before liboracle (and with it the OpenMP runtime) is first loaded
-    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())
     n = args.n or (N_DEFAULT + (args.gpus.bit_length() - 1))
-    ns = args.cpu_sample_n
+    cl, _ = cnf.load_instance(n) if os.path.exists(cnf.instance_path(n)) else (
+        cnf.random_instance(n, int(round(4.5 * n)), 1000 + n), None)
+    if (1 << n) * 18 > (os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")) * 0.8:
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle state for n={n} does not fit host RAM"}))
+        return 0
+    orc = OracleAtConfig(n, cl)
+    cores = set_omp_threads(os.cpu_count() or 1)
     for _ in range(args.warmup):
-        oracle_sample(n, ns, 1)
-    per = []
-    for _ in range(args.steps):
-        dt, scaled, cores = oracle_sample(n, ns, 1)
-        per.append(scaled)
+        orc.step()
+    per = [orc.step() for _ in range(args.steps)]
     t_step = float(np.mean(per))
     # whole-job units as in the GPU arm: Trotter steps of 2^30-amplitude shards
     units = 2.0 ** (n - N_DEFAULT) if args.gpus > 1 else 1.0
     val = units / t_step
-    sample = (f"oracle Trotter step on a seeded n={ns} instance, 1 step per bench step, scaled by "
-              f"2^{n - ns}*(n+1)/(n_s+1) to n={n}")
+    sample = (f"oracle Trotter step k of the bench schedule (n={n}, T=200, K=1e4) on the checked-in instance, "
+              f"in place, one step per bench step, {cores} OpenMP threads")
     line = {"impl": "reference", "metric": "trotter_steps_per_s", "value": val,
             "unit": "steps/s" if args.gpus == 1 else "shard-steps/s (2^30 amplitudes per shard)",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": f"n={n} unique-solution 3-SAT, T=200, K=1e4 (dt=0.02)",
-                                            "n": n},
-            "cpu_baseline": {"value": val, "unit": "steps/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "data": "synthetic", "config": {"workload": f"n={n} unique-solution 3-SAT (inputs/instances), T=200, "
+                                                        f"K=1e4 (dt=0.02)", "n": n},
+            "cpu_baseline": {"value": val, "unit": "steps/s", "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu": cpu_model(), "step_s": per, "single_thread": single_thread_record()},
             "e2e": {"value": val, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -363,10 +407,15 @@ def run_ours(args):
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1:  # contract: rank 0 at N = 1 only
         try:
-            dt, scaled, cores = oracle_sample(n, args.cpu_sample_n, 2)
-            cpu = {"value": 1.0 / scaled, "unit": "steps/s", "cores": cores, "kind": "oracle",
-                   "sample": f"2 oracle Trotter steps on a seeded n={args.cpu_sample_n} instance "
-                             f"({dt:.3f} s/step), scaled by 2^{n - args.cpu_sample_n}*(n+1)/(n_s+1) to n={n}"}
+            orc = OracleAtConfig(n, cl)
+            cores = set_omp_threads(os.cpu_count() or 1)
+            per = [orc.step() for _ in range(2)]
+            cpu = {"value": 1.0 / float(np.mean(per)), "unit": "steps/s", "cores": cores, "kind": "oracle",
+                   "sample": f"the first 2 Trotter steps of the bench schedule at n={n} (the checked-in instance, "
+                             f"T=200, K=1e4), oracle_evolve in place, {cores} OpenMP threads; energy table and "
+                             f"initial state built outside the timing",
+                   "step_s": per, "cpu": cpu_model(), "single_thread": single_thread_record()}
+            del orc
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": f"failed: {e}"}
@@ -389,7 +438,10 @@ def run_ours(args):
                                st["passes_per_step_num"] / st["passes_per_step_den"], "tile_groups": st["groups"],
                            "l2": "state 16 GiB >> 126 MB L2 (no flush needed)",
                            "parallelism": f"dp{world}" if world > 1 else "single"},
-                "effective_hbm_gbs": alg_bytes / (ms / 1e3) / 1e9,
+                "effective_hbm_gbs": (traffic * nl / (ms / 1e3) / 1e9) if traffic else None,
+                "effective_hbm_source": ("ncu dram__bytes_read.sum + dram__bytes_write.sum per launch of the benched "
+                                         "kernel (profiles/traffic.json) x launches / step time") if traffic else
+                                        "no ncu traffic record for this kernel/config",
                 "algorithmic_gbs_33B": 33 * amps * trotter / (ms / 1e3) / 1e9,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
                 "clocks": clocks, "p_succ_last": p_succ}

@@ -9,8 +9,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def run_reference(*extra):
-    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
-                          "--warmup", "0", "--cpu-sample-n", "16", *extra],
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "2",
+                          "--warmup", "1", *extra],
                          capture_output=True, text=True, cwd=ROOT, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
@@ -19,7 +19,9 @@ def run_reference(*extra):
 
 
 def test_reference_arm_line():
-    d = run_reference()
+    """At a small n (--qubits 16, the checked-in instance); the default is the
+    bench's n = 30 (one oracle step ~11 s on 16 cores, too long for the CPU suite)."""
+    d = run_reference("--qubits", "16")
     for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
               "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
         assert k in d, k
@@ -27,14 +29,16 @@ def test_reference_arm_line():
     assert d["value"] > 0 and d["unit"] == "steps/s" and d["higher_is_better"] is True
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
-    assert d["config"]["n"] == 30
+    assert d["config"]["n"] == 16
+    assert len(d["cpu_baseline"]["step_s"]) == 2 and d["cpu_baseline"]["cpu"]
+    # one oracle step of the schedule per bench step: ms_per_step is their mean
+    assert abs(d["ms_per_step"] / 1e3 - sum(d["cpu_baseline"]["step_s"]) / 2) < 1e-9
 
 
 def test_reference_arm_multi_gpu_units():
-    """--gpus 4 (rank 0 of a torchrun job): n = 32, whole-job shard-steps/s."""
-    one = run_reference()
-    four = run_reference("--gpus", "4")
-    assert four["config"]["n"] == 32 and four["n_gpus"] == 4
+    """--gpus 4 (rank 0 of a torchrun job): whole-job shard-steps/s, i.e. the
+    state's Trotter steps/s times 2^(n - 30) shards of 2^30 amplitudes."""
+    four = run_reference("--gpus", "4", "--qubits", "18")
+    assert four["config"]["n"] == 18 and four["n_gpus"] == 4
     assert four["unit"].startswith("shard-steps/s")
-    # 4 shards of 2^30 amplitudes per step at 4x the per-step cost: same order as N = 1
-    assert 0.2 < four["value"] / one["value"] < 5.0
+    assert abs(four["value"] - 2.0 ** (18 - 30) / (four["ms_per_step"] / 1e3)) < 1e-9 * four["value"]
