@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--tma-groups", type=int, default=0, help="0 = auto, 1 or 2 consumer groups per TMA CTA")
     ap.add_argument("--super", type=int, default=1,
                     help="QAA_OPT_SUPER bits (1 = L2-blocked Trotter steps, default; 0 = two HBM passes per step)")
+    ap.add_argument("--shard-sync", type=int, default=0,
+                    help="QAA_OPT_SHARD_SYNC: 0 = device-side phase barrier (default), 1 = host barrier")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--share-gpu", action="store_true",
@@ -267,13 +269,18 @@ def run_ours(args):
     # the timing events below are recorded on the same stream
     stream = torch.cuda.Stream(device=local)
     torch.cuda.set_stream(stream)
+    def apply_options(c):
+        """The same kernel configuration for the timed and the e2e contexts."""
+        c.set_option(q.OPT_ROW_BITS, args.row_bits)
+        c.set_option(q.OPT_STEP_SPANNING, args.step_spanning)
+        c.set_option(q.OPT_CTAS_PER_SM, args.ctas_per_sm)
+        c.set_option(q.OPT_KERNEL, args.kernel)
+        c.set_option(q.OPT_TMA_GROUPS, args.tma_groups)
+        c.set_option(q.OPT_SUPER, args.super)
+        c.set_option(q.OPT_SHARD_SYNC, args.shard_sync)
+
     ctx = q.Context(local, stream=stream.cuda_stream, rank=rank, world=world, comm=comm)
-    ctx.set_option(q.OPT_ROW_BITS, args.row_bits)
-    ctx.set_option(q.OPT_STEP_SPANNING, args.step_spanning)
-    ctx.set_option(q.OPT_CTAS_PER_SM, args.ctas_per_sm)
-    ctx.set_option(q.OPT_KERNEL, args.kernel)
-    ctx.set_option(q.OPT_TMA_GROUPS, args.tma_groups)
-    ctx.set_option(q.OPT_SUPER, args.super)
+    apply_options(ctx)
     ctx.load_instance(n, cl)
     ctx.init_uniform()
     chunk = args.chunk
@@ -369,8 +376,7 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         ctx2 = q.Context(local, stream=stream.cuda_stream, rank=rank, world=world, comm=comm)
-        ctx2.set_option(q.OPT_ROW_BITS, args.row_bits)
-        ctx2.set_option(q.OPT_STEP_SPANNING, args.step_spanning)
+        apply_options(ctx2)
         lits = np.ascontiguousarray(np.asarray(cl, dtype=np.int32).reshape(-1))
         pinned = torch.from_numpy(lits).pin_memory().numpy()
         e2e_steps = max(2, min(args.steps, 10))

@@ -50,13 +50,17 @@ typedef enum {
   QAA_E_STATE = 4, /* call out of order (e.g. evolve before init), or the
                       context is poisoned by an earlier CUDA/NCCL error      */
   QAA_E_CUDA = 5,  /* CUDA runtime error (poisons the context)              */
-  QAA_E_NCCL = 6   /* NCCL error (poisons the context)                      */
+  QAA_E_NCCL = 6   /* a host collective (qaa_comm callback) failed; poisons
+                      the context. The name is historical: the sharded path
+                      uses CUDA IPC peer stores, not NCCL                    */
 } qaa_status;
 
 typedef struct qaa_ctx qaa_ctx;
 
-/* Host-side collectives the library needs when world > 1 (bootstrap of the
- * CUDA-IPC peer pointers, one barrier per Trotter step, scalar reductions).
+/* Host-side collectives the library needs when world > 1: the bootstrap of the
+ * CUDA-IPC peer pointers at load, the scalar reductions of the observables, and
+ * the per-phase barrier only when QAA_OPT_SHARD_SYNC = 1 (by default the phase
+ * barrier runs on the device, through IPC-mapped arrival counters).
  * The caller implements them over its process group (the Python binding uses
  * torch.distributed). Both return 0 on success; any other value makes the
  * library call fail with QAA_E_NCCL (and poisons the context).
@@ -131,7 +135,9 @@ qaa_status qaa_init_basis(qaa_ctx* ctx, uint64_t x);
  * dt = T/steps, s_k = schedule[k] if schedule != NULL (host array of `steps`
  * doubles in [0, 1]) else (k + 0.5)/steps. T = 0 is the identity.
  * Coefficients are computed on the host in binary64 (R11). Enqueued on the
- * stream; returns without a host sync. The state is left in canonical layout.
+ * stream; returns without a host sync (also when sharded: the per-phase
+ * barrier runs on the device unless QAA_OPT_SHARD_SYNC = 1). The state is left
+ * in canonical layout.
  * Errors: STATE (no init), USAGE (T < 0 or not finite, steps < 1, a schedule
  * value outside [0, 1]). Collective when world > 1 (identical arguments). */
 qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t steps, const double* schedule);
@@ -259,6 +265,11 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *  QAA_OPT_SUPER_SPLIT   split roles in the L2-blocked launch: this many CTAs run only the
  *                        group-0 tiles (from HBM), the others only the group-k tiles, each
  *                        side in chunk order (0 = one interleaved sequence, default).
+ *  QAA_OPT_SHARD_SYNC    sharded phase barrier: 0 (default) = on the device (every rank adds
+ *                        1 to every rank's CUDA-IPC-mapped arrival counter after its peer
+ *                        stores, then waits for its own to reach epoch * world), so a
+ *                        sharded qaa_evolve is enqueued without a host sync; 1 = stream
+ *                        sync + the caller's qaa_comm barrier per phase (the round-1 plan).
  *  QAA_OPT_ENERGY_W64    test hook: 1 = the 64-bit energy-table kernel even when every
  *                        assignment fits 32 bits (default 0: 32-bit kernel for n <= 32).
  *  QAA_OPT_ORDER         1 (default) = first-order Lie-Trotter, D then X (R7);
@@ -276,7 +287,8 @@ enum {
   QAA_OPT_ORDER = 8,
   QAA_OPT_ENERGY_W64 = 9,
   QAA_OPT_SUPER_GRID = 10,
-  QAA_OPT_SUPER_SPLIT = 11
+  QAA_OPT_SUPER_SPLIT = 11,
+  QAA_OPT_SHARD_SYNC = 12
 };
 qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value);
 

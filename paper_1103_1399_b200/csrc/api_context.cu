@@ -75,6 +75,9 @@ void qaa_destroy(qaa_ctx* ctx) {
     if (ctx->bufs[b]) cudaFree(ctx->bufs[b]);
   }
   if (ctx->E_B) cudaFree(ctx->E_B);
+  for (int r = 0; r < 8; r++)
+    if (ctx->peer_sync_open[r]) cudaIpcCloseMemHandle(ctx->peer_sync[r]);
+  if (ctx->sync_buf) cudaFree(ctx->sync_buf);
   for (int b = 0; b < 2; b++)
     if (ctx->shard_top_eg[b]) cudaFree(ctx->shard_top_eg[b]);
   for (int k = 0; k < 4; k++)
@@ -132,6 +135,10 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
     case QAA_OPT_SUPER_SPLIT:
       if (value < 0 || value >= ctx->num_sms) return fail(ctx, QAA_E_USAGE, "super split must be in 0..%d", ctx->num_sms - 1);
       ctx->super_split = (int)value;
+      return QAA_OK;
+    case QAA_OPT_SHARD_SYNC:
+      if (value < 0 || value > 1) return fail(ctx, QAA_E_USAGE, "shard sync must be 0 (device) or 1 (host)");
+      ctx->shard_sync = (int)value;
       return QAA_OK;
     case QAA_OPT_PROFILE:
       ctx->profile = value != 0;

@@ -133,6 +133,11 @@ struct qaa_ctx {
   int cur = 0;                       // buffer holding the current state
   double2* peers[2][8] = {{nullptr}};  // peers[b][r]: rank r's buffer b (own rank: local pointer)
   bool peer_open[2][8] = {{false}};
+  unsigned* sync_buf = nullptr;      // own arrival counter of the device-side phase barrier (IPC-exported)
+  unsigned* peer_sync[8] = {nullptr};  // every rank's counter (own rank: local pointer)
+  bool peer_sync_open[8] = {false};
+  unsigned sync_epoch = 0;           // barriers issued so far (identical on every rank)
+  int shard_sync = 0;                // 0: device-side barrier (async evolve), 1: host barrier + stream sync
   uint8_t* E_B = nullptr;            // energies in layout B
   size_t E_B_cap = 0;
   // stats
@@ -230,6 +235,7 @@ qaa_status comm_allgather(qaa_ctx* ctx, const void* send, void* recv, size_t byt
 qaa_status comm_sum(qaa_ctx* ctx, double* v, int n);
 qaa_status setup_shard_buffers(qaa_ctx* ctx, size_t bytes);
 qaa_status shard_remap(qaa_ctx* ctx);
+qaa_status shard_barrier(qaa_ctx* ctx);
 qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<StepCoef>& sc, const double2* dphi, int n_phi);
 // api_evolve.cu: coefficient rows (H1), profiling events, plan choice
 void build_step(double T, int64_t K, double wb, double theta, int n, int n_phi, double2* phi_row, StepCoef* sc);

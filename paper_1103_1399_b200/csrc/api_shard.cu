@@ -51,22 +51,44 @@ qaa_status setup_shard_buffers(qaa_ctx* ctx, size_t bytes) {
     }
   }
   ctx->buf_cap = bytes;
-  cudaIpcMemHandle_t mine[2];
+  // the device-side phase barrier's arrival counter (zeroed before any peer can
+  // signal: peers first pass the host barrier below)
+  if (!ctx->sync_buf) {
+    CUDA_TRY(cudaMalloc(&ctx->sync_buf, 256));
+    CUDA_TRY(cudaMemset(ctx->sync_buf, 0, 256));
+    ctx->sync_epoch = 0;
+    for (int r = 0; r < 8; r++) {
+      if (ctx->peer_sync_open[r]) cudaIpcCloseMemHandle(ctx->peer_sync[r]);
+      ctx->peer_sync_open[r] = false;
+      ctx->peer_sync[r] = nullptr;
+    }
+  }
+  cudaIpcMemHandle_t mine[3];
   for (int b = 0; b < 2; b++) CUDA_TRY(cudaIpcGetMemHandle(&mine[b], ctx->bufs[b]));
-  std::vector<cudaIpcMemHandle_t> all(2 * (size_t)ctx->world);
+  CUDA_TRY(cudaIpcGetMemHandle(&mine[2], ctx->sync_buf));
+  std::vector<cudaIpcMemHandle_t> all(3 * (size_t)ctx->world);
   qaa_status st = comm_allgather(ctx, mine, all.data(), sizeof mine);
   if (st) return st;
-  for (int r = 0; r < ctx->world; r++)
+  for (int r = 0; r < ctx->world; r++) {
     for (int b = 0; b < 2; b++) {
       if (r == ctx->rank) {
         ctx->peers[b][r] = ctx->bufs[b];
         continue;
       }
       void* p = nullptr;
-      CUDA_TRY(cudaIpcOpenMemHandle(&p, all[2 * (size_t)r + b], cudaIpcMemLazyEnablePeerAccess));
+      CUDA_TRY(cudaIpcOpenMemHandle(&p, all[3 * (size_t)r + b], cudaIpcMemLazyEnablePeerAccess));
       ctx->peers[b][r] = (double2*)p;
       ctx->peer_open[b][r] = true;
     }
+    if (r == ctx->rank) {
+      ctx->peer_sync[r] = ctx->sync_buf;
+    } else if (!ctx->peer_sync_open[r]) {
+      void* p = nullptr;
+      CUDA_TRY(cudaIpcOpenMemHandle(&p, all[3 * (size_t)r + 2], cudaIpcMemLazyEnablePeerAccess));
+      ctx->peer_sync[r] = (unsigned*)p;
+      ctx->peer_sync_open[r] = true;
+    }
+  }
   st = comm_barrier(ctx);
   if (st) return st;
   ctx->cur = 0;
@@ -76,13 +98,28 @@ qaa_status setup_shard_buffers(qaa_ctx* ctx, size_t bytes) {
   return QAA_OK;
 }
 
+// End of a phase: every rank's peer stores into the others' next buffers are
+// complete and visible before anyone reads its next buffer. Default: the
+// device-side barrier (enqueued, no host sync: evolve stays asynchronous);
+// QAA_OPT_SHARD_SYNC = 1: stream sync + the caller's host barrier.
+qaa_status shard_barrier(qaa_ctx* ctx) {
+  if (ctx->shard_sync == 1 || !ctx->sync_buf) {
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return comm_barrier(ctx);
+  }
+  ctx->sync_epoch++;
+  CUDA_TRY(launch_shard_barrier(ctx->peer_sync, ctx->sync_buf, ctx->world, ctx->sync_epoch * (unsigned)ctx->world,
+                                ctx->stream));
+  ctx->stats.kernel_launches_total++;
+  return QAA_OK;
+}
+
 // one layout swap (A <-> B) of the whole sharded state: stores, barrier, flip
 qaa_status shard_remap(qaa_ctx* ctx) {
   CUDA_TRY(launch_remap(ctx->bufs[ctx->cur], ctx->peers[ctx->cur ^ 1], (int64_t)1 << ctx->L, ctx->L - ctx->gbits,
                         ctx->rank, ctx->num_sms, ctx->stream));
   ctx->stats.kernel_launches_total++;
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  qaa_status st = comm_barrier(ctx);
+  qaa_status st = shard_barrier(ctx);
   if (st) return st;
   ctx->cur ^= 1;
   ctx->state = ctx->bufs[ctx->cur];
@@ -92,7 +129,8 @@ qaa_status shard_remap(qaa_ctx* ctx) {
 
 // Sharded evolve (plan.hpp ShardPass): every phase ends with a
 // pass whose tiles are stored straight into the peers' other shard buffer
-// (the bit swap of the top local and the rank qubits), then one host barrier.
+// (the bit swap of the top local and the rank qubits), then one phase barrier
+// (device side by default: the whole evolve is enqueued without a host sync).
 
 qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<StepCoef>& sc, const double2* dphi,
                                  int n_phi) {
@@ -180,8 +218,7 @@ qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<StepCoef>& 
         ctx->stats.pass_launches++;
         ctx->stats.super_launches++;
         ctx->stats.kernel_launches_total++;
-        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-        qaa_status st = comm_barrier(ctx);
+        qaa_status st = shard_barrier(ctx);
         if (st) return st;
         ctx->cur ^= 1;
         ctx->state = ctx->bufs[ctx->cur];
@@ -258,8 +295,7 @@ qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<StepCoef>& 
     ctx->stats.pass_launches++;
     ctx->stats.kernel_launches_total++;
     if (sp.remote) {
-      CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-      qaa_status st = comm_barrier(ctx);
+      qaa_status st = shard_barrier(ctx);
       if (st) return st;
       ctx->cur ^= 1;
       ctx->state = ctx->bufs[ctx->cur];

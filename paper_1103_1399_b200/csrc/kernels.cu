@@ -961,4 +961,39 @@ cudaError_t launch_permute_energy(const uint8_t* E, uint8_t* Eg, const int (&phy
   permute_energy_kernel<<<(int)grid, 256, 0, st>>>(E, Eg, a, pos);
   return cudaGetLastError();
 }
+// ------------------------------------------------------------------ sharded phase barrier (device side)
+// One thread: release this rank's prior stores at system scope, add 1 to every
+// rank's arrival counter (CUDA-IPC-mapped; peers' counters over NVLink), then
+// wait until the own counter reaches `target` = epoch * world. Kernels queued
+// behind it on the stream see every peer's pre-barrier stores. A bounded wait:
+// a rank that never arrives becomes a trap (launch error), not a hang.
+struct ShardSyncArgs {
+  unsigned* peer[8];
+  unsigned* mine;
+  int world;
+  unsigned target;
+};
+__global__ void shard_barrier_kernel(const ShardSyncArgs a) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  for (int r = 0; r < a.world; r++) asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(a.peer[r]) : "memory");
+  for (unsigned long long it = 0;; it++) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.mine) : "memory");
+    if ((int)(v - a.target) >= 0) break;
+    __nanosleep(100);
+    if (it > (1ull << 31)) __trap();
+  }
+  __threadfence_system();
+}
+cudaError_t launch_shard_barrier(unsigned* const* peer_flags, unsigned* my_flag, int world, unsigned target,
+                                 cudaStream_t st) {
+  ShardSyncArgs a;
+  for (int r = 0; r < 8; r++) a.peer[r] = r < world ? peer_flags[r] : nullptr;
+  a.mine = my_flag;
+  a.world = world;
+  a.target = target;
+  shard_barrier_kernel<<<1, 32, 0, st>>>(a);
+  return cudaGetLastError();
+}
 }  // namespace qaa

@@ -146,6 +146,11 @@ void superpass_tm_energy_positions(uint16_t* pos);  // host: TILE entries
 cudaError_t launch_superpass_tm(const CUtensorMap* kmap, const SuperArgs& a, int ngroups, bool bd, int grid,
                                 cudaStream_t st);
 
+// Sharded phase barrier on the device (api_shard.cu shard_barrier): add 1 to
+// every rank's IPC-mapped arrival counter, wait for the own one to reach target.
+cudaError_t launch_shard_barrier(unsigned* const* peer_flags, unsigned* my_flag, int world, unsigned target,
+                                 cudaStream_t st);
+
 // Whole-evolution kernel for L <= 12 local qubits: one CTA keeps the state in
 // shared memory for all K steps (SURVEY §7 hard part 5; latency-bound sizes).
 struct ResidentArgs {

@@ -19,7 +19,7 @@ __all__ = [
     "qaa_init_basis", "qaa_evolve", "qaa_sweep", "qaa_time_energy_table", "qaa_set_driver", "qaa_spectrum", "qaa_success_prob", "qaa_energy", "qaa_norm2", "qaa_sigma_x",
     "qaa_num_solutions", "qaa_max_energy", "qaa_copy_state", "qaa_set_state", "qaa_copy_energy_table",
     "qaa_state_ptr", "qaa_set_option", "qaa_get_stats", "qaa_reset_stats", "qaa_plan_describe",
-    "qaa_version", "OPT_ROW_BITS", "OPT_PROFILE", "OPT_STEP_SPANNING", "OPT_CTAS_PER_SM", "OPT_KERNEL", "OPT_TMA_GROUPS", "OPT_SUPER", "OPT_ORDER", "OPT_ENERGY_W64", "OPT_SUPER_GRID", "OPT_SUPER_SPLIT",
+    "qaa_version", "OPT_ROW_BITS", "OPT_PROFILE", "OPT_STEP_SPANNING", "OPT_CTAS_PER_SM", "OPT_KERNEL", "OPT_TMA_GROUPS", "OPT_SUPER", "OPT_ORDER", "OPT_ENERGY_W64", "OPT_SUPER_GRID", "OPT_SUPER_SPLIT", "OPT_SHARD_SYNC",
     "PLAN_RECORD", "SHARD_RECORD", "TorchComm", "qaa_plan_describe_sharded",
 ]
 
@@ -33,6 +33,7 @@ OPT_ROW_BITS, OPT_PROFILE, OPT_STEP_SPANNING, OPT_CTAS_PER_SM, OPT_KERNEL, OPT_T
 OPT_ENERGY_W64 = 9
 OPT_SUPER_GRID = 10
 OPT_SUPER_SPLIT = 11
+OPT_SHARD_SYNC = 12
 PLAN_RECORD = 10
 SHARD_RECORD = 10
 
@@ -78,8 +79,10 @@ class TorchComm:
         self._b = BARRIER_FN(self._barrier)
         self._a = ALLGATHER_FN(self._allgather)
         self.struct = qaa_comm(None, self._b, self._a)
+        self.calls = {"barrier": 0, "allgather": 0}  # how often libqaa called back (tests)
 
     def _barrier(self, user):
+        self.calls["barrier"] += 1
         try:
             self.dist.barrier(group=self.group)
             return 0
@@ -87,6 +90,7 @@ class TorchComm:
             return 1
 
     def _allgather(self, user, send, recv, nbytes):
+        self.calls["allgather"] += 1
         try:
             import torch
             mine = torch.frombuffer(bytearray(ctypes.string_at(send, nbytes)), dtype=torch.uint8) if nbytes else \

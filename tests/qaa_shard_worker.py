@@ -40,9 +40,12 @@ def shard_worker(rank, world, port, outdir, n, clauses, T, K, schedule, psi0, s_
         ctx.init_uniform()
     else:
         ctx.set_state(psi0)  # each rank copies the part it owns
+    before = dict(comm.calls)
     ctx.evolve(T, K, schedule)
+    host_calls = {k: comm.calls[k] - before[k] for k in before}  # during evolve (no sync yet)
     local = ctx.state(rank << L, 1 << L)
     res = {"state": local, "super_launches": ctx.stats()["super_launches"], "groups": ctx.stats()["groups"],
+           "host_calls": host_calls,
            "success": ctx.success_prob(), "norm2": ctx.norm2(),
            "sigma_x": ctx.sigma_x(), "energy": np.array([ctx.energy(s) for s in s_values]),
            "nsol": ctx.num_solutions(), "emax": ctx.max_energy(), "E": ctx.energy_table(rank << L, 1 << L)}

@@ -32,12 +32,16 @@ def test_torchcomm_callbacks_gloo_world2():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,world,K,fused", [(16, 2, 5, 0), (17, 4, 4, 0), (18, 8, 3, 0), (22, 2, 4, 0), (24, 4, 3, 0),
-                                             (24, 2, 3, 1), (24, 4, 4, 1), (25, 8, 3, 1)])
-def test_sharded_evolution_parity(n, world, K, fused):
+@pytest.mark.parametrize("n,world,K,fused,hostsync", [(16, 2, 5, 0, 0), (17, 4, 4, 0, 0), (18, 8, 3, 0, 0),
+                                                      (22, 2, 4, 0, 0), (24, 4, 3, 0, 0), (24, 2, 3, 1, 0),
+                                                      (24, 4, 4, 1, 0), (25, 8, 3, 1, 0), (24, 4, 3, 1, 1),
+                                                      (18, 8, 3, 0, 1)])
+def test_sharded_evolution_parity(n, world, K, fused, hostsync):
     """fused = 1: three local tile groups with the [group 0][group 1 + layout
     swap] pass pair of every phase as one L2-blocked launch (QAA_OPT_SUPER 17:
-    forced below the 256-chunk threshold at these test sizes)."""
+    forced below the 256-chunk threshold at these test sizes). hostsync = 0
+    (default): the per-phase barrier runs on the device, so evolve makes no host
+    collective call at all; 1: stream sync + qaa_comm barrier per phase."""
     from oracle import oracle
     import paper_1103_1399_b200 as q
     cl = cnf.load_instance(n)[0] if os.path.exists(cnf.instance_path(n)) else cnf.random_instance(n, 4 * n, n)
@@ -46,12 +50,15 @@ def test_sharded_evolution_parity(n, world, K, fused):
     psi0 = cnf.random_state(n, 5)
     s_values = [0.0, 0.3, 1.0]
     with tempfile.TemporaryDirectory() as d:
-        opts = {q.OPT_SUPER: 17} if fused else None
+        opts = {q.OPT_SUPER: 17} if fused else {}
+        opts[q.OPT_SHARD_SYNC] = hostsync
         mp.spawn(W.shard_worker, args=(world, free_port(), d, n, cl, T, K, sched, psi0, s_values, opts),
                  nprocs=world, join=True)
         res = [np.load(os.path.join(d, f"rank{r}.npy"), allow_pickle=True).item() for r in range(world)]
     for r in res:
         assert (r["super_launches"] == K) if fused else (r["super_launches"] == 0)
+        assert r["host_calls"]["allgather"] == 0
+        assert (r["host_calls"]["barrier"] > 0) if hostsync else (r["host_calls"]["barrier"] == 0)
     got = np.concatenate([r["state"] for r in res])
     E = oracle.energy_table(n, cl)
     want = oracle.evolve(n, E, psi0, T, K, sched)
