@@ -270,6 +270,12 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        stores, then waits for its own to reach epoch * world), so a
  *                        sharded qaa_evolve is enqueued without a host sync; 1 = stream
  *                        sync + the caller's qaa_comm barrier per phase (the round-1 plan).
+ *  QAA_OPT_PERSIST       1: for 13 <= n - log2(world) <= 21 on one GPU with the automatic
+ *                        kernel choice, all K steps run as ONE cooperative launch of the
+ *                        persistent pass kernel (state L2-resident, a grid barrier between
+ *                        passes) instead of one launch per pass. 0 (default): per-pass
+ *                        launches -- measured faster (7.4 vs 8.9 us/step at n = 13..18:
+ *                        a pass is bound by one CTA's tile program, not by the launch).
  *  QAA_OPT_ENERGY_W64    test hook: 1 = the 64-bit energy-table kernel even when every
  *                        assignment fits 32 bits (default 0: 32-bit kernel for n <= 32).
  *  QAA_OPT_ORDER         1 (default) = first-order Lie-Trotter, D then X (R7);
@@ -288,7 +294,8 @@ enum {
   QAA_OPT_ENERGY_W64 = 9,
   QAA_OPT_SUPER_GRID = 10,
   QAA_OPT_SUPER_SPLIT = 11,
-  QAA_OPT_SHARD_SYNC = 12
+  QAA_OPT_SHARD_SYNC = 12,
+  QAA_OPT_PERSIST = 13
 };
 qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value);
 
@@ -308,6 +315,7 @@ typedef struct {
   double super_kernel_ms;    /* of pass_kernel_ms: their event-timed durations */
   int64_t super_kernels_timed;
   int64_t tm_launches;       /* of super_launches: tensor-memory exchange variant (pass_tmem.cu) */
+  int64_t persist_launches;  /* of pass_launches: persistent whole-evolve launches (QAA_OPT_PERSIST) */
   uint64_t tm_diag[8];       /* diagnostics (QAA_OPT_SUPER bit 10), summed over warps' lane 0 since the
                                 context's first such launch: [0] cycles in slot-landed waits, [1] items,
                                 [2] deferred group-k items, [3] cycles in deferred waits, [4] / [5]

@@ -84,6 +84,7 @@ void qaa_destroy(qaa_ctx* ctx) {
     if (ctx->Eg_tm[k]) cudaFree(ctx->Eg_tm[k]);
   if (ctx->d_pos_tm) cudaFree(ctx->d_pos_tm);
   if (ctx->d_tm_diag) cudaFree(ctx->d_tm_diag);
+  if (ctx->d_persist) cudaFree(ctx->d_persist);
   if (ctx->coef_done) cudaEventDestroy(ctx->coef_done);
   for (auto& p : ctx->ev_pool) {
     cudaEventDestroy(p.first);
@@ -139,6 +140,10 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
     case QAA_OPT_SHARD_SYNC:
       if (value < 0 || value > 1) return fail(ctx, QAA_E_USAGE, "shard sync must be 0 (device) or 1 (host)");
       ctx->shard_sync = (int)value;
+      return QAA_OK;
+    case QAA_OPT_PERSIST:
+      if (value < 0 || value > 1) return fail(ctx, QAA_E_USAGE, "persist must be 0 or 1");
+      ctx->persist = (int)value;
       return QAA_OK;
     case QAA_OPT_PROFILE:
       ctx->profile = value != 0;

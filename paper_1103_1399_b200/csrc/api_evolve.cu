@@ -145,6 +145,86 @@ static const Program* get_program(qaa_ctx* ctx, int g, bool pre, bool d, bool po
   return &(ctx->progs[key] = p);
 }
 
+
+// Persistent evolve (pass_fast.cu qaa_persist): 13 <= L <= 21 with the
+// automatic kernel choice, first-order steps in tangent form, every pass one of
+// the compiled-in register programs. One cooperative launch for all K steps
+// (the state stays in L2), a grid barrier between passes. Returns false (and
+// leaves *st untouched) when not applicable.
+static bool pass_fast_prog(const qaa_ctx* ctx, const PassPlan& pp, const std::vector<StepCoef>& sc, int* fp_out) {
+  const Group& gr = ctx->geom.groups[(size_t)pp.group];
+  const bool pre = pp.pre_step >= 0, d = pp.d_step >= 0, post = pp.post_step >= 0;
+  int fp = -1;
+  if (pp.group == 0) {
+    if (!pre && d && post) fp = FP_G0_DPOST;
+    else if (pre && !d && !post) fp = FP_G0_PRE;
+    else if (pre && d && post) fp = FP_G0_PRE_D_POST;
+  } else if ((gr.rot_local & ~0xFF8u) == 0) {
+    if (pre && !d && !post) fp = FP_GK_PRE;
+    else if (d && post) fp = FP_GK_PRE_D_POST;
+  }
+  if ((pre && sc[(size_t)pp.pre_step].form != 0) || (post && sc[(size_t)pp.post_step].form != 0)) fp = -1;
+  *fp_out = fp;
+  return fp >= 0;
+}
+
+static bool try_persist(qaa_ctx* ctx, const std::vector<PassPlan>& plan, const std::vector<StepCoef>& sc,
+                        const double2* dphi, const double* dcoef, int n_phi, qaa_status* st) {
+  if (!ctx->persist || ctx->world != 1 || ctx->kernel_mode != 2 || ctx->order != 1) return false;
+  if (ctx->L < 13 || ctx->L > PERSIST_MAX_L || ctx->geom.groups.size() > 4 || n_phi > 256) return false;
+  std::vector<PersistPass> recs(plan.size());
+  for (size_t i = 0; i < plan.size(); i++) {
+    const PassPlan& pp = plan[i];
+    int fp;
+    if (!pass_fast_prog(ctx, pp, sc, &fp)) return false;
+    const Group& gr = ctx->geom.groups[(size_t)pp.group];
+    // LANE3 (rotate tile bit 3 with lane shuffles) exists only for group k > 0 programs
+    const int lane3 = pp.group > 0 ? (int)((gr.rot_local >> 3) & 1) : 0;
+    recs[i] = PersistPass{fp, lane3, pp.group, (int)pp.pre_step, (int)pp.d_step, (int)pp.post_step};
+  }
+  const int maxg = persist_max_grid(ctx->num_sms);
+  if (maxg <= 0) return false;
+  const size_t bytes = recs.size() * sizeof(PersistPass) + 256;
+  if (ctx->d_persist_cap < bytes) {
+    CUDA_TRY_ST(cudaStreamSynchronize(ctx->stream));
+    *st = ensure_buffer(ctx, &ctx->d_persist, &ctx->d_persist_cap, bytes);
+    if (*st) return true;
+  }
+  unsigned* bar = (unsigned*)ctx->d_persist;
+  PersistPass* dpass = (PersistPass*)((char*)ctx->d_persist + 256);
+  CUDA_TRY_ST(cudaMemsetAsync(bar, 0, 256, ctx->stream));
+  CUDA_TRY_ST(cudaMemcpyAsync(dpass, recs.data(), recs.size() * sizeof(PersistPass), cudaMemcpyHostToDevice,
+                              ctx->stream));
+  PersistLaunch L;
+  L.psi = ctx->state;
+  L.E = ctx->E;
+  L.passes = dpass;
+  L.npass = (int)recs.size();
+  L.phi_all = dphi;
+  L.n_phi = n_phi;
+  L.coef = dcoef;
+  L.ngroups = (int)ctx->geom.groups.size();
+  L.groups = ctx->geom.groups.data();
+  L.bar = bar;
+  const int grid = (int)std::min<int64_t>(ctx->geom.groups[0].ntiles, maxg);
+  size_t ev = ctx->ev_used;
+  if (ctx->profile) {
+    *st = ensure_events(ctx, ev + 1);
+    if (*st) return true;
+    CUDA_TRY_ST(cudaEventRecord(ctx->ev_pool[ev].first, ctx->stream));
+  }
+  CUDA_TRY_ST(launch_persist(L, grid, ctx->stream));
+  if (ctx->profile) {
+    CUDA_TRY_ST(cudaEventRecord(ctx->ev_pool[ev].second, ctx->stream));
+    ctx->ev_used = ev + 1;
+  }
+  ctx->stats.pass_launches++;
+  ctx->stats.persist_launches++;
+  ctx->stats.kernel_launches_total++;
+  *st = QAA_OK;
+  return true;
+}
+
 extern "C" {
 
 qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule) {
@@ -245,6 +325,10 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
   // Strang: the closing half step D_K follows the pass that completes X_{K-1}
   // (its program becomes rotate + D; it runs on the generic kernel)
   if (ctx->order == 2) plan.back().d_step = K;
+  {
+    qaa_status st = QAA_OK;
+    if (try_persist(ctx, plan, sc, dphi, dcoef, n_phi, &st)) return st;
+  }
   const int max_grid = ctx->num_sms * ctx->ctas_per_sm;
   if (ctx->profile) {
     qaa_status st = ensure_events(ctx, ctx->ev_used + plan.size());

@@ -27,6 +27,7 @@ namespace {
 constexpr int64_t ZLIST_CAP = 1 << 16;  // keep Z as a sorted list up to this size
 constexpr int RESIDENT_MAX_L = TILE_BITS;
 constexpr int SWEEP_MAX_L = 16;
+constexpr int PERSIST_MAX_L = 21;
 // The L2-blocked step pays from 256 chunks up (n >= 28 on one GPU, measured):
 // below that the strided groups have padded 256-byte rows, the two-pass plan
 // streams at the copy peak and the chunk pipeline is too short (n = 24: 0.44
@@ -102,7 +103,10 @@ struct qaa_ctx {
   int super_tm_flags = 0;
   int super_lag = 1;
   int super_grid = 0;  // 0: one CTA per SM
-  int super_split = 0;  // split roles: CTAs running group-0 tiles only (0 = interleaved sequence)
+  int super_split = 0;
+  int persist = 0;  // persistent evolve for 13 <= L <= 21 (opt-in: measured slower)
+  void* d_persist = nullptr;  // its barrier words and pass records
+  size_t d_persist_cap = 0;  // split roles: CTAs running group-0 tiles only (0 = interleaved sequence)
   unsigned long long* d_tm_diag = nullptr;  // pass_tmem.cu diagnostics counters (QAA_OPT_SUPER bit 10)
   int tm_ok[4] = {0, 0, 0, 0};  // per paired group: swizzled map (+ K3-packed energies) ready
   CUtensorMap tmaps_sw[4];
@@ -167,6 +171,17 @@ inline qaa_status fail(qaa_ctx* c, qaa_status st, const char* fmt, ...) {
     if (e_ != cudaSuccess)                                                                  \
       return fail(ctx, QAA_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
                   __FILE__, __LINE__);                                                      \
+  } while (0)
+
+// CUDA_TRY for helpers that report through a status out-parameter and return true
+#define CUDA_TRY_ST(call)                                                                          \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) {                                                                       \
+      *st = fail(ctx, QAA_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                 __LINE__);                                                                        \
+      return true;                                                                                 \
+    }                                                                                              \
   } while (0)
 
 #define CHECK_CTX()                                                             \

@@ -73,6 +73,27 @@ cudaError_t launch_remap(const double2* src, double2* const* peers, int64_t N, i
 constexpr int FAST_XBUF = TILE + TILE / 16;  // padded exchange buffer (amplitudes)
 constexpr size_t FAST_SMEM_BYTES = sizeof(double2) * (FAST_XBUF + 256 * 8);  // + 8 copies of the D table
 cudaError_t pass_fast_setup();
+
+// Persistent evolve (pass_fast.cu qaa_persist) for 13 <= L <= 21: all passes of
+// the plan in one cooperative launch, a grid barrier between passes.
+struct PersistPass {
+  int fp, lane3, group;
+  int pre, d, post;  // step indices, -1 = absent
+};
+struct PersistLaunch {
+  double2* psi;
+  const uint8_t* E;
+  const PersistPass* passes;  // device array
+  int npass;
+  const double2* phi_all;
+  int n_phi;
+  const double* coef;
+  int ngroups;
+  const Group* groups;        // host, copied by value into the launch
+  unsigned* bar;              // device [2], zeroed
+};
+int persist_max_grid(int num_sms);
+cudaError_t launch_persist(const PersistLaunch& L, int grid, cudaStream_t st);
 cudaError_t launch_pass_fast(const FastArgs& a, int prog, bool lane3, bool prefetch, int grid, cudaStream_t st);
 
 // Warp-specialised TMA pass (pass_tma.cu): same programs as FastArgs, tiles

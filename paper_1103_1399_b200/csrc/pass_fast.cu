@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 
 #include "pass_common.cuh"
 
@@ -105,13 +106,14 @@ __device__ __forceinline__ void program(const FastArgs& a, double2 (&v)[RPT], co
   }
 }
 
-template <bool HAS_D>
+// CG = true: L2-only loads (data written by other SMs earlier in the same launch)
+template <bool HAS_D, bool CG = false>
 __device__ __forceinline__ void load(const FastArgs& a, const Off& pa, const Off& pe, int64_t T, double2 (&v)[RPT],
                                      uint32_t (&ep)[4]) {
   const int64_t base = tbase(a, T);
   const double2* src = a.psi + base;
 #pragma unroll
-  for (int r = 0; r < RPT; r++) v[r] = src[roff(pa, r)];
+  for (int r = 0; r < RPT; r++) v[r] = CG ? __ldcg(src + roff(pa, r)) : src[roff(pa, r)];
   if (HAS_D) {
     const uint8_t* eb = a.E + base;
 #pragma unroll
@@ -194,6 +196,120 @@ __global__ void __launch_bounds__(NTHREADS, PREFETCH ? 1 : 2) qaa_pass_fast(cons
   if (a.remote) __threadfence_system();
 }
 
+
+// ============================================================================
+// Persistent evolve for 13 <= L <= 21 (one launch for all K steps): the state
+// (1..32 MiB) stays in L2, every pass of the plan runs over the CTA's tiles
+// and ends with a grid barrier -- instead of one launch (~8 us of launch and
+// ramp latency at n = 16) per pass. Cooperative launch (co-residency).
+// ============================================================================
+struct PersistGroup {
+  int phys[TILE_BITS];
+  uint32_t rot_local;
+  int nseg;
+  int seg_src[MAX_SEGS], seg_dst[MAX_SEGS], seg_len[MAX_SEGS];
+  int64_t ntiles;
+};
+struct PersistArgs {
+  double2* psi;
+  const uint8_t* E;
+  const PersistPass* passes;   // npass records (device)
+  int npass;
+  const double2* phi_all;      // step k's D row at phi_all + k n_phi
+  int n_phi;
+  const double* coef;          // tan(beta_k) per step
+  PersistGroup groups[4];
+  unsigned* bar;               // [2]: arrival count, generation (zeroed before launch)
+};
+
+// sense-free grid barrier: the last arriving CTA resets the count and bumps
+// the generation; stores before it are released at gpu scope
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned gen;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      for (;;) {
+        unsigned g;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+        if (g != gen) break;
+        __nanosleep(20);
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int PROG, bool LANE3>
+__device__ __forceinline__ void persist_pass(const FastArgs& a, double2* xb, const double2* phis, int lane, int warp) {
+  using PI = ProgInfo<PROG>;
+  const Off pa = make_off<PA>(a, lane, warp);
+  const Off pe = make_off<PI::e_pat>(a, lane, warp);
+  const Off ps = make_off<PI::store_pat>(a, lane, warp);
+  double2 v[RPT];
+  uint32_t ep[4] = {0, 0, 0, 0};
+  for (int64_t T = blockIdx.x; T < a.ntiles; T += gridDim.x) {
+    load<PI::has_d, true>(a, pa, pe, T, v, ep);
+    program<PROG, LANE3>(a, v, ep, xb, phis, lane, warp);
+    store(a, ps, T, v);
+  }
+}
+
+__global__ void __launch_bounds__(NTHREADS, 2) qaa_persist(const PersistArgs pa) {
+  extern __shared__ double2 smem[];
+  double2* xb = smem;
+  double2* phis = smem + FAST_XBUF;
+  __shared__ FastArgs fa;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int p = 0; p < pa.npass; p++) {
+    const PersistPass r = pa.passes[p];
+    if (tid == 0) {
+      const PersistGroup& gr = pa.groups[r.group];
+      fa.psi = pa.psi;
+      fa.E = pa.E;
+      fa.phi = r.d >= 0 ? pa.phi_all + (int64_t)r.d * pa.n_phi : nullptr;
+      fa.n_phi = pa.n_phi;
+      const double c0 = r.pre >= 0 ? pa.coef[r.pre] : 0.0, c1 = r.post >= 0 ? pa.coef[r.post] : 0.0;
+      for (int b = 0; b < TILE_BITS; b++) {
+        const bool rb = (gr.rot_local >> b) & 1;
+        fa.t[0][b] = rb ? c0 : 0.0;
+        fa.t[1][b] = rb ? c1 : 0.0;
+        fa.phys[b] = gr.phys[b];
+      }
+      fa.ntiles = gr.ntiles;
+      fa.nseg = gr.nseg;
+      for (int s = 0; s < MAX_SEGS; s++) {
+        fa.seg_src[s] = gr.seg_src[s];
+        fa.seg_dst[s] = gr.seg_dst[s];
+        fa.seg_len[s] = gr.seg_len[s];
+      }
+      fa.remote = 0;
+    }
+    __syncthreads();
+    if (r.d >= 0)
+      for (int e = tid; e < pa.n_phi * 8; e += NTHREADS) phis[e] = fa.phi[e >> 3];
+    __syncthreads();
+    switch (r.fp * 2 + r.lane3) {
+      case FP_G0_DPOST * 2: persist_pass<FP_G0_DPOST, false>(fa, xb, phis, lane, warp); break;
+      case FP_G0_PRE * 2: persist_pass<FP_G0_PRE, false>(fa, xb, phis, lane, warp); break;
+      case FP_G0_PRE_D_POST * 2: persist_pass<FP_G0_PRE_D_POST, false>(fa, xb, phis, lane, warp); break;
+      case FP_GK_PRE * 2: persist_pass<FP_GK_PRE, false>(fa, xb, phis, lane, warp); break;
+      case FP_GK_PRE * 2 + 1: persist_pass<FP_GK_PRE, true>(fa, xb, phis, lane, warp); break;
+      case FP_GK_PRE_D_POST * 2: persist_pass<FP_GK_PRE_D_POST, false>(fa, xb, phis, lane, warp); break;
+      case FP_GK_PRE_D_POST * 2 + 1: persist_pass<FP_GK_PRE_D_POST, true>(fa, xb, phis, lane, warp); break;
+      default: __trap();
+    }
+    grid_sync(pa.bar, gridDim.x);
+  }
+}
+
 typedef void (*FastKernel)(const FastArgs);
 
 template <bool PF>
@@ -211,7 +327,56 @@ FastKernel pick(int prog, bool lane3) {
 
 }  // namespace
 
+// co-resident CTAs of the persistent kernel (0 on error)
+int persist_max_grid(int num_sms) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qaa_persist, NTHREADS, FAST_SMEM_BYTES) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return per_sm * num_sms;
+}
+
+cudaError_t launch_persist(const PersistLaunch& L, int grid, cudaStream_t st) {
+  PersistArgs a;
+  memset(&a, 0, sizeof a);
+  a.psi = L.psi;
+  a.E = L.E;
+  a.passes = L.passes;
+  a.npass = L.npass;
+  a.phi_all = L.phi_all;
+  a.n_phi = L.n_phi;
+  a.coef = L.coef;
+  a.bar = L.bar;
+  for (int g = 0; g < L.ngroups && g < 4; g++) {
+    for (int b = 0; b < TILE_BITS; b++) a.groups[g].phys[b] = L.groups[g].phys[b];
+    a.groups[g].rot_local = L.groups[g].rot_local;
+    a.groups[g].nseg = L.groups[g].nseg;
+    for (int s = 0; s < MAX_SEGS; s++) {
+      a.groups[g].seg_src[s] = L.groups[g].seg_src[s];
+      a.groups[g].seg_dst[s] = L.groups[g].seg_dst[s];
+      a.groups[g].seg_len[s] = L.groups[g].seg_len[s];
+    }
+    a.groups[g].ntiles = L.groups[g].ntiles;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = FAST_SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, qaa_persist, a);
+}
+
 cudaError_t pass_fast_setup() {
+  {
+    cudaError_t e = cudaFuncSetAttribute(qaa_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FAST_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+  }
   for (int p = 0; p < FP_COUNT; p++)
     for (int l = 0; l < 2; l++)
       for (int pf = 0; pf < 2; pf++) {

@@ -144,6 +144,29 @@ def test_pass_parity_small(q, ctx, orc, n, span, variant):
     assert_close(got, want)
 
 
+@pytest.mark.parametrize("n", [13, 14, 16, 18, 20, 21])
+@pytest.mark.parametrize("span", [2, 1, 0])
+def test_persist_parity(q, ctx, orc, n, span):
+    """The persistent evolve (QAA_OPT_PERSIST = 1, for 13 <= n <= 21 with the
+    automatic kernel choice): every pass of the plan in one cooperative launch
+    with grid barriers, against the oracle; and the per-pass launches (default)."""
+    ctx.set_option(q.OPT_PERSIST, 1)
+    cl = instance(n)
+    psi0 = cnf.random_state(n, 200 + n)
+    K = 7
+    sched = np.random.default_rng(n + 7).uniform(0, 1, K)
+    got, want, _ = run_both(q, ctx, orc, n, cl, 2.2, K, schedule=sched, psi0=psi0, span=span)
+    assert_close(got, want)
+    st = ctx.stats()
+    assert st["persist_launches"] == 1 and st["pass_launches"] == 1
+    ctx.set_option(q.OPT_PERSIST, 0)
+    ctx.reset_stats()
+    ctx.set_state(psi0)
+    ctx.evolve(2.2, K, sched)
+    assert ctx.stats()["persist_launches"] == 0
+    assert_close(ctx.state(), want)
+
+
 @pytest.mark.parametrize("c", [3, 4, 5])
 def test_pass_parity_row_bits(q, ctx, orc, c):
     n = 22
