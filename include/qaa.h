@@ -316,6 +316,7 @@ typedef struct {
   int64_t super_kernels_timed;
   int64_t tm_launches;       /* of super_launches: tensor-memory exchange variant (pass_tmem.cu) */
   int64_t persist_launches;  /* of pass_launches: persistent whole-evolve launches (QAA_OPT_PERSIST) */
+  int64_t pw_launches;       /* of super_launches: producer-warp variant (QAA_OPT_SUPER bit 14) */
   uint64_t tm_diag[8];       /* diagnostics (QAA_OPT_SUPER bit 10), summed over warps' lane 0 since the
                                 context's first such launch: [0] cycles in slot-landed waits, [1] items,
                                 [2] deferred group-k items, [3] cycles in deferred waits, [4] / [5]

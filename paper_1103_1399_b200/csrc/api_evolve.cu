@@ -128,6 +128,19 @@ static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_p
     e = launch_superpass_tm(&ctx->tmaps_sw[k], a, ctx->super_groups, bd, ctx->super_grid ? ctx->super_grid : ctx->num_sms,
                             ctx->stream);
     ctx->stats.tm_launches++;
+  } else if (ctx->super_pw) {
+    a.qab = (unsigned*)((char*)ctx->d_super + 16);
+    a.tm_flags = ctx->super_tm_flags;
+    if (a.tm_flags & 8) {
+      if (!ctx->d_tm_diag) {
+        CUDA_TRY(cudaMalloc(&ctx->d_tm_diag, 8 * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMemsetAsync(ctx->d_tm_diag, 0, 8 * sizeof(unsigned long long), ctx->stream));
+      }
+      a.dbg = ctx->d_tm_diag;
+    }
+    e = launch_superpass_pw(&ctx->tmaps[(size_t)k], a, (gk.rot_local >> 3) & 1, bd,
+                            ctx->super_grid ? ctx->super_grid : ctx->num_sms, ctx->stream);
+    ctx->stats.pw_launches++;
   } else {
     e = launch_superpass(&ctx->tmaps[(size_t)k], a, (gk.rot_local >> 3) & 1, ctx->super_groups, bd,
                          ctx->super_grid ? ctx->super_grid : ctx->num_sms, ctx->stream);

@@ -102,6 +102,7 @@ struct qaa_ctx {
   int super_tm = 0;             // tensor-memory exchanges in the L2-blocked step (pass_tmem.cu)
   int super_tm_flags = 0;
   int super_lag = 1;
+  int super_pw = 0;  // producer-warp L2-blocked step
   int super_grid = 0;  // 0: one CTA per SM
   int super_split = 0;
   int persist = 0;  // persistent evolve for 13 <= L <= 21 (opt-in: measured slower)

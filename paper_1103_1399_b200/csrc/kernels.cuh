@@ -142,6 +142,7 @@ struct SuperArgs {
   // doneB[c - lag - 1] == 2^tpc_bits (all B(c - lag - 1) issued: bounds the L2 live set)
   int split_a;
   unsigned* doneB;     // [nchunks] group-k tiles issued per chunk (zeroed before launch)
+  unsigned* qab;       // producer-warp variant: [0] next group-0 tile, [1] next group-k tile (zeroed)
   int done_shift;      // done[c] counts 2^done_shift arrivals per tile (3: one per warp, pass_tmem.cu)
   int tm_flags;        // pass_tmem.cu A/B switches: 1 = group-0 slot released at the tile's end,
                        // 2 = publish right after the stores, 4 = spin (no suspend hint) in waits,
@@ -151,6 +152,10 @@ struct SuperArgs {
 };
 cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, int ngroups, bool bd, int grid,
                              cudaStream_t st);
+// the same step with a producer warp (pass_tma.cu qaa_superpass_pw): two consumer
+// groups + one warp that claims tiles dynamically and issues every load
+cudaError_t launch_superpass_pw(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, bool bd, int grid,
+                                cudaStream_t st);
 cudaError_t launch_pass_tma(const CUtensorMap* map, const TmaArgs& a, int prog, bool lane3, int ngroups, int grid,
                             cudaStream_t st);
 // gather a group's energy layout: Eg[T*4096 + pack(l)] = E[tbase(T) + off(l)], pack =

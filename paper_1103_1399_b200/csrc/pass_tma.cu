@@ -399,6 +399,178 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
   if (!BD && a.remote) __threadfence_system();
 }
 
+
+// ============================================================================
+// L2-blocked step with a PRODUCER WARP (QAA_OPT_SUPER bit 14): warp 16 alone
+// decides what each slot holds and issues its loads; the 16 consumer warps only
+// wait for landed tiles, so a chunk dependency never stalls them (with the
+// consumer-issued schedule above, 70-80 % of the group-k tiles were found
+// deferred and their groups waited on the chunk, then on the load).
+// Each CTA owns the group-0 tiles (A) and group-k tiles (B) b, b + grid, ... of
+// a launch (chunk order); the producer takes its next B tile when that chunk is
+// complete, else its next A tile as long as A stays within one chunk of B (two
+// chunks live in L2), else the B tile, waiting for its chunk itself. A filled
+// slot never waits on anything but its own load, and every A tile is issued
+// before any wait on its chunk, so every chunk completes: no deadlock.
+// ============================================================================
+constexpr int PW_THREADS = 2 * NTHREADS + 32;
+
+template <bool BD>
+__device__ __forceinline__ void pw_issue_b(const CUtensorMap* kmap, const SuperArgs& a, unsigned t, int s,
+                                           uint64_t* fb, double2* slots, uint8_t* eslots, SlotMeta* meta,
+                                           uint64_t pol) {
+  const uint32_t c = t >> a.tpc_bits, i = t & ((1u << a.tpc_bits) - 1);
+  const uint32_t T = pdep32(i, a.k_imask) | pdep32(c, a.k_cmask);
+  const unsigned target = 1u << a.tpc_bits;
+  const long long t0 = (a.tm_flags & 8) ? clock64() : 0;
+  for (uint32_t it = 0; ld_acquire(&a.done[c]) < target; it++) {
+    __nanosleep(64);
+    if (it > (1u << 28)) __trap();
+  }
+  if (a.tm_flags & 8) atomicAdd(&a.dbg[2], (unsigned long long)(clock64() - t0));
+  fence_async_global();  // generic-proxy stores of chunk c -> this async-proxy read
+  meta[s] = SlotMeta{SK_B, (int)c, T, 0};
+  load_gk<BD>(kmap, a, T, slots + (size_t)s * FAST_XBUF, eslots + (size_t)s * TILE, fb, pol);
+}
+__device__ __forceinline__ void pw_issue_a(const SuperArgs& a, unsigned t, int s, uint64_t* fb, double2* slots,
+                                           SlotMeta* meta, uint64_t pol) {
+  const uint32_t c = t >> a.tpc_bits, i = t & ((1u << a.tpc_bits) - 1);
+  const uint32_t T = pdep32(i, a.z_imask) | pdep32(c, a.z_cmask);
+  meta[s] = SlotMeta{SK_A, (int)c, T, 0};
+  mbar_expect_tx(fb, TILE * 16u);
+  bulk_g2s_hint(slots + (size_t)s * FAST_XBUF, a.g0.psi + tbase(a.g0, T), TILE * 16u, fb, pol);
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <bool BD>
+__device__ void pw_producer(const CUtensorMap* kmap, const SuperArgs& a, double2* slots, uint8_t* eslots,
+                            uint64_t* full, uint64_t* empty, SlotMeta* meta, uint64_t pol) {
+  // this CTA's own tiles of each kind, round robin, chunk order; the choice
+  // between them is made BEFORE waiting for the slot, so the global readiness
+  // load overlaps the consumers' work on it
+  const unsigned n = (unsigned)a.nchunks << a.tpc_bits;
+  const unsigned target = 1u << a.tpc_bits;
+  unsigned tA = blockIdx.x, tB = blockIdx.x;
+  int ends = 0;
+  for (int J = 0; ends < 2; J++) {
+    const int s = J % TMA_SLOTS;
+    int kind = SK_END;
+    if (tB < n) {
+      const unsigned cb = tB >> a.tpc_bits;
+      if (ld_acquire(&a.done[cb]) >= target) kind = SK_B;
+      else if (tA < n && (tA >> a.tpc_bits) <= cb + 1) kind = SK_A;
+      else kind = SK_B;  // wait for the chunk at issue time
+      if ((a.tm_flags & 8) && kind == SK_B && ld_acquire(&a.done[cb]) < target) atomicAdd(&a.dbg[3], 1ull);
+    } else if (tA < n) {
+      kind = SK_A;
+    }
+    if (J >= TMA_SLOTS) {
+      const long long t0 = (a.tm_flags & 8) ? clock64() : 0;
+      mbar_wait_sleep(&empty[s], (uint32_t)(((J - TMA_SLOTS) / TMA_SLOTS) & 1));
+      if (a.tm_flags & 8) atomicAdd(&a.dbg[4], (unsigned long long)(clock64() - t0));
+      fence_async_shared();  // the consumers' generic reads of the slot -> the async-proxy refill
+    }
+    uint64_t* fb = &full[2 * s + (J & 1)];
+    if (kind == SK_B) {
+      pw_issue_b<BD>(kmap, a, tB, s, fb, slots, eslots, meta, pol);
+      tB += gridDim.x;
+    } else if (kind == SK_A) {
+      pw_issue_a(a, tA, s, fb, slots, meta, pol);
+      tA += gridDim.x;
+    } else {
+      meta[s] = SlotMeta{SK_END, 0, 0, 0};
+      mbar_arrive_notx(fb);
+      ends++;
+    }
+  }
+}
+
+template <bool LANE3, bool BD>
+__global__ void __launch_bounds__(PW_THREADS, 1) qaa_superpass_pw(const __grid_constant__ CUtensorMap kmap,
+                                                                 const SuperArgs a) {
+  constexpr int NG = 2;
+  constexpr int BPROG = BD ? FP_GK_PRE_D_POST : FP_GK_PRE;
+  extern __shared__ __align__(128) unsigned char sm[];
+  double2* slots = reinterpret_cast<double2*>(sm);
+  uint8_t* eslots = sm + TMA_SLOTS * SLOT_BYTES;
+  double2* phis = reinterpret_cast<double2*>(eslots + TMA_SLOTS * TILE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(phis + TMA_MAX_PHI * PHI_COPIES);
+  SlotMeta* meta = reinterpret_cast<SlotMeta*>(full + NG * TMA_SLOTS + NG);
+  uint64_t* empty = slot_consumed(sm);  // per slot: its 8 consumer warps are done with it
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t pol_dead = a.hints ? policy_evict_first() : policy_evict_normal();
+  const uint64_t pol_keep = a.hints == 2 ? policy_evict_last() : policy_evict_normal();
+  if (tid == 0) {
+    for (int s = 0; s < NG * TMA_SLOTS; s++) mbar_init(&full[s], 1);
+    for (int s = 0; s < TMA_SLOTS; s++) mbar_init(&empty[s], NTHREADS / 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (BD)
+    for (int e = tid; e < a.gk.n_phi * PHI_COPIES; e += PW_THREADS) phis[e] = a.gk.phi[e / PHI_COPIES];
+  __syncthreads();
+  if (warp == 2 * (NTHREADS / 32)) {
+    if (lane == 0) pw_producer<BD>(&kmap, a, slots, eslots, full, empty, meta, pol_dead);
+    return;
+  }
+  const int g = warp >> 3, lw = warp & 7, gtid = tid & (NTHREADS - 1);
+  double2 v[RPT];
+  for (int J = g;; J += NG) {
+    const int s = J % TMA_SLOTS;
+    const long long t0 = (a.tm_flags & 8) ? clock64() : 0;
+    mbar_wait_sleep(&full[NG * s + g], (uint32_t)((J / period<NG>()) & 1));
+    if ((a.tm_flags & 8) && lane == 0) {
+      atomicAdd(&a.dbg[0], (unsigned long long)(clock64() - t0));
+      atomicAdd(&a.dbg[1], 1ull);
+    }
+    const SlotMeta m = meta[s];
+    if (m.kind == SK_END) break;
+    double2* xb = slots + (size_t)s * FAST_XBUF;
+    uint8_t* es = eslots + (size_t)s * TILE;
+    const bool isb = m.kind != SK_A;
+    if (isb) {
+      load_landed<Info<BPROG>::load_pat>(v, xb, lane, lw);
+      program<BPROG, LANE3>(a.gk, v, xb, es, phis, lane, lw, g);
+    } else {
+      load_landed<Info<FP_G0_PRE>::load_pat>(v, xb, lane, lw);
+      program<FP_G0_PRE, false>(a.g0, v, xb, nullptr, phis, lane, lw, g);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_notx(&empty[s]);
+    if (isb) {
+      const Off psk = make_off<Info<BPROG>::store_pat>(a.gk, lane, lw);
+      const int64_t tb = tbase(a.gk, m.T);
+      if (!BD && a.remote) {
+        const int64_t j = tb >> a.gshift;
+        double2* dst = a.peers[j] + (tb - (j << a.gshift) + ((int64_t)a.rank << a.gshift));
+#pragma unroll
+        for (int r = 0; r < RPT; r++) dst[roff(psk, r)] = v[r];
+      } else {
+        double2* dst = a.gk.psi + tb;
+#pragma unroll
+        for (int r = 0; r < RPT; r++) st_hint(dst + roff(psk, r), v[r], pol_dead);
+      }
+    } else {
+      const Off ps0 = make_off<Info<FP_G0_PRE>::store_pat>(a.g0, lane, lw);
+      double2* dst = a.g0.psi + tbase(a.g0, m.T);
+#pragma unroll
+      for (int r = 0; r < RPT; r++) st_hint(dst + roff(ps0, r), v[r], pol_keep);
+      group_bar(g);
+      if (gtid == 0) red_release_add(&a.done[m.c], 1u);
+    }
+  }
+  if (!BD && a.remote) __threadfence_system();
+}
+
+typedef void (*PwKernel)(const CUtensorMap, const SuperArgs);
+PwKernel pick_pw(bool lane3, bool bd) {
+  return bd ? (lane3 ? qaa_superpass_pw<true, true> : qaa_superpass_pw<false, true>)
+            : (lane3 ? qaa_superpass_pw<true, false> : qaa_superpass_pw<false, false>);
+}
+
 typedef void (*SuperKernel)(const CUtensorMap, const SuperArgs);
 template <bool BD>
 SuperKernel pick_super_bd(bool lane3, int ng) {
@@ -447,7 +619,28 @@ cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool l
   return cudaLaunchKernelEx(&cfg, k, *kmap, a);
 }
 
+cudaError_t launch_superpass_pw(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, bool bd, int grid,
+                                cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)PW_THREADS);
+  cfg.dynamicSmemBytes = TMA_SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, pick_pw(lane3, bd), *kmap, a);
+}
+
 cudaError_t pass_tma_setup() {
+  for (int l = 0; l < 2; l++)
+    for (int bd = 0; bd < 2; bd++) {
+      cudaError_t e = cudaFuncSetAttribute(pick_pw(l, bd), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)TMA_SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+    }
   for (int l = 0; l < 2; l++)
     for (int ng = 1; ng <= 2; ng++)
       for (int bd = 0; bd < 2; bd++) {

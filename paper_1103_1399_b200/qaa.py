@@ -115,7 +115,7 @@ class qaa_stats(ctypes.Structure):
                 ("tile_bits", ctypes.c_int), ("row_bits", ctypes.c_int),
                 ("kernel_launches_total", ctypes.c_int64), ("super_launches", ctypes.c_int64),
                 ("super_kernel_ms", ctypes.c_double), ("super_kernels_timed", ctypes.c_int64),
-                ("tm_launches", ctypes.c_int64), ("persist_launches", ctypes.c_int64),
+                ("tm_launches", ctypes.c_int64), ("persist_launches", ctypes.c_int64), ("pw_launches", ctypes.c_int64),
                 ("tm_diag", ctypes.c_uint64 * 8)]
 
     def as_dict(self):

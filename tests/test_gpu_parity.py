@@ -384,13 +384,14 @@ def test_torch_owned_state(q, orc):
 
 
 @pytest.mark.parametrize("n", [22, 23, 24, 26])
-@pytest.mark.parametrize("sup", [17, 19, 49, 81, 83, 0])
+@pytest.mark.parametrize("sup", [17, 19, 49, 81, 83, 16401, 0])
 @pytest.mark.parametrize("K", [1, 2, 5])
 def test_super_pass_parity(q, ctx, orc, n, sup, K):
     """L2-blocked Trotter steps (QAA_OPT_SUPER bit 0; bit 1 = one consumer group;
     bit 4 = also below 256 chunks, i.e. at these test sizes; bit 5 = dynamic work
     queue instead of the static round robin; bit 6 = tensor-memory exchanges instead
-    of shared memory) against the oracle; 0 = the two-pass plan."""
+    of shared memory; bit 14 = the producer-warp variant) against the oracle; 0 = the
+    two-pass plan."""
     ctx.set_option(q.OPT_SUPER, sup)
     cl = instance(n)
     psi0 = cnf.random_state(n, 31 + n)
@@ -402,6 +403,7 @@ def test_super_pass_parity(q, ctx, orc, n, sup, K):
         assert st["pass_launches"] == K + 1  # first pass, K-1 fused pairs, the fused closing pair
         assert st["super_launches"] == K
         assert st["tm_launches"] == (K if sup & 64 else 0)
+        assert st["pw_launches"] == (K if (sup & 16384) and not (sup & 64) else 0)
 
 
 def _full_state(q, n, cl, sup, K, sched, T=1.7, against=None):
@@ -432,8 +434,8 @@ def _full_state(q, n, cl, sup, K, sched, T=1.7, against=None):
     return out, st
 
 
-@pytest.mark.parametrize("n", [22, 24, 27, 30, 31])
-def test_super_bitwise_equals_two_pass(q, n):
+@pytest.mark.parametrize("n,sup", [(22, 17), (24, 17), (27, 17), (30, 17), (31, 17), (24, 16401), (30, 16401)])
+def test_super_bitwise_equals_two_pass(q, n, sup):
     """The (default, shared-memory) L2-blocked step runs the very per-tile programs of the
     two-pass plan, only fused into one launch over L2-resident chunks (deferred
     loads, cross-CTA release/acquire): at full size the whole state must be
@@ -443,10 +445,12 @@ def test_super_bitwise_equals_two_pass(q, n):
     cl = instance(n)
     K = 7
     sched = np.random.default_rng(n).uniform(0, 1, K)
-    a, st = _full_state(q, n, cl, 17, K, sched)
+    a, st = _full_state(q, n, cl, sup, K, sched)
     # three tile groups: K - 1 fused [G0][Gk D] pairs + the fused closing pair;
-    # four (n = 31): one fused plain pair [G0][Gb] per step
+    # four (n = 31): one fused plain pair [G0][Gb] per step. sup = 16401: the
+    # producer-warp variant (same per-tile programs, dynamic choice of tiles)
     assert st["super_launches"] == K and st["tm_launches"] == 0
+    assert st["pw_launches"] == (K if sup & 16384 else 0)
     (err, eq), st0 = _full_state(q, n, cl, 0, K, sched, against=a)
     assert st0["super_launches"] == 0
     assert eq, err

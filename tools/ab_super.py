@@ -47,3 +47,16 @@ if any(s & 1024 for s in sups):
               f"landed-wait cyc {d[0] / nw / K:.3g}, deferred-wait cyc {d[3] / nw / K:.3g}, "
               f"g0 prog cyc {d[4] / nw / K:.3g}, gk prog cyc {d[5] / nw / K:.3g}, "
               f"done-spin cyc (group leader) {d[6] / (148 * 2) / K:.3g}, issued early at arrival {d[7] / nw / K:.1f}")
+# producer-warp diagnostics (bit 14 + bit 10)
+if any((s & 16384) and (s & 1024) for s in sups):
+    with q.Context(0) as c:
+        c.load_instance(n, cl)
+        c.init_uniform()
+        s = [x for x in sups if (x & 16384) and (x & 1024)][0]
+        c.set_option(q.OPT_SUPER, s)
+        c.evolve(200.0 * K / 10000, K)
+        d = c.stats()["tm_diag"]
+        nw = 148 * 16
+        print(f"pw diag per launch (K={K}): consumer items/warp {d[1] / nw / K:.0f}, consumer full-wait cyc/warp "
+              f"{d[0] / nw / K:.3g}, producer chunk-wait cyc/CTA {d[2] / 148 / K:.3g}, B-not-ready decisions/CTA "
+              f"{d[3] / 148 / K:.1f}, producer empty-wait cyc/CTA {d[4] / 148 / K:.3g}")
