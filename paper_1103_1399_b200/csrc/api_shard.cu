@@ -43,19 +43,29 @@ qaa_status setup_shard_buffers(qaa_ctx* ctx, size_t bytes) {
     ctx->bufs[b] = nullptr;
   }
   ctx->buf_cap = 0;
-  for (int b = 0; b < 2; b++) {
-    cudaError_t e = cudaMalloc(&ctx->bufs[b], bytes);
-    if (e != cudaSuccess) {
+  // Every rank reaches the allgather below even when its allocation fails: the
+  // ranks agree on success (an ok word in the gathered record) and fail together
+  // with CAP instead of leaving the others blocked in a collective.
+  struct Rec {
+    int ok;
+    int pad;
+    cudaIpcMemHandle_t h[3];
+  } mine;
+  memset(&mine, 0, sizeof mine);
+  mine.ok = 1;
+  for (int b = 0; b < 2 && mine.ok; b++)
+    if (cudaMalloc(&ctx->bufs[b], bytes) != cudaSuccess) {
       cudaGetLastError();
-      return fail(ctx, QAA_E_CAP, "shard buffers of 2 x %zu bytes do not fit on the device", bytes);
+      ctx->bufs[b] = nullptr;
+      mine.ok = 0;
     }
-  }
-  ctx->buf_cap = bytes;
   // the device-side phase barrier's arrival counter (zeroed before any peer can
   // signal: peers first pass the host barrier below)
-  if (!ctx->sync_buf) {
-    CUDA_TRY(cudaMalloc(&ctx->sync_buf, 256));
-    CUDA_TRY(cudaMemset(ctx->sync_buf, 0, 256));
+  if (mine.ok && !ctx->sync_buf) {
+    if (cudaMalloc(&ctx->sync_buf, 256) != cudaSuccess || cudaMemset(ctx->sync_buf, 0, 256) != cudaSuccess) {
+      cudaGetLastError();
+      mine.ok = 0;
+    }
     ctx->sync_epoch = 0;
     for (int r = 0; r < 8; r++) {
       if (ctx->peer_sync_open[r]) cudaIpcCloseMemHandle(ctx->peer_sync[r]);
@@ -63,12 +73,27 @@ qaa_status setup_shard_buffers(qaa_ctx* ctx, size_t bytes) {
       ctx->peer_sync[r] = nullptr;
     }
   }
-  cudaIpcMemHandle_t mine[3];
-  for (int b = 0; b < 2; b++) CUDA_TRY(cudaIpcGetMemHandle(&mine[b], ctx->bufs[b]));
-  CUDA_TRY(cudaIpcGetMemHandle(&mine[2], ctx->sync_buf));
-  std::vector<cudaIpcMemHandle_t> all(3 * (size_t)ctx->world);
-  qaa_status st = comm_allgather(ctx, mine, all.data(), sizeof mine);
+  if (mine.ok) {
+    for (int b = 0; b < 2; b++)
+      if (cudaIpcGetMemHandle(&mine.h[b], ctx->bufs[b]) != cudaSuccess) mine.ok = 0;
+    if (cudaIpcGetMemHandle(&mine.h[2], ctx->sync_buf) != cudaSuccess) mine.ok = 0;
+    cudaGetLastError();
+  }
+  std::vector<Rec> recs((size_t)ctx->world);
+  qaa_status st = comm_allgather(ctx, &mine, recs.data(), sizeof mine);
   if (st) return st;
+  for (int r = 0; r < ctx->world; r++)
+    if (!recs[(size_t)r].ok) {
+      for (int b = 0; b < 2; b++) {
+        if (ctx->bufs[b]) cudaFree(ctx->bufs[b]);
+        ctx->bufs[b] = nullptr;
+      }
+      return fail(ctx, QAA_E_CAP, "shard buffers of 2 x %zu bytes do not fit on the device of rank %d", bytes, r);
+    }
+  ctx->buf_cap = bytes;
+  std::vector<cudaIpcMemHandle_t> all(3 * (size_t)ctx->world);
+  for (int r = 0; r < ctx->world; r++)
+    for (int b = 0; b < 3; b++) all[3 * (size_t)r + b] = recs[(size_t)r].h[b];
   for (int r = 0; r < ctx->world; r++) {
     for (int b = 0; b < 2; b++) {
       if (r == ctx->rank) {
