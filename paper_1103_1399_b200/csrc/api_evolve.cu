@@ -110,6 +110,10 @@ static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_p
   // phi == nullptr: the plain pair of a four-group plan (kernel variant without D)
   const bool bd = phi != nullptr;
   cudaError_t e;
+  if (ctx->super_tm && !ctx->tm_built) {
+    qaa_status st = build_tm(ctx);
+    if (st) return st;
+  }
   if (ctx->super_tm && ctx->tm_ok[k] && (!bd || ctx->Eg_tm[k])) {
     if (bd) a.gk.Eg = ctx->Eg_tm[k];
     a.done_shift = 3;  // per-warp publish

@@ -109,7 +109,8 @@ struct qaa_ctx {
   void* d_persist = nullptr;  // its barrier words and pass records
   size_t d_persist_cap = 0;  // split roles: CTAs running group-0 tiles only (0 = interleaved sequence)
   unsigned long long* d_tm_diag = nullptr;  // pass_tmem.cu diagnostics counters (QAA_OPT_SUPER bit 10)
-  int tm_ok[4] = {0, 0, 0, 0};  // per paired group: swizzled map (+ K3-packed energies) ready
+  bool tm_built = false;        // build_tm ran for the current geometry (lazily, on first use)
+  int tm_ok[4] = {0, 0, 0, 0};  // per paired group: swizzled map (+ K4-packed energies) ready
   CUtensorMap tmaps_sw[4];
   TmaArgs tm_geo[4];             // its tensor-map dims (ndims, dim_seg) for the load coordinates
   uint8_t* Eg_tm[4] = {nullptr, nullptr, nullptr, nullptr};

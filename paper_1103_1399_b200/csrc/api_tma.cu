@@ -244,8 +244,9 @@ qaa_status build_tma(qaa_ctx* ctx) {
       if (ctx->tma_ok[(size_t)k] &&
           make_super_args(ctx, k, ctx->tma_static[0], ctx->tma_static[(size_t)k], &ctx->super_static[k]))
         ctx->super_ok[k] = true;
-  qaa_status st = build_tm(ctx);
-  if (st) return st;
+  // the tensor-memory variant's tables are built on its first use (build_tm)
+  ctx->tm_built = false;
+  for (int k = 0; k < 4; k++) ctx->tm_ok[k] = 0;
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return QAA_OK;
 }
@@ -257,6 +258,7 @@ qaa_status build_tma(qaa_ctx* ctx) {
 // 128-byte-row bits (row_bits = 3; unrotated padding bits above them are
 // fine). Missing pieces leave tm_ok[k] = 0 (legacy kernel).
 qaa_status build_tm(qaa_ctx* ctx) {
+  ctx->tm_built = true;
   for (int k = 0; k < 4; k++) ctx->tm_ok[k] = 0;
   const int P = (int)ctx->geom.groups.size();
   const size_t N = (size_t)1 << ctx->L;
