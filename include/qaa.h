@@ -257,8 +257,14 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        (pass_tmem.cu: register-pattern changes through tcgen05.st/ld
  *                        instead of shared memory; measured 3-10 % slower);
  *                        bits 7-10 and 13: its A/B switches and diagnostics counters
- *                        (SuperArgs.tm_flags); bits 11-12: chunk lag - 1 (default lag 1:
- *                        two chunks live in L2; 2-3 measured slower). Values 0..16383.
+ *                        (SuperArgs.tm_flags; with the default kernel bit 7 = publish a
+ *                        group-0 tile after the next landed read, bit 8 = right after its
+ *                        stores); bits 11-12: chunk lag - 1 (default lag 1: two chunks
+ *                        live in L2; 2-3 measured slower); bit 14: producer-warp variant;
+ *                        bit 15: the round-1 synchronisation (a group barrier before every
+ *                        exchange write and before each group-0 tile's publish) instead of
+ *                        the default split-phase write-after-read mbarriers and deferred
+ *                        per-warp publish (measured 2-5 % slower). Values 0..65535.
  *  QAA_OPT_SUPER_GRID    CTAs of an L2-blocked launch (0 = one per SM, default; else 1..SMs):
  *                        a tuning hook -- a chunk's 2^tpc tiles are dealt round robin, so a
  *                        grid dividing them evenly balances the per-chunk work.
@@ -276,6 +282,16 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        passes) instead of one launch per pass. 0 (default): per-pass
  *                        launches -- measured faster (7.4 vs 8.9 us/step at n = 13..18:
  *                        a pass is bound by one CTA's tile program, not by the launch).
+ *  QAA_OPT_CLUSTER       1 (default): for 13 <= n <= 16 on one GPU with the automatic kernel
+ *                        choice, all K steps run as ONE launch with the state resident in the
+ *                        registers of a thread-block cluster of 2^(n-12) CTAs (cluster bits
+ *                        swapped with local bits over DSMEM once per step); 0: per-pass
+ *                        kernels through HBM/L2.
+ *  QAA_OPT_DIAG          timing diagnostics ONLY (results are wrong by design): the
+ *                        L2-blocked step at the bench configuration with work removed --
+ *                        1 = no rotations, 2 = no shared-memory exchanges, 4 = no D,
+ *                        8 = group-k tiles ignore the chunk dependency; sums 3, 7, 15.
+ *                        Other configurations return QAA_E_CUDA at evolve. Default 0.
  *  QAA_OPT_ENERGY_W64    test hook: 1 = the 64-bit energy-table kernel even when every
  *                        assignment fits 32 bits (default 0: 32-bit kernel for n <= 32).
  *  QAA_OPT_ORDER         1 (default) = first-order Lie-Trotter, D then X (R7);
@@ -295,7 +311,9 @@ enum {
   QAA_OPT_SUPER_GRID = 10,
   QAA_OPT_SUPER_SPLIT = 11,
   QAA_OPT_SHARD_SYNC = 12,
-  QAA_OPT_PERSIST = 13
+  QAA_OPT_PERSIST = 13,
+  QAA_OPT_DIAG = 14,
+  QAA_OPT_CLUSTER = 16
 };
 qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value);
 
@@ -321,6 +339,7 @@ typedef struct {
                                 context's first such launch: [0] cycles in slot-landed waits, [1] items,
                                 [2] deferred group-k items, [3] cycles in deferred waits, [4] / [5]
                                 cycles in group-0 / group-k tile programs; zeros otherwise */
+  int64_t cluster_launches;  /* of pass_launches: cluster-resident whole-evolve launches (QAA_OPT_CLUSTER) */
 } qaa_stats;
 qaa_status qaa_get_stats(qaa_ctx* ctx, qaa_stats* out);
 qaa_status qaa_reset_stats(qaa_ctx* ctx);

@@ -161,7 +161,7 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       ctx->order = (int)value;
       return QAA_OK;
     case QAA_OPT_SUPER:
-      if (value < 0 || value > 32767) return fail(ctx, QAA_E_USAGE, "super option must be in 0..32767");
+      if (value < 0 || value > 65535) return fail(ctx, QAA_E_USAGE, "super option must be in 0..65535");
       // bit 0: L2-blocked Trotter steps; bit 1: one consumer group per CTA (default two);
       // bits 2-3: L2 eviction hints (0 = evict-last for the group-0 output that the
       // group-k sub-pass reads back + evict-first for dead data; 1 = none; 2 = evict-first only)
@@ -173,7 +173,16 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       ctx->super_tm_flags = (int)((value >> 7) & 15) | (int)((value >> 9) & 16);  // bits 7-10, 13: pass_tmem.cu switches
       ctx->super_lag = 1 + (int)((value >> 11) & 3);    // bits 11-12: chunk lag - 1 (SuperArgs.lag)
       ctx->super_pw = (value >> 14) & 1;                // bit 14: producer-warp variant (qaa_superpass_pw)
+      ctx->super_v2 = ((value >> 15) & 1) ? 0 : 1;      // bit 15: group barriers instead of split-phase WAR + deferred publish
       ctx->super_hints = ((value >> 2) & 3) == 1 ? 0 : (((value >> 2) & 3) == 2 ? 1 : 2);
+      return QAA_OK;
+    case QAA_OPT_CLUSTER:
+      if (value < 0 || value > 1) return fail(ctx, QAA_E_USAGE, "cluster must be 0 or 1");
+      ctx->cluster_evolve = (int)value;
+      return QAA_OK;
+    case QAA_OPT_DIAG:
+      if (value < 0 || value > 15) return fail(ctx, QAA_E_USAGE, "diag must be in 0..15");
+      ctx->diag = (int)value;
       return QAA_OK;
     case QAA_OPT_TMA_GROUPS:
       if (value < 0 || value > 2) return fail(ctx, QAA_E_USAGE, "tma groups must be 0 (auto), 1 or 2");

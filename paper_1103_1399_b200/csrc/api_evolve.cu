@@ -106,6 +106,10 @@ static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_p
   a.done = (unsigned*)((char*)ctx->d_super + 256);
   a.doneB = a.done + a.nchunks;
   a.split_a = ctx->super_split;
+  a.v2 = ctx->super_v2 && !ctx->super_split;
+  a.tm_flags = ctx->super_tm_flags;  // v2: 1 = publish after the next landed read, 2 = right after the stores
+  a.diag = ctx->diag;
+  a.done_shift = a.v2 ? 3 : 0;
   CUDA_TRY(cudaMemsetAsync(ctx->d_super, 0, 256 + 2 * (size_t)a.nchunks * sizeof(unsigned), ctx->stream));
   // phi == nullptr: the plain pair of a four-group plan (kernel variant without D)
   const bool bd = phi != nullptr;
@@ -334,6 +338,35 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
       ctx->ev_used = ev + 1;
     }
     ctx->stats.pass_launches++;
+    ctx->stats.kernel_launches_total++;
+    return QAA_OK;
+  }
+  if (ctx->cluster_evolve && ctx->L >= 13 && ctx->L <= 16 && ctx->kernel_mode == 2) {
+    // the whole evolution in one launch, state in one cluster's registers
+    ClusterArgs ca;
+    memset(&ca, 0, sizeof ca);
+    ca.psi = ctx->state;
+    ca.E = ctx->E;
+    ca.L = ctx->L;
+    ca.K = K;
+    ca.phi_all = dphi;
+    ca.n_phi = n_phi;
+    ca.coef = dcoef;
+    ca.form = dform;
+    ca.final_d = ctx->order == 2 ? 1 : 0;
+    size_t ev = ctx->ev_used;
+    if (ctx->profile) {
+      qaa_status st = ensure_events(ctx, ev + 1);
+      if (st) return st;
+      CUDA_TRY(cudaEventRecord(ctx->ev_pool[ev].first, ctx->stream));
+    }
+    CUDA_TRY(launch_cluster_evolve(ca, 1, ctx->stream));
+    if (ctx->profile) {
+      CUDA_TRY(cudaEventRecord(ctx->ev_pool[ev].second, ctx->stream));
+      ctx->ev_used = ev + 1;
+    }
+    ctx->stats.pass_launches++;
+    ctx->stats.cluster_launches++;
     ctx->stats.kernel_launches_total++;
     return QAA_OK;
   }

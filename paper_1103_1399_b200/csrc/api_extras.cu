@@ -1,4 +1,7 @@
 // api_extras.cu -- NEXT rows: spectrum (F3), energy-table timing (F2), batched sweep (F1), plan description.
+#include <algorithm>
+#include <vector>
+
 #include "api_internal.hpp"
 
 extern "C" {
@@ -104,10 +107,16 @@ qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, 
   int32_t* hform = (int32_t*)(hcoef + rows);
   int64_t* hK = (int64_t*)(((uintptr_t)(hform + rows) + 15) & ~(uintptr_t)15);
   int64_t* hoff = hK + nrep;
+  // replicas are launched longest first (cluster slots free up in order, the
+  // longest replica never waits behind short ones); results are mapped back below
+  std::vector<int> ord((size_t)nrep);
+  for (int r = 0; r < nrep; r++) ord[(size_t)r] = r;
+  std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return K[x] > K[y]; });
   int64_t row = 0;
-  for (int r = 0; r < nrep; r++) {
-    hK[r] = K[r];
-    hoff[r] = row;
+  for (int i = 0; i < nrep; i++) {
+    const int r = ord[(size_t)i];
+    hK[i] = K[r];
+    hoff[i] = row;
     const double dt = T[r] / (double)K[r];
     for (int64_t k = 0; k < K[r]; k++) {
       const double s = ((double)k + 0.5) / (double)K[r];
@@ -145,13 +154,37 @@ qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, 
   a.final_d = ctx->order == 2 ? 1 : 0;
   double* dout = (double*)(db + ((used + 15) & ~(size_t)15));
   a.out = dout;
-  if (ctx->L >= 10)  // register phases, one CTA (n <= 13) or one cluster (n = 14..16) per replica
+  if (ctx->cluster_evolve && ctx->L >= 13 && ctx->L <= 16) {
+    // one register-resident cluster of 2^(n-12) CTAs per replica (cluster_evolve.cu)
+    ClusterArgs ca;
+    memset(&ca, 0, sizeof ca);
+    ca.E = ctx->E;
+    ca.L = ctx->L;
+    ca.amp0 = a.amp0;
+    ca.Krep = a.K;
+    ca.row_off = a.row_off;
+    ca.phi_all = a.phi_all;
+    ca.n_phi = n_phi;
+    ca.coef = a.coef;
+    ca.form = a.form;
+    ca.final_d = a.final_d;
+    ca.out = dout;
+    CUDA_TRY(launch_cluster_evolve(ca, nrep, ctx->stream));
+    ctx->stats.cluster_launches++;
+  } else if (ctx->L >= 10)  // register phases, one CTA (n <= 13) or one cluster (n = 14..16) per replica
     CUDA_TRY(launch_sweep_cluster(a, nrep, ctx->stream));
   else
     CUDA_TRY(launch_sweep(a, nrep, ctx->stream));
   ctx->stats.kernel_launches_total++;
-  CUDA_TRY(cudaMemcpyAsync(out, dout, (size_t)nrep * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  double* hres = (double*)ctx->h_out;  // pinned; reused when nrep fits
+  std::vector<double> tmp;
+  if (nrep > 64) {
+    tmp.resize((size_t)nrep);
+    hres = tmp.data();
+  }
+  CUDA_TRY(cudaMemcpyAsync(hres, dout, (size_t)nrep * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < nrep; i++) out[ord[(size_t)i]] = hres[i];
   return QAA_OK;
 }
 

@@ -103,6 +103,9 @@ struct qaa_ctx {
   int super_tm_flags = 0;
   int super_lag = 1;
   int super_pw = 0;  // producer-warp L2-blocked step
+  int diag = 0;      // QAA_OPT_DIAG (timing diagnostics only)
+  int cluster_evolve = 1;  // QAA_OPT_CLUSTER: 13 <= L <= 16 in one cluster-resident launch
+  int super_v2 = 1;  // split-phase WAR guards + deferred publish (QAA_OPT_SUPER bit 15 clears it)
   int super_grid = 0;  // 0: one CTA per SM
   int super_split = 0;
   int persist = 0;  // persistent evolve for 13 <= L <= 21 (opt-in: measured slower)

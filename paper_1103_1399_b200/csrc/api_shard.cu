@@ -230,6 +230,8 @@ qaa_status evolve_sharded(qaa_ctx* ctx, int64_t K, const std::vector<StepCoef>& 
         }
         a.queue = ctx->super_dynamic ? (unsigned long long*)ctx->d_super : nullptr;
         a.done = (unsigned*)((char*)ctx->d_super + 256);
+        a.v2 = ctx->super_v2;
+        a.done_shift = ctx->super_v2 ? 3 : 0;
         CUDA_TRY(cudaMemsetAsync(ctx->d_super, 0, need, ctx->stream));
         if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
         CUDA_TRY(launch_superpass(&ctx->shard_kmap[ctx->cur], a, (g1.rot_local >> 3) & 1, ctx->super_groups, false,

@@ -143,7 +143,9 @@ struct SuperArgs {
   int split_a;
   unsigned* doneB;     // [nchunks] group-k tiles issued per chunk (zeroed before launch)
   unsigned* qab;       // producer-warp variant: [0] next group-0 tile, [1] next group-k tile (zeroed)
-  int done_shift;      // done[c] counts 2^done_shift arrivals per tile (3: one per warp, pass_tmem.cu)
+  int done_shift;      // done[c] counts 2^done_shift arrivals per tile (3: one per warp: pass_tmem.cu, v2)
+  int v2;              // qaa_superpass: split-phase WAR guards + deferred per-warp publish (default 1)
+  int diag;            // QAA_OPT_DIAG: diagnostic kernel variant (work removed; wrong results by design)
   int tm_flags;        // pass_tmem.cu A/B switches: 1 = group-0 slot released at the tile's end,
                        // 2 = publish right after the stores, 4 = spin (no suspend hint) in waits,
                        // 8 = count waits into dbg (diagnostics), 16 = no early retry of deferred loads
@@ -191,6 +193,25 @@ struct ResidentArgs {
   int final_d;              // 1: apply row K of phi_all after the last X (Strang closing half step)
 };
 cudaError_t launch_resident(const ResidentArgs& a, cudaStream_t st);
+// 13 <= L <= 16: all K steps in one launch, the state in the registers of one
+// thread-block cluster of 2^(L-12) CTAs per replica (cluster_evolve.cu)
+struct ClusterArgs {
+  double2* psi;             // single evolve: canonical state in/out; nullptr: replicas start uniform
+  const uint8_t* E;
+  int L;
+  double amp0;              // 2^{-n/2} (replicas)
+  int64_t K;                // steps (single evolve)
+  const int64_t* Krep;      // per replica steps (sweep) or nullptr
+  const int64_t* row_off;   // per replica first row of phi_all/coef/form, or nullptr
+  const double2* phi_all;   // rows of n_phi entries
+  int n_phi;
+  const double* coef;
+  const int32_t* form;
+  int final_d;              // Strang: apply row off+K after the last X
+  double* out;              // per replica P_succ, or nullptr
+};
+cudaError_t launch_cluster_evolve(const ClusterArgs& a, int nrep, cudaStream_t st);
+int cluster_evolve_max_active(int L);
 // 10 <= L <= 12: register-phase variant (2-3x faster than the per-qubit loop)
 cudaError_t launch_resident_phases(const ResidentArgs& a, cudaStream_t st);
 

@@ -36,6 +36,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// one non-blocking probe of the phase
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(sa(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // bounded wait: a lost arrival becomes a trap (launch error) instead of a hang
 __device__ __forceinline__ void mbar_wait_bounded(uint64_t* b, uint32_t parity) {
   for (uint32_t it = 0;; it++) {
@@ -457,7 +469,7 @@ __device__ void super_issue(const CUtensorMap* kmap, const SuperArgs& a, int64_t
     return;
   }
   const uint32_t T = pdep32(i, a.k_imask) | pdep32((uint32_t)c, a.k_cmask);
-  if (ld_acquire(&a.done[c]) >= (1u << (a.tpc_bits + a.done_shift))) {
+  if ((a.diag & 8) || ld_acquire(&a.done[c]) >= (1u << (a.tpc_bits + a.done_shift))) {
     fence_async_global();  // generic-proxy stores of chunk c -> this async-proxy read
     meta[s] = SlotMeta{SK_B, (int)c, T, 0};
     load_gk<BD>(kmap, a, T, slots + (size_t)s * FAST_XBUF, eslots + (size_t)s * TILE, fb, pol_dead);

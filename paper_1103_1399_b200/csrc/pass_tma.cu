@@ -64,6 +64,35 @@ __device__ __forceinline__ void xchg(double2* xb, double2 (&v)[RPT], int lane, i
 #pragma unroll
   for (int r = 0; r < RPT; r++) v[r] = xb[bl + padA(r << reg_shift<TO>())];
 }
+// Split-phase write-after-read guard (the L2-blocked step, SuperArgs.v2): every
+// thread of the group arrives on the group's WAR mbarrier (count 256, release
+// semantics: its reads of the buffer are performed first) right after its last
+// read of the buffer, and waits on it only right before its next write into the
+// buffer -- the rotations in between no longer wait for the slowest warp.
+struct War {
+  uint64_t* bar;
+  uint32_t ph;
+};
+template <bool SPLIT>
+__device__ __forceinline__ void war_arrive(War& w) {
+  if (SPLIT) mbar_arrive_notx(w.bar);
+}
+template <int FROM, int TO, bool SPLIT>
+__device__ __forceinline__ void xchg_s(double2* xb, double2 (&v)[RPT], int lane, int warp, int g, War& w) {
+  if (!SPLIT) {
+    xchg<FROM, TO>(xb, v, lane, warp, g);
+    return;
+  }
+  const int bs = padA(pat_tl<FROM>(lane, warp));
+  mbar_wait(w.bar, w.ph & 1);
+  w.ph++;
+#pragma unroll
+  for (int r = 0; r < RPT; r++) xb[bs + padA(r << reg_shift<FROM>())] = v[r];
+  group_bar(g);
+  const int bl = padA(pat_tl<TO>(lane, warp));
+#pragma unroll
+  for (int r = 0; r < RPT; r++) v[r] = xb[bl + padA(r << reg_shift<TO>())];
+}
 // Warp-local exchange PB -> PC, in place in the landed (unpadded) tile. Both
 // patterns hold warp bits 9..11, so a warp only ever touches its own 512
 // amplitudes: no group barrier. Position of local index l: l ^ ((l >> 4) & 7)
@@ -99,9 +128,11 @@ __device__ __forceinline__ void diag(double2 (&v)[RPT], const uint8_t* es, const
   }
 }
 
-template <int PROG, bool LANE3>
+template <int PROG, bool LANE3, bool SPLIT = false, int DIAG = 0>
 __device__ __forceinline__ void program(const TmaArgs& a, double2 (&v)[RPT], double2* xb, const uint8_t* es,
-                                        const double2* phis, int lane, int warp, int g) {
+                                        const double2* phis, int lane, int warp, int g, War& w) {
+  static_assert(!SPLIT || PROG == FP_G0_PRE || PROG == FP_GK_PRE || PROG == FP_GK_PRE_D_POST,
+                "split-phase WAR guard: L2-blocked step programs only");
   const double(&t0)[TILE_BITS] = a.t[0];
   const double(&t1)[TILE_BITS] = a.t[1];
   if (PROG == FP_G0_DPOST) {
@@ -113,11 +144,12 @@ __device__ __forceinline__ void program(const TmaArgs& a, double2 (&v)[RPT], dou
     rot_regs<PB>(v, t1);
   } else if (PROG == FP_G0_PRE) {
     // landed read in PB; PB -> PC warp-local; one cross-warp exchange to PA
-    rot_regs<PB>(v, t0);
-    xchg_local_pb_pc(xb, v, lane, warp);
-    rot_regs<PC>(v, t0);
-    xchg<PC, PA>(xb, v, lane, warp, g);
-    rot_regs<PA>(v, t0);
+    if (!(DIAG & 1)) rot_regs<PB>(v, t0);
+    if (!(DIAG & 2)) xchg_local_pb_pc(xb, v, lane, warp);
+    if (!(DIAG & 2)) war_arrive<SPLIT>(w);
+    if (!(DIAG & 1)) rot_regs<PC>(v, t0);
+    if (!(DIAG & 2)) xchg_s<PC, PA, SPLIT>(xb, v, lane, warp, g, w);
+    if (!(DIAG & 1)) rot_regs<PA>(v, t0);
   } else if (PROG == FP_G0_PRE_D_POST) {
     rot_regs<PA>(v, t0);
     xchg<PA, PC>(xb, v, lane, warp, g);
@@ -131,29 +163,32 @@ __device__ __forceinline__ void program(const TmaArgs& a, double2 (&v)[RPT], dou
     xchg<PC, PA>(xb, v, lane, warp, g);
     rot_regs<PA>(v, t1);
   } else if (PROG == FP_GK_PRE) {
-    rot_regs<PA>(v, t0);
-    xchg<PA, PB>(xb, v, lane, warp, g);
-    rot_regs<PB>(v, t0);
+    if (!(DIAG & 2)) war_arrive<SPLIT>(w);
+    if (!(DIAG & 1)) rot_regs<PA>(v, t0);
+    if (!(DIAG & 2)) xchg_s<PA, PB, SPLIT>(xb, v, lane, warp, g, w);
+    if (!(DIAG & 1)) rot_regs<PB>(v, t0);
     if (LANE3) rot_lane(v, 3, t0[3]);
   } else if (PROG == FP_GK_PRE_D_POST) {
-    rot_regs<PA>(v, t0);
-    xchg<PA, PB>(xb, v, lane, warp, g);
-    rot_regs<PB>(v, t0);
+    if (!(DIAG & 2)) war_arrive<SPLIT>(w);
+    if (!(DIAG & 1)) rot_regs<PA>(v, t0);
+    if (!(DIAG & 2)) xchg_s<PA, PB, SPLIT>(xb, v, lane, warp, g, w);
+    if (!(DIAG & 2)) war_arrive<SPLIT>(w);
+    if (!(DIAG & 1)) rot_regs<PB>(v, t0);
     if (LANE3) {
       // tile bit 3 through a register: PB -> PB3, D in PB3 (the packed energy
       // slice follows PB3), post rotations of bits 3..6, PB3 -> PB, bit 7
-      swap_r3_l3(v, lane);
-      rot_regbit<3>(v, t0[3]);
-      diag<PB, true>(v, es, phis, lane, warp);
-      rot_regs_pb3(v, t1);
-      swap_r3_l3(v, lane);
-      rot_regbit<3>(v, t1[7]);
+      if (!(DIAG & 1)) swap_r3_l3(v, lane);
+      if (!(DIAG & 1)) rot_regbit<3>(v, t0[3]);
+      if (!(DIAG & 4)) diag<PB, true>(v, es, phis, lane, warp);
+      if (!(DIAG & 1)) rot_regs_pb3(v, t1);
+      if (!(DIAG & 1)) swap_r3_l3(v, lane);
+      if (!(DIAG & 1)) rot_regbit<3>(v, t1[7]);
     } else {
-      diag<PB, true>(v, es, phis, lane, warp);
-      rot_regs<PB>(v, t1);
+      if (!(DIAG & 4)) diag<PB, true>(v, es, phis, lane, warp);
+      if (!(DIAG & 1)) rot_regs<PB>(v, t1);
     }
-    xchg<PB, PA>(xb, v, lane, warp, g);
-    rot_regs<PA>(v, t1);
+    if (!(DIAG & 2)) xchg_s<PB, PA, SPLIT>(xb, v, lane, warp, g, w);
+    if (!(DIAG & 1)) rot_regs<PA>(v, t1);
   }
 }
 
@@ -244,7 +279,8 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_pass_tma(const __grid_co
     load_landed<I::load_pat>(v, xb, lane, lw);  // landed layout: tile-local order
     // no barrier: the first shared-memory write of every program is warp-local
     // in place or an exchange with a leading barrier
-    program<PROG, LANE3>(a, v, xb, es, phis, lane, lw, g);
+    War w{nullptr, 0};
+    program<PROG, LANE3>(a, v, xb, es, phis, lane, lw, g, w);
     // release the slot (the program's final rotations consumed every value this
     // warp read from it); the last warp of the group refills it
     __syncwarp();
@@ -285,7 +321,13 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_pass_tma(const __grid_co
 // BD: the group-k sub-pass is rotate/D/rotate (single GPU); otherwise a plain
 // rotate whose tiles may be stored straight into the peers' next shard buffers
 // (a.remote: the layout swap of the sharded plan)
-template <bool LANE3, int NG, bool BD>
+// V2 (SuperArgs.v2, default): split-phase write-after-read guards on a per-group
+// mbarrier (xchg_s) and a DEFERRED per-warp publish of the group-0 tiles: a warp
+// does not wait for its group after its stores; it remembers the chunk and adds
+// its 1/8 of the tile to done[c] (red.release) at its next tile's first exchange,
+// when its stores have drained -- or before any wait on a chunk and at the end,
+// so a chunk's count can never wait on a warp that waits for it.
+template <bool LANE3, int NG, bool BD, bool V2, int DIAG = 0>
 __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_constant__ CUtensorMap kmap,
                                                                  const SuperArgs a) {
   constexpr int BPROG = BD ? FP_GK_PRE_D_POST : FP_GK_PRE;
@@ -306,6 +348,8 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
   if (tid == 0) {
     for (int s = 0; s < NG * TMA_SLOTS; s++) mbar_init(&full[s], 1);
     for (int g = 0; g < NG; g++) mbar_init(&late[g], 1);
+    if (V2)
+      for (int g = 0; g < NG; g++) mbar_init(&slot_consumed(sm)[g], NTHREADS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int64_t J = 0; J < TMA_SLOTS; J++) super_issue<NG, BD>(&kmap, a, J, slots, eslots, full, meta, pol_dead);
   }
@@ -317,11 +361,25 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
   const Off ps0 = make_off<Info<FP_G0_PRE>::store_pat>(a.g0, lane, lw);
   uint32_t late_phase = 0;
   double2 v[RPT];
+  War war{V2 ? &slot_consumed(sm)[g] : nullptr, 0};
+  int pend = -1;  // V2: chunk of this warp's unpublished group-0 tile
+  const unsigned chunk_done = 1u << (a.tpc_bits + a.done_shift);
+  auto publish = [&]() {
+    if (V2 && pend >= 0) {
+      __syncwarp();
+      if (lane == 0) red_release_add(&a.done[pend], 1u);
+      pend = -1;
+    }
+  };
   for (int64_t J = g;; J += NG) {
     const int s = (int)(J % TMA_SLOTS);
+    // never block with an unpublished tile: the landed tile may wait on a load
+    // whose issuer waits for this chunk (the refill order is not J order)
+    if (V2 && pend >= 0 && !mbar_test(&full[NG * s + g], (uint32_t)((J / period<NG>()) & 1))) publish();
     mbar_wait_bounded(&full[NG * s + g], (uint32_t)((J / period<NG>()) & 1));
     const SlotMeta m = meta[s];
     if (m.kind == SK_END) {
+      publish();
       // tile J+3 belongs to the other group and is only ever issued by the
       // finisher of J: pass the end marker on before leaving
       group_bar(g);
@@ -331,8 +389,10 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
     double2* xb = slots + (size_t)s * FAST_XBUF;
     uint8_t* es = eslots + (size_t)s * TILE;
     if (m.kind == SK_B_DEFERRED) {
+      publish();
+      if (DIAG & 8) __trap();  // super_issue never defers in this variant
       if (gtid == 0) {
-        for (uint32_t it = 0; ld_acquire(&a.done[m.c]) < (1u << a.tpc_bits); it++) {
+        for (uint32_t it = 0; ld_acquire(&a.done[m.c]) < chunk_done; it++) {
           __nanosleep(32);
           if (it > (1u << 26)) __trap();
         }
@@ -362,11 +422,14 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
     const bool isb = m.kind != SK_A && m.kind != SK_A_DEFERRED;
     if (isb) {
       load_landed<Info<BPROG>::load_pat>(v, xb, lane, lw);
-      program<BPROG, LANE3>(a.gk, v, xb, es, phis, lane, lw, g);
+      if (a.tm_flags & 1) publish();
+      program<BPROG, LANE3, V2, DIAG>(a.gk, v, xb, es, phis, lane, lw, g, war);
     } else {
       load_landed<Info<FP_G0_PRE>::load_pat>(v, xb, lane, lw);
-      program<FP_G0_PRE, false>(a.g0, v, xb, nullptr, phis, lane, lw, g);
+      if (a.tm_flags & 1) publish();
+      program<FP_G0_PRE, false, V2, DIAG>(a.g0, v, xb, nullptr, phis, lane, lw, g, war);
     }
+    publish();  // the previous group-0 tile's stores have drained by now
     __syncwarp();
     if (lane == 0 && last_warp_out(&cnt[s])) super_issue<NG, BD>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
     if (isb) {
@@ -387,13 +450,16 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
       double2* dst = a.g0.psi + tbase(a.g0, m.T);
 #pragma unroll
       for (int r = 0; r < RPT; r++) st_hint(dst + roff(ps0, r), v[r], pol_keep);
-      // publish: the group's stores of this group-0 tile happen before the
-      // barrier; one gpu-scope release add makes them visible to the
-      // acquiring issuer of chunk c's group-k tiles (the grid-sync pattern).
-      // (A barrier-free variant -- per-warp counter, the 8th warp releases --
-      // was measured 2 % slower.)
-      group_bar(g);
-      if (gtid == 0) red_release_add(&a.done[m.c], 1u);
+      if (V2) {
+        pend = m.c;  // published one tile later (publish() above)
+        if (a.tm_flags & 2) publish();
+      } else {
+        // publish: the group's stores of this group-0 tile happen before the
+        // barrier; one gpu-scope release add makes them visible to the
+        // acquiring issuer of chunk c's group-k tiles (the grid-sync pattern).
+        group_bar(g);
+        if (gtid == 0) red_release_add(&a.done[m.c], 1u);
+      }
     }
   }
   if (!BD && a.remote) __threadfence_system();
@@ -518,6 +584,7 @@ __global__ void __launch_bounds__(PW_THREADS, 1) qaa_superpass_pw(const __grid_c
   }
   const int g = warp >> 3, lw = warp & 7, gtid = tid & (NTHREADS - 1);
   double2 v[RPT];
+  War war{nullptr, 0};
   for (int J = g;; J += NG) {
     const int s = J % TMA_SLOTS;
     const long long t0 = (a.tm_flags & 8) ? clock64() : 0;
@@ -533,10 +600,10 @@ __global__ void __launch_bounds__(PW_THREADS, 1) qaa_superpass_pw(const __grid_c
     const bool isb = m.kind != SK_A;
     if (isb) {
       load_landed<Info<BPROG>::load_pat>(v, xb, lane, lw);
-      program<BPROG, LANE3>(a.gk, v, xb, es, phis, lane, lw, g);
+      program<BPROG, LANE3>(a.gk, v, xb, es, phis, lane, lw, g, war);
     } else {
       load_landed<Info<FP_G0_PRE>::load_pat>(v, xb, lane, lw);
-      program<FP_G0_PRE, false>(a.g0, v, xb, nullptr, phis, lane, lw, g);
+      program<FP_G0_PRE, false>(a.g0, v, xb, nullptr, phis, lane, lw, g, war);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive_notx(&empty[s]);
@@ -572,13 +639,29 @@ PwKernel pick_pw(bool lane3, bool bd) {
 }
 
 typedef void (*SuperKernel)(const CUtensorMap, const SuperArgs);
-template <bool BD>
+template <bool BD, bool V2>
 SuperKernel pick_super_bd(bool lane3, int ng) {
-  if (ng == 1) return lane3 ? qaa_superpass<true, 1, BD> : qaa_superpass<false, 1, BD>;
-  return lane3 ? qaa_superpass<true, 2, BD> : qaa_superpass<false, 2, BD>;
+  if (ng == 1) return lane3 ? qaa_superpass<true, 1, BD, V2> : qaa_superpass<false, 1, BD, V2>;
+  return lane3 ? qaa_superpass<true, 2, BD, V2> : qaa_superpass<false, 2, BD, V2>;
 }
-SuperKernel pick_super(bool lane3, int ng, bool bd) {
-  return bd ? pick_super_bd<true>(lane3, ng) : pick_super_bd<false>(lane3, ng);
+// diagnostic variants (QAA_OPT_DIAG, bench configuration only; results are wrong
+// by design): 1 = no rotations, 2 = no shared-memory exchanges, 4 = no D,
+// 8 = group-k tiles ignore the chunk dependency (super_issue)
+SuperKernel pick_super_diag(int diag) {
+  switch (diag) {
+    case 1: return qaa_superpass<true, 2, true, true, 1>;
+    case 2: return qaa_superpass<true, 2, true, true, 2>;
+    case 3: return qaa_superpass<true, 2, true, true, 3>;
+    case 4: return qaa_superpass<true, 2, true, true, 4>;
+    case 7: return qaa_superpass<true, 2, true, true, 7>;
+    case 8: return qaa_superpass<true, 2, true, true, 8>;
+    case 15: return qaa_superpass<true, 2, true, true, 15>;
+    default: return nullptr;
+  }
+}
+SuperKernel pick_super(bool lane3, int ng, bool bd, bool v2) {
+  if (v2) return bd ? pick_super_bd<true, true>(lane3, ng) : pick_super_bd<false, true>(lane3, ng);
+  return bd ? pick_super_bd<true, false>(lane3, ng) : pick_super_bd<false, false>(lane3, ng);
 }
 
 typedef void (*TmaKernel)(const CUtensorMap, const TmaArgs);
@@ -603,7 +686,11 @@ TmaKernel pick(int prog, bool lane3, int ng) { return ng == 1 ? pick_ng<1>(prog,
 
 cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, int ngroups, bool bd, int grid,
                              cudaStream_t st) {
-  SuperKernel k = pick_super(lane3, ngroups, bd);  // shared-memory attribute set in pass_tma_setup
+  SuperKernel k = pick_super(lane3, ngroups, bd, a.v2 != 0);  // shared-memory attribute set in pass_tma_setup
+  if (a.diag && bd) {  // the D-less closing pair keeps the real kernel
+    if (!lane3 || ngroups != 2 || !a.v2 || !pick_super_diag(a.diag)) return cudaErrorInvalidValue;
+    k = pick_super_diag(a.diag);
+  }
   // cooperative launch: the chunk dependencies spin across CTAs, so every CTA
   // must be co-resident -- the launch fails instead of deadlocking
   cudaLaunchConfig_t cfg = {};
@@ -643,11 +730,18 @@ cudaError_t pass_tma_setup() {
     }
   for (int l = 0; l < 2; l++)
     for (int ng = 1; ng <= 2; ng++)
-      for (int bd = 0; bd < 2; bd++) {
-        cudaError_t e = cudaFuncSetAttribute(pick_super(l, ng, bd), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)TMA_SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-      }
+      for (int bd = 0; bd < 2; bd++)
+        for (int v2 = 0; v2 < 2; v2++) {
+          cudaError_t e = cudaFuncSetAttribute(pick_super(l, ng, bd, v2), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)TMA_SMEM_BYTES);
+          if (e != cudaSuccess) return e;
+        }
+  for (int d = 1; d < 16; d++)
+    if (pick_super_diag(d)) {
+      cudaError_t e = cudaFuncSetAttribute(pick_super_diag(d), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)TMA_SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+    }
   for (int p = 0; p < FP_COUNT; p++)
     for (int l = 0; l < 2; l++)
       for (int ng = 1; ng <= 2; ng++) {

@@ -206,6 +206,64 @@ def test_cot_form_large_beta(q, ctx, orc):
         assert_close(got, want)
 
 
+@pytest.mark.parametrize("n", [13, 14, 15, 16])
+@pytest.mark.parametrize("K", [1, 2, 7])
+def test_cluster_evolve_parity(q, ctx, orc, n, K):
+    """13 <= n <= 16: the whole evolution in ONE launch, state resident in the
+    registers of a 2^(n-12)-CTA cluster (cluster bits swapped with local bits over
+    DSMEM every step) -- against the oracle from a random state, random schedule."""
+    cl = instance(n)
+    psi0 = cnf.random_state(n, 40 + n)
+    sched = np.random.default_rng(n * 10 + K).uniform(0, 1, K)
+    got, want, _ = run_both(q, ctx, orc, n, cl, 1.1 * K, K, schedule=sched, psi0=psi0)
+    assert_close(got, want)
+    st = ctx.stats()
+    assert st["cluster_launches"] == 1 and st["pass_launches"] == 1
+
+
+@pytest.mark.parametrize("n", [13, 16])
+def test_cluster_evolve_forms_and_orders(q, ctx, orc, n):
+    """The cluster-resident evolve with the cot form (|beta| > pi/4), Strang
+    splitting (closing half step after the last phase) and the driving term."""
+    cl = instance(n)
+    E = orc.energy_table(n, cl)
+    psi0 = cnf.random_state(n, 3)
+    sched = np.array([0.0, 0.1, 0.5, 0.95, 0.0])
+    got, want, _ = run_both(q, ctx, orc, n, cl, 2.0 * 5 * 1.3, 5, schedule=sched, psi0=psi0)  # beta up to 1.3
+    assert_close(got, want)
+    ctx.set_option(q.OPT_ORDER, 2)
+    ctx.set_state(psi0)
+    sched = np.random.default_rng(n).uniform(0, 1, 6)
+    ctx.evolve(2.2, 6, sched)
+    assert_close(ctx.state(), orc.evolve_strang(n, E, psi0, 2.2, 6, sched))
+    ctx.set_option(q.OPT_ORDER, 1)
+    ctx.set_driver(0.7, -0.4)
+    ctx.set_state(psi0)
+    ctx.evolve(1.9, 5, sched[:5])
+    assert_close(ctx.state(), orc.evolve_driven(n, E, psi0, 1.9, 5, 0.7, -0.4, sched[:5]))
+    assert ctx.stats()["cluster_launches"] == 3
+
+
+def test_cluster_evolve_matches_pass_kernels(q, orc):
+    """n = 16: the cluster-resident launch and the per-pass kernels (QAA_OPT_CLUSTER 0)
+    agree to rounding on a 40-step run, and both match the oracle."""
+    n, K, T = 16, 40, 5.0
+    cl = instance(n)
+    out = []
+    for cflag in (1, 0):
+        with q.Context(0) as c:
+            c.set_option(q.OPT_CLUSTER, cflag)
+            c.load_instance(n, cl)
+            c.init_uniform()
+            c.evolve(T, K)
+            assert c.stats()["cluster_launches"] == (1 if cflag else 0)
+            out.append(c.state())
+    want = orc.evolve(n, orc.energy_table(n, cl), orc.init_uniform(n), T, K)
+    for got in out:
+        assert_close(got, want)
+    assert np.max(np.abs(out[0] - out[1])) < 1e-13
+
+
 def test_config1_n8_full(q, ctx, orc):
     """BASELINE configs[0]: n = 8 unique-solution instance, T = 10, 100 steps."""
     cl, sol = cnf.load_instance(8)
@@ -369,6 +427,35 @@ def test_error_codes(q, ctx):
     assert "outside" in q.qaa_last_error(ctx.ctx)
 
 
+def test_option_ranges(q, ctx):
+    for key, bad in ((q.OPT_SUPER, 65536), (q.OPT_SUPER, -1), (q.OPT_DIAG, 16), (q.OPT_DIAG, -1)):
+        with pytest.raises(q.QaaError) as e:
+            ctx.set_option(key, bad)
+        assert e.value.status == 1
+    ctx.set_option(q.OPT_DIAG, 0)
+    ctx.set_option(q.OPT_SUPER, 1)
+
+
+@pytest.mark.parametrize("n", [22, 25])
+def test_super_v2_sync_bitwise(q, n):
+    """The default L2-blocked step (split-phase write-after-read mbarriers, deferred
+    per-warp publish) and the round-1 synchronisation (QAA_OPT_SUPER bit 15) run the
+    same per-tile arithmetic: the states after 5 random-schedule steps are equal bit
+    for bit (a lost or early-read tile would break this)."""
+    cl = instance(n)
+    sched = np.random.default_rng(7 * n).uniform(0, 1, 5)
+    out = []
+    for sup in (17, 17 | 32768):
+        with q.Context(0) as c:
+            c.set_option(q.OPT_SUPER, sup)
+            c.load_instance(n, cl)
+            c.set_state(cnf.random_state(n, 5 + n))
+            c.evolve(1.7, 5, sched)
+            assert c.stats()["super_launches"] == 5
+            out.append(c.state())
+    assert np.array_equal(out[0].view(np.uint64), out[1].view(np.uint64))
+
+
 def test_torch_owned_state(q, orc):
     import torch
     c = q.Context(0, n_max=14, torch_state=True)
@@ -505,14 +592,18 @@ def test_strang_parity(q, ctx, orc, n, span, kernel):
     ctx.set_option(q.OPT_ORDER, 1)
 
 
-@pytest.mark.parametrize("n", [6, 8, 10, 11, 12, 13, 14, 15, 16])
+@pytest.mark.parametrize("n,cluster", [(6, 1), (8, 1), (10, 1), (11, 1), (12, 1), (13, 1), (14, 1), (15, 1),
+                                       (16, 1), (13, 0), (14, 0), (15, 0), (16, 0)])
 @pytest.mark.parametrize("order", [1, 2])
-def test_sweep_parity(q, ctx, orc, n, order):
-    """NEXT F1: batched T sweep (one CTA per replica up to n = 13 -- per-qubit
-    loop below n = 10, 16-amplitude register phases from 10 --, one cluster of
-    2^(n-13) CTAs with DSMEM exchange for n = 14..16) against one oracle run per
-    replica (configs[1]-style sweep T in {1,2,5,10,20} at dt = 0.05)."""
+def test_sweep_parity(q, ctx, orc, n, cluster, order):
+    """NEXT F1: batched T sweep (one CTA per replica up to n = 12 -- per-qubit
+    loop below n = 10, 16-amplitude register phases from 10 --; for n = 13..16 one
+    register-resident cluster of 2^(n-12) CTAs per replica (default), or with
+    QAA_OPT_CLUSTER 0 the shared-memory cluster of 2^(n-13) CTAs with per-bit DSMEM
+    phases) against one oracle run per replica (configs[1]-style sweep T in
+    {1,2,5,10,20} at dt = 0.05)."""
     cl = cnf.paper_instance()[1] if n == 6 else instance(n)
+    ctx.set_option(q.OPT_CLUSTER, cluster)
     ctx.set_option(q.OPT_ORDER, order)
     ctx.load_instance(n, cl)
     Ts = np.array([1.0, 2.0, 5.0, 10.0, 20.0])
@@ -533,32 +624,6 @@ def test_sweep_errors(q, ctx):
     ctx.load_instance(8, instance(8))
     with pytest.raises(q.QaaError):
         ctx.sweep([1.0], [0])
-
-
-@pytest.mark.parametrize("n", [31, 32, 33])
-def test_max_size_closed_forms(q, orc, n):
-    """Largest single-GPU sizes (n = 33: 128 GiB state, four tile groups):
-    s = 1 closed form psi_K(x) = 2^{-n/2} e^{-i T E(x)} on sampled x with E from
-    the oracle, and the norm after a few general steps."""
-    import torch
-    free, _ = torch.cuda.mem_get_info()
-    need = (16 + 1 + 3) * (1 << n) + (4 << 30)
-    if free < need:
-        pytest.skip(f"needs {need >> 30} GiB free, have {free >> 30}")
-    cl, sol = cnf.load_instance(n)
-    with q.Context(0) as c:
-        c.load_instance(n, cl)
-        assert c.num_solutions() == 1 and c.energy_table(sol, 1)[0] == 0
-        c.init_uniform()
-        T, K = 0.21, 3
-        c.evolve(T, K, np.ones(K))
-        rng = np.random.default_rng(n)
-        for s0 in list(rng.integers(0, (1 << n) - 32, 12)) + [sol - 5]:
-            xs = np.arange(s0, s0 + 32, dtype=np.uint64)
-            want = 2.0 ** (-n / 2) * np.exp(-1j * T * orc.energy_at(n, cl, xs).astype(float))
-            assert_close(c.state(int(s0), 32), want, atol=1e-15, rtol_l2=1e-12)
-        c.evolve(0.06, 3)
-        assert abs(c.norm2() - 1.0) < 1e-12
 
 
 def test_empty_instance_large(q, ctx, orc):
