@@ -287,6 +287,15 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        registers of a thread-block cluster of 2^(n-12) CTAs (cluster bits
  *                        swapped with local bits over DSMEM once per step); 0: per-pass
  *                        kernels through HBM/L2.
+ *  QAA_OPT_WARPTILE      1 (default): for 13 <= n <= 16 on one GPU with the automatic kernel
+ *                        choice, all passes of the cyclic step-spanning plan run as ONE
+ *                        cooperative launch, one warp per 2^9-amplitude tile (state in L2),
+ *                        a grid barrier between passes; takes precedence over
+ *                        QAA_OPT_CLUSTER (measured 4.1-5.0 vs 5.3-8.3 us per step at
+ *                        n = 13..16). 2: also for 17 <= n <= 21 (there slower than the
+ *                        per-pass kernels; a test hook). 0: off.
+ *  QAA_OPT_WARP_GRID     tuning hook for the warp-tile launch: ctas * 16 + warps per CTA
+ *                        (1..8); 0 (default) = automatic.
  *  QAA_OPT_DIAG          timing diagnostics ONLY (results are wrong by design): the
  *                        L2-blocked step at the bench configuration with work removed --
  *                        1 = no rotations, 2 = no shared-memory exchanges, 4 = no D,
@@ -313,7 +322,9 @@ enum {
   QAA_OPT_SHARD_SYNC = 12,
   QAA_OPT_PERSIST = 13,
   QAA_OPT_DIAG = 14,
-  QAA_OPT_CLUSTER = 16
+  QAA_OPT_CLUSTER = 16,
+  QAA_OPT_WARPTILE = 17,
+  QAA_OPT_WARP_GRID = 18
 };
 qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value);
 
@@ -340,6 +351,7 @@ typedef struct {
                                 [2] deferred group-k items, [3] cycles in deferred waits, [4] / [5]
                                 cycles in group-0 / group-k tile programs; zeros otherwise */
   int64_t cluster_launches;  /* of pass_launches: cluster-resident whole-evolve launches (QAA_OPT_CLUSTER) */
+  int64_t warp_launches;     /* of pass_launches: warp-tile whole-evolve launches (QAA_OPT_WARPTILE) */
 } qaa_stats;
 qaa_status qaa_get_stats(qaa_ctx* ctx, qaa_stats* out);
 qaa_status qaa_reset_stats(qaa_ctx* ctx);

@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libqaa.so")
-SOURCES = ["api_context.cu", "api_tma.cu", "api_shard.cu", "api_evolve.cu", "api_observe.cu", "api_extras.cu", "kernels.cu", "pass_fast.cu", "pass_tma.cu", "pass_tmem.cu", "cluster_evolve.cu", "spectrum.cu", "plan.cpp"]
+SOURCES = ["api_context.cu", "api_tma.cu", "api_shard.cu", "api_evolve.cu", "api_observe.cu", "api_extras.cu", "kernels.cu", "pass_fast.cu", "pass_tma.cu", "pass_tmem.cu", "cluster_evolve.cu", "warp_evolve.cu", "spectrum.cu", "plan.cpp"]
 HEADERS = ["api_internal.hpp", "kernels.cuh", "pass_common.cuh", "plan.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

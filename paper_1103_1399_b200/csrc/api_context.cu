@@ -85,6 +85,8 @@ void qaa_destroy(qaa_ctx* ctx) {
   if (ctx->d_pos_tm) cudaFree(ctx->d_pos_tm);
   if (ctx->d_tm_diag) cudaFree(ctx->d_tm_diag);
   if (ctx->d_persist) cudaFree(ctx->d_persist);
+  for (int g = 0; g < 4; g++)
+    if (ctx->Ewt[g]) cudaFree(ctx->Ewt[g]);
   if (ctx->coef_done) cudaEventDestroy(ctx->coef_done);
   for (auto& p : ctx->ev_pool) {
     cudaEventDestroy(p.first);
@@ -175,6 +177,15 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       ctx->super_pw = (value >> 14) & 1;                // bit 14: producer-warp variant (qaa_superpass_pw)
       ctx->super_v2 = ((value >> 15) & 1) ? 0 : 1;      // bit 15: group barriers instead of split-phase WAR + deferred publish
       ctx->super_hints = ((value >> 2) & 3) == 1 ? 0 : (((value >> 2) & 3) == 2 ? 1 : 2);
+      return QAA_OK;
+    case QAA_OPT_WARPTILE:
+      if (value < 0 || value > 2) return fail(ctx, QAA_E_USAGE, "warptile must be 0, 1 or 2");
+      ctx->warptile = (int)value;
+      return QAA_OK;
+    case QAA_OPT_WARP_GRID:
+      if (value < 0 || (value && ((value & 15) < 1 || (value & 15) > 8 || (value >> 4) < 1)))
+        return fail(ctx, QAA_E_USAGE, "warp grid must be 0 or ctas * 16 + warps (1..8)");
+      ctx->warp_grid = (int)value;
       return QAA_OK;
     case QAA_OPT_CLUSTER:
       if (value < 0 || value > 1) return fail(ctx, QAA_E_USAGE, "cluster must be 0 or 1");
@@ -347,6 +358,7 @@ qaa_status qaa_load_instance(qaa_ctx* ctx, int n, int m, const int32_t* lits) {
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     ctx->z_listed = true;
   }
+  ctx->wt_built = false;  // warp-tile energy tables follow E (built on first use)
   if (ctx->world == 1) {
     qaa_status st = build_tma(ctx);
     if (st) return st;

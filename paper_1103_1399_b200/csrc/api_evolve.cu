@@ -246,6 +246,103 @@ static bool try_persist(qaa_ctx* ctx, const std::vector<PassPlan>& plan, const s
   return true;
 }
 
+// Warp-tile groups (warp_evolve.cu): group 0 = bits 0..8; group g >= 1 = bits
+// {0, 1} + fillers {2, ...} (not rotated) + the next <= 7 bits (rotated)
+int warp_group_count(int L) { return 1 + (L - 9 + 6) / 7; }
+static void build_warp_geo(int L, WarpGeo* out, int* ngroups) {
+  int ng = 0;
+  WarpGeo g0;
+  memset(&g0, 0, sizeof g0);
+  for (int b = 0; b < 9; b++) g0.phys[b] = b;
+  g0.rot = 0x1FFu;
+  out[ng++] = g0;
+  for (int next = 9; next < L;) {
+    const int hb = std::min(7, L - next);
+    WarpGeo g;
+    memset(&g, 0, sizeof g);
+    int t = 0;
+    for (int b = 0; b < 2 + (7 - hb); b++) g.phys[t++] = b;  // row bits + fillers
+    for (int b = 0; b < hb; b++) {
+      g.rot |= 1u << t;
+      g.phys[t++] = next + b;
+    }
+    next += hb;
+    out[ng++] = g;
+  }
+  for (int k = 0; k < ng; k++) {
+    bool in[64] = {false};
+    for (int b = 0; b < 9; b++) in[out[k].phys[b]] = true;
+    out[k].nfree = 0;
+    for (int p = 0; p < L; p++)
+      if (!in[p]) out[k].free_bits[out[k].nfree++] = p;
+  }
+  *ngroups = ng;
+}
+
+static qaa_status run_warp_evolve(qaa_ctx* ctx, const WarpPass* dplan, int64_t npass, const double2* dphi,
+                                  const double* dcoef, const int32_t* dform, int n_phi) {
+  if (!ctx->wt_built) {
+    build_warp_geo(ctx->L, ctx->wgeo, &ctx->wt_groups);
+    for (int g = 0; g < ctx->wt_groups; g++) {
+      if (ctx->Ewt[g]) cudaFree(ctx->Ewt[g]);
+      ctx->Ewt[g] = nullptr;
+      CUDA_TRY(cudaMalloc(&ctx->Ewt[g], (size_t)1 << ctx->L));
+      CUDA_TRY(launch_warp_energy(ctx->E, ctx->Ewt[g], ctx->wgeo[g], ctx->L, ctx->num_sms, ctx->stream));
+      ctx->stats.kernel_launches_total++;
+    }
+    ctx->wt_built = true;
+  }
+  {
+    qaa_status st = ensure_buffer(ctx, &ctx->d_persist, &ctx->d_persist_cap, 256);
+    if (st) return st;
+  }
+  WarpEvolveArgs wa;
+  memset(&wa, 0, sizeof wa);
+  wa.psi = ctx->state;
+  wa.L = ctx->L;
+  for (int g = 0; g < ctx->wt_groups; g++) {
+    wa.geo[g] = ctx->wgeo[g];
+    wa.Eg[g] = ctx->Ewt[g];
+  }
+  wa.plan = dplan;
+  wa.npass = npass;
+  wa.phi_all = dphi;
+  wa.n_phi = n_phi;
+  wa.coef = dcoef;
+  wa.form = dform;
+  wa.bar = (unsigned*)ctx->d_persist;
+  if (ctx->super_tm_flags & 8) {  // QAA_OPT_SUPER bit 10: phase cycle counters into tm_diag
+    if (!ctx->d_tm_diag) {
+      CUDA_TRY(cudaMalloc(&ctx->d_tm_diag, 8 * sizeof(unsigned long long)));
+      CUDA_TRY(cudaMemsetAsync(ctx->d_tm_diag, 0, 8 * sizeof(unsigned long long), ctx->stream));
+    }
+    wa.dbg = ctx->d_tm_diag;
+  }
+  CUDA_TRY(cudaMemsetAsync(ctx->d_persist, 0, 16, ctx->stream));
+  size_t ev = ctx->ev_used;
+  if (ctx->profile) {
+    qaa_status st = ensure_events(ctx, ev + 1);
+    if (st) return st;
+    CUDA_TRY(cudaEventRecord(ctx->ev_pool[ev].first, ctx->stream));
+  }
+  // grid: fewer, fuller CTAs make the per-pass grid barrier cheaper (tuning hook
+  // QAA_OPT_WARP_GRID = ctas * 16 + warps per CTA; 0 = automatic)
+  int grid = ctx->num_sms, warps = 8;
+  if (ctx->warp_grid) {
+    grid = std::min(ctx->num_sms, ctx->warp_grid >> 4);
+    warps = ctx->warp_grid & 15;
+  }
+  CUDA_TRY(launch_warp_evolve(wa, grid, warps, ctx->stream));
+  if (ctx->profile) {
+    CUDA_TRY(cudaEventRecord(ctx->ev_pool[ev].second, ctx->stream));
+    ctx->ev_used = ev + 1;
+  }
+  ctx->stats.pass_launches++;
+  ctx->stats.warp_launches++;
+  ctx->stats.kernel_launches_total++;
+  return QAA_OK;
+}
+
 extern "C" {
 
 qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule) {
@@ -263,7 +360,16 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
   const size_t phi_bytes = (size_t)(ctx->order == 2 ? K + 1 : K) * n_phi * sizeof(double2);
   const size_t coef_bytes = (size_t)K * sizeof(double);
   const size_t form_bytes = (size_t)K * sizeof(int32_t);
-  const size_t total = phi_bytes + coef_bytes + form_bytes + 256;
+  // the warp-tile path stages its pass records behind the coefficients
+  const bool use_warp = ctx->warptile && ctx->world == 1 && ctx->kernel_mode == 2 && ctx->L >= WARP_MIN_L &&
+                        ctx->L <= (ctx->warptile == 2 ? WARP_MAX_L : WARP_AUTO_MAX_L);
+  std::vector<PassPlan> wplan;
+  if (use_warp) {
+    build_pass_schedule(warp_group_count(ctx->L), K, 1, &wplan);
+    if (ctx->order == 2) wplan.back().d_step = K;  // Strang closing half step
+  }
+  const size_t wplan_off = (phi_bytes + coef_bytes + form_bytes + 15) & ~(size_t)15;
+  const size_t total = (use_warp ? wplan_off + wplan.size() * sizeof(WarpPass) : phi_bytes + coef_bytes + form_bytes) + 256;
   // staging buffer may still be feeding a previous async copy
   if (ctx->coef_pending) {
     CUDA_TRY(cudaEventSynchronize(ctx->coef_done));
@@ -294,6 +400,26 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
     const double theta = 0.5 * dtK * weight_p(ctx, sl);
     for (int e = 0; e < n_phi; e++)
       hphi[(size_t)K * n_phi + e] = make_double2(std::cos(theta * (double)e), -std::sin(theta * (double)e));
+  }
+  if (use_warp) {
+    WarpPass* hp = (WarpPass*)((char*)ctx->h_coef + wplan_off);
+    for (size_t i = 0; i < wplan.size(); i++) {
+      const PassPlan& pp = wplan[i];
+      WarpPass w{pp.group, 0, 0, 0.0, 0.0};
+      if (pp.pre_step >= 0) {
+        w.flags |= WP_PRE | (sc[(size_t)pp.pre_step].form ? 8 : 0);
+        w.cpre = sc[(size_t)pp.pre_step].coef;
+      }
+      if (pp.d_step >= 0) {
+        w.flags |= WP_D;
+        w.d = pp.d_step;
+      }
+      if (pp.post_step >= 0) {
+        w.flags |= WP_POST | (sc[(size_t)pp.post_step].form ? 16 : 0);
+        w.cpost = sc[(size_t)pp.post_step].coef;
+      }
+      hp[i] = w;
+    }
   }
   // the device table is read by kernels still queued from a previous evolve:
   // growing it must not free memory under them
@@ -340,6 +466,11 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
     ctx->stats.pass_launches++;
     ctx->stats.kernel_launches_total++;
     return QAA_OK;
+  }
+  if (use_warp) {
+    qaa_status st = run_warp_evolve(ctx, (const WarpPass*)((char*)ctx->d_coef + wplan_off), (int64_t)wplan.size(),
+                                    dphi, dcoef, dform, n_phi);
+    return st;
   }
   if (ctx->cluster_evolve && ctx->L >= 13 && ctx->L <= 16 && ctx->kernel_mode == 2) {
     // the whole evolution in one launch, state in one cluster's registers

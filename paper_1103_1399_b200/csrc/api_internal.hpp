@@ -41,6 +41,10 @@ struct ClauseRecHost {
 static_assert(sizeof(ClauseRecHost) == 32, "clause record layout");
 }  // namespace
 
+constexpr int WARP_MIN_L = 13, WARP_MAX_L = 21;  // warp_evolve.cu range (QAA_OPT_WARPTILE 2)
+constexpr int WARP_AUTO_MAX_L = 16;               // default range: faster than the per-pass kernels up to here
+int warp_group_count(int L);
+
 struct qaa_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -105,6 +109,12 @@ struct qaa_ctx {
   int super_pw = 0;  // producer-warp L2-blocked step
   int diag = 0;      // QAA_OPT_DIAG (timing diagnostics only)
   int cluster_evolve = 1;  // QAA_OPT_CLUSTER: 13 <= L <= 16 in one cluster-resident launch
+  int warptile = 1;        // QAA_OPT_WARPTILE: 13 <= L <= 21 in one warp-tile cooperative launch
+  int warp_grid = 0;       // QAA_OPT_WARP_GRID: ctas * 16 + warps (0 = automatic)
+  bool wt_built = false;   // Ewt / wgeo match the loaded instance
+  int wt_groups = 0;
+  WarpGeo wgeo[4];
+  uint8_t* Ewt[4] = {nullptr, nullptr, nullptr, nullptr};
   int super_v2 = 1;  // split-phase WAR guards + deferred publish (QAA_OPT_SUPER bit 15 clears it)
   int super_grid = 0;  // 0: one CTA per SM
   int super_split = 0;

@@ -212,6 +212,37 @@ struct ClusterArgs {
 };
 cudaError_t launch_cluster_evolve(const ClusterArgs& a, int nrep, cudaStream_t st);
 int cluster_evolve_max_active(int L);
+// 13 <= L <= 21: all passes of the cyclic plan in one cooperative launch, one
+// warp per 2^9-amplitude tile, grid barrier between passes (warp_evolve.cu)
+struct WarpGeo {
+  int phys[9];          // tile bit b -> physical bit
+  uint32_t rot;         // tile bits rotated by this group
+  int nfree;            // L - 9
+  int free_bits[32];    // tile-id bit i -> physical bit
+};
+struct WarpPass {
+  int group;
+  int flags;       // WP_PRE | WP_D | WP_POST, bit 3 / bit 4: pre / post in the cot form
+  int64_t d;       // row of phi_all for D
+  double cpre, cpost;  // rotation coefficients (tan or cot of beta) of the pre / post steps
+};
+enum { WP_PRE = 1, WP_D = 2, WP_POST = 4 };
+struct WarpEvolveArgs {
+  double2* psi;
+  int L;
+  WarpGeo geo[4];
+  const uint8_t* Eg[4];   // per group: tile T's energies at Eg + 512 T, PX order (lane * 16 + r)
+  const WarpPass* plan;
+  int64_t npass;
+  const double2* phi_all;
+  int n_phi;
+  const double* coef;
+  const int32_t* form;
+  unsigned* bar;          // grid barrier arrivals (zeroed before launch)
+  unsigned long long* dbg;  // diagnostics (QAA_OPT_DIAG bit 16 via the tm_diag stats), or nullptr
+};
+cudaError_t launch_warp_energy(const uint8_t* E, uint8_t* Eg, const WarpGeo& g, int L, int num_sms, cudaStream_t st);
+cudaError_t launch_warp_evolve(const WarpEvolveArgs& a, int grid, int warps, cudaStream_t st);
 // 10 <= L <= 12: register-phase variant (2-3x faster than the per-qubit loop)
 cudaError_t launch_resident_phases(const ResidentArgs& a, cudaStream_t st);
 

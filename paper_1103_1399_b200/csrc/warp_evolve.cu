@@ -1,0 +1,251 @@
+// warp_evolve.cu -- all K Trotter steps of a 13..21-qubit state in ONE cooperative
+// launch with WARP-sized tiles (SURVEY §7 hard part 5; the
+// paper's regime of small instances; VERDICT r01 "persistent evolve for 13 <= n <= 21").
+//
+// The state (1..32 MiB) stays in L2. A pass of the cyclic step-spanning plan
+// (plan.cpp build_pass_schedule, step_spanning 1: K(P-1)+1 passes) runs over tiles
+// of 2^9 amplitudes, ONE WARP per tile (16 amplitudes per lane), so a tile's
+// program needs no block barrier and is short; passes are separated by a grid
+// barrier. Tile groups (WarpGeo): group 0 = physical bits 0..8; group g >= 1 =
+// bits {0, 1} (64-byte rows, not rotated) + the next <= 7 bits, filled up with
+// more low bits (not rotated) when fewer remain. L = 16: 2 groups, one pass per
+// step; 17 <= L <= 23: 3 groups, two passes per step.
+// Per tile: load in pattern PL (lane = tile bits 0..4, registers = 5..8; coalesced),
+// rotate 5..8, warp-local shared-memory exchange to PX (registers = 0..3, lane =
+// 4..8), rotate 0..3 and tile bit 4 (lane bit 0, shuffle), D with the group's
+// energy slice packed in PX order (one 16-byte load per lane), the post rotations
+// in reverse order, exchange back to PL, store.
+// State loads bypass L1 (ld.global.cg): other SMs wrote the data in the previous pass.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pass_common.cuh"
+
+namespace qaa {
+namespace {
+
+using namespace pc;
+
+constexpr int WE_WARPS = 8;
+constexpr int WE_BUF = 512 + 32;  // per-warp exchange buffer (amplitudes), padded l + (l >> 4)
+
+template <int FORM>
+__device__ __forceinline__ void we_pair(double2& a, double2& b, double c) {
+  double2 na, nb;
+  if (FORM == 0) {
+    na = make_double2(fma(-c, b.y, a.x), fma(c, b.x, a.y));
+    nb = make_double2(fma(-c, a.y, b.x), fma(c, a.x, b.y));
+  } else {
+    na = make_double2(fma(c, a.x, -b.y), fma(c, a.y, b.x));
+    nb = make_double2(fma(c, b.x, -a.y), fma(c, b.y, a.x));
+  }
+  a = na;
+  b = nb;
+}
+// rotate the register bits i (0..3) selected by mask
+template <int FORM>
+__device__ __forceinline__ void we_regs(double2 (&v)[16], uint32_t mask, double c) {
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+    if ((mask >> i) & 1)
+#pragma unroll
+      for (int r = 0; r < 16; r++)
+        if (!(r & (1 << i))) we_pair<FORM>(v[r], v[r | (1 << i)], c);
+}
+// rotate lane bit 0: each lane updates its own element from its partner's,
+// own' = own + i c partner (tangent) or c own + i partner (cot) -- the same
+// formula on both sides of the pair
+template <int FORM>
+__device__ __forceinline__ void we_lane0(double2 (&v)[16], double c) {
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    const double px = __shfl_xor_sync(0xffffffffu, v[r].x, 1);
+    const double py = __shfl_xor_sync(0xffffffffu, v[r].y, 1);
+    v[r] = FORM == 0 ? make_double2(fma(-c, py, v[r].x), fma(c, px, v[r].y))
+                     : make_double2(fma(c, v[r].x, -py), fma(c, v[r].y, px));
+  }
+}
+__device__ __forceinline__ void we_rot(double2 (&v)[16], uint32_t rot, double c, int form, bool pl) {
+  if (pl) {
+    if (form == 0) we_regs<0>(v, (rot >> 5) & 15, c);
+    else we_regs<1>(v, (rot >> 5) & 15, c);
+  } else {
+    if (form == 0) {
+      we_regs<0>(v, rot & 15, c);
+      if ((rot >> 4) & 1) we_lane0<0>(v, c);
+    } else {
+      we_regs<1>(v, rot & 15, c);
+      if ((rot >> 4) & 1) we_lane0<1>(v, c);
+    }
+  }
+}
+// PL (l = lane | r << 5) <-> PX (l = r | lane << 4) through the warp's padded buffer
+template <bool TO_PX>
+__device__ __forceinline__ void we_xchg(double2* xb, double2 (&v)[16], int lane) {
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    const int l = TO_PX ? (lane | (r << 5)) : (r | (lane << 4));
+    xb[l + (l >> 4)] = v[r];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    const int l = TO_PX ? (r | (lane << 4)) : (lane | (r << 5));
+    v[r] = xb[l + (l >> 4)];
+  }
+}
+__device__ __forceinline__ double2 ldcg2(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    for (;;) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (v >= target) break;
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(WE_WARPS * 32, 1) qaa_warp_evolve(const WarpEvolveArgs a) {
+  const int nw = blockDim.x >> 5;  // warps per CTA (<= WE_WARPS)
+  extern __shared__ __align__(16) double2 xbuf[];  // WE_WARPS x WE_BUF
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2* xb = xbuf + warp * WE_BUF;
+  const int64_t ntiles = (int64_t)1 << (a.L - 9);
+  const int64_t nwarps = (int64_t)gridDim.x * nw;
+  const int64_t wid = (int64_t)warp * gridDim.x + blockIdx.x;  // consecutive tiles on different SMs
+  // pass records carry their coefficients (host-packed): one 32-byte load per pass,
+  // the next one issued before the grid barrier so its latency hides behind it
+  WarpPass nx = a.plan[0];
+  for (int64_t p = 0; p < a.npass; p++) {
+    const WarpPass ps = nx;
+    if (p + 1 < a.npass) nx = a.plan[p + 1];
+    const WarpGeo& g = a.geo[ps.group];
+    // per-thread offsets of the load/store pattern PL: lane part + 4 register strides
+    int64_t thrL = 0, sL[4];
+#pragma unroll
+    for (int b = 0; b < 5; b++)
+      if ((lane >> b) & 1) thrL += (int64_t)1 << g.phys[b];
+#pragma unroll
+    for (int i = 0; i < 4; i++) sL[i] = (int64_t)1 << g.phys[5 + i];
+    const bool pre = ps.flags & WP_PRE, d = ps.flags & WP_D, post = ps.flags & WP_POST;
+    const int fpre = (ps.flags >> 3) & 1, fpost = (ps.flags >> 4) & 1;
+    const double2* phi = a.phi_all + ps.d * a.n_phi;
+    const uint8_t* Eg = a.Eg[ps.group];
+    const uint32_t rot = g.rot;
+    long long tt0 = clock64(), tt1 = 0, tt2 = 0, tt3 = 0;
+    for (int64_t T = wid; T < ntiles; T += nwarps) {
+      // tile base: the tile-id bits scattered to the group's free physical bits
+      int64_t base = 0;
+      for (int i = 0; i < g.nfree; i++)
+        if ((T >> i) & 1) base += (int64_t)1 << g.free_bits[i];
+      double2 v[16];
+      const double2* src = a.psi + base + thrL;
+#pragma unroll
+      for (int r = 0; r < 16; r++) {
+        int64_t o = 0;
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+          if ((r >> i) & 1) o += sL[i];
+        v[r] = ldcg2(src + o);
+      }
+      uint4 pk = make_uint4(0, 0, 0, 0);
+      if (d) pk = __ldg(reinterpret_cast<const uint4*>(Eg + (T << 9) + (lane << 4)));
+      if (a.dbg) {
+        double s0 = v[0].x + v[15].y;
+        tt1 = clock64() + (s0 == 12345.678 ? 1 : 0);
+      }
+      if (pre) we_rot(v, rot, ps.cpre, fpre, true);
+      we_xchg<true>(xb, v, lane);
+      double2 f[16];
+      if (d) {  // the D factors: loads issued before the PX rotations that precede their use
+#pragma unroll
+        for (int r = 0; r < 16; r++) {
+          const uint32_t w = r < 4 ? pk.x : (r < 8 ? pk.y : (r < 12 ? pk.z : pk.w));
+          f[r] = __ldg(phi + ((w >> (8 * (r & 3))) & 0xffu));
+        }
+      }
+      if (pre) we_rot(v, rot, ps.cpre, fpre, false);
+      if (d) {
+#pragma unroll
+        for (int r = 0; r < 16; r++) v[r] = cmul(f[r], v[r]);
+      }
+      if (post) we_rot(v, rot, ps.cpost, fpost, false);
+      we_xchg<false>(xb, v, lane);
+      if (post) we_rot(v, rot, ps.cpost, fpost, true);
+      if (a.dbg) {
+        double s0 = v[0].x + v[15].y;
+        tt2 = clock64() + (s0 == 12345.678 ? 1 : 0);
+      }
+      double2* dst = a.psi + base + thrL;
+#pragma unroll
+      for (int r = 0; r < 16; r++) {
+        int64_t o = 0;
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+          if ((r >> i) & 1) o += sL[i];
+        __stcg(dst + o, v[r]);
+      }
+    }
+    tt3 = clock64();
+    if (p + 1 < a.npass) grid_barrier(a.bar, (unsigned)(p + 1) * gridDim.x);
+    if (a.dbg && lane == 0 && warp == 0 && blockIdx.x < 2 && tt1) {
+      atomicAdd(&a.dbg[0], (unsigned long long)(tt1 - tt0));  // pass start -> tile loaded
+      atomicAdd(&a.dbg[1], (unsigned long long)(tt2 - tt1));  // compute
+      atomicAdd(&a.dbg[2], (unsigned long long)(tt3 - tt2));  // stores issued
+      atomicAdd(&a.dbg[3], (unsigned long long)(clock64() - tt3));  // barrier
+      atomicAdd(&a.dbg[4], 1ull);
+    }
+  }
+}
+
+// Eg[T * 512 + lane * 16 + r] = E[base(T) + tile-local index (r | lane << 4) scattered]
+__global__ void warp_energy_kernel(const uint8_t* E, uint8_t* Eg, WarpGeo g, int L) {
+  const int64_t n = (int64_t)1 << L;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t T = i >> 9;
+    const int l = (int)(i & 511);  // = lane * 16 + r, the PX local index r | lane << 4
+    int64_t x = 0;
+    for (int j = 0; j < g.nfree; j++)
+      if ((T >> j) & 1) x += (int64_t)1 << g.free_bits[j];
+    for (int b = 0; b < 9; b++)
+      if ((l >> b) & 1) x += (int64_t)1 << g.phys[b];
+    Eg[i] = E[x];
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_warp_energy(const uint8_t* E, uint8_t* Eg, const WarpGeo& g, int L, int num_sms, cudaStream_t st) {
+  warp_energy_kernel<<<num_sms * 4, 256, 0, st>>>(E, Eg, g, L);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_warp_evolve(const WarpEvolveArgs& a, int grid, int warps, cudaStream_t st) {
+  if (warps < 1 || warps > WE_WARPS) return cudaErrorInvalidValue;
+  const int smem = warps * WE_BUF * (int)sizeof(double2);
+  cudaError_t e = cudaFuncSetAttribute(qaa_warp_evolve, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(warps * 32);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, qaa_warp_evolve, a);
+}
+
+}  // namespace qaa

@@ -19,7 +19,7 @@ __all__ = [
     "qaa_init_basis", "qaa_evolve", "qaa_sweep", "qaa_time_energy_table", "qaa_set_driver", "qaa_spectrum", "qaa_success_prob", "qaa_energy", "qaa_norm2", "qaa_sigma_x",
     "qaa_num_solutions", "qaa_max_energy", "qaa_copy_state", "qaa_set_state", "qaa_copy_energy_table",
     "qaa_state_ptr", "qaa_set_option", "qaa_get_stats", "qaa_reset_stats", "qaa_plan_describe",
-    "qaa_version", "OPT_ROW_BITS", "OPT_PROFILE", "OPT_STEP_SPANNING", "OPT_CTAS_PER_SM", "OPT_KERNEL", "OPT_TMA_GROUPS", "OPT_SUPER", "OPT_ORDER", "OPT_ENERGY_W64", "OPT_SUPER_GRID", "OPT_SUPER_SPLIT", "OPT_SHARD_SYNC", "OPT_PERSIST", "OPT_DIAG", "OPT_CLUSTER",
+    "qaa_version", "OPT_ROW_BITS", "OPT_PROFILE", "OPT_STEP_SPANNING", "OPT_CTAS_PER_SM", "OPT_KERNEL", "OPT_TMA_GROUPS", "OPT_SUPER", "OPT_ORDER", "OPT_ENERGY_W64", "OPT_SUPER_GRID", "OPT_SUPER_SPLIT", "OPT_SHARD_SYNC", "OPT_PERSIST", "OPT_DIAG", "OPT_CLUSTER", "OPT_WARPTILE", "OPT_WARP_GRID",
     "PLAN_RECORD", "SHARD_RECORD", "TorchComm", "qaa_plan_describe_sharded",
 ]
 
@@ -37,6 +37,8 @@ OPT_SHARD_SYNC = 12
 OPT_PERSIST = 13
 OPT_DIAG = 14
 OPT_CLUSTER = 16
+OPT_WARPTILE = 17
+OPT_WARP_GRID = 18
 PLAN_RECORD = 10
 SHARD_RECORD = 10
 
@@ -118,7 +120,7 @@ class qaa_stats(ctypes.Structure):
                 ("kernel_launches_total", ctypes.c_int64), ("super_launches", ctypes.c_int64),
                 ("super_kernel_ms", ctypes.c_double), ("super_kernels_timed", ctypes.c_int64),
                 ("tm_launches", ctypes.c_int64), ("persist_launches", ctypes.c_int64), ("pw_launches", ctypes.c_int64),
-                ("tm_diag", ctypes.c_uint64 * 8), ("cluster_launches", ctypes.c_int64)]
+                ("tm_diag", ctypes.c_uint64 * 8), ("cluster_launches", ctypes.c_int64), ("warp_launches", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: (list(getattr(self, f)) if f == "tm_diag" else getattr(self, f)) for f, _ in self._fields_}

@@ -149,7 +149,10 @@ def test_pass_parity_small(q, ctx, orc, n, span, variant):
 def test_persist_parity(q, ctx, orc, n, span):
     """The persistent evolve (QAA_OPT_PERSIST = 1, for 13 <= n <= 21 with the
     automatic kernel choice): every pass of the plan in one cooperative launch
-    with grid barriers, against the oracle; and the per-pass launches (default)."""
+    with grid barriers, against the oracle (the single-launch engines that take
+    precedence at n <= 16 are switched off here)."""
+    ctx.set_option(q.OPT_WARPTILE, 0)
+    ctx.set_option(q.OPT_CLUSTER, 0)
     ctx.set_option(q.OPT_PERSIST, 1)
     cl = instance(n)
     psi0 = cnf.random_state(n, 200 + n)
@@ -212,6 +215,7 @@ def test_cluster_evolve_parity(q, ctx, orc, n, K):
     """13 <= n <= 16: the whole evolution in ONE launch, state resident in the
     registers of a 2^(n-12)-CTA cluster (cluster bits swapped with local bits over
     DSMEM every step) -- against the oracle from a random state, random schedule."""
+    ctx.set_option(q.OPT_WARPTILE, 0)
     cl = instance(n)
     psi0 = cnf.random_state(n, 40 + n)
     sched = np.random.default_rng(n * 10 + K).uniform(0, 1, K)
@@ -221,10 +225,14 @@ def test_cluster_evolve_parity(q, ctx, orc, n, K):
     assert st["cluster_launches"] == 1 and st["pass_launches"] == 1
 
 
-@pytest.mark.parametrize("n", [13, 16])
-def test_cluster_evolve_forms_and_orders(q, ctx, orc, n):
-    """The cluster-resident evolve with the cot form (|beta| > pi/4), Strang
-    splitting (closing half step after the last phase) and the driving term."""
+@pytest.mark.parametrize("n,engine", [(13, "cluster"), (16, "cluster"), (13, "warp"), (16, "warp"), (17, "warp"),
+                                      (21, "warp")])
+def test_small_engines_forms_and_orders(q, ctx, orc, n, engine):
+    """The single-launch small-state engines (cluster-resident, n <= 16; warp-tile
+    cooperative, n <= 21) with the cot form (|beta| > pi/4), Strang splitting
+    (closing half step after the last pass) and the driving term."""
+    ctx.set_option(q.OPT_WARPTILE, 2 if engine == "warp" else 0)
+    ctx.set_option(q.OPT_CLUSTER, 1 if engine == "cluster" else 0)
     cl = instance(n)
     E = orc.energy_table(n, cl)
     psi0 = cnf.random_state(n, 3)
@@ -241,7 +249,23 @@ def test_cluster_evolve_forms_and_orders(q, ctx, orc, n):
     ctx.set_state(psi0)
     ctx.evolve(1.9, 5, sched[:5])
     assert_close(ctx.state(), orc.evolve_driven(n, E, psi0, 1.9, 5, 0.7, -0.4, sched[:5]))
-    assert ctx.stats()["cluster_launches"] == 3
+    assert ctx.stats()["cluster_launches" if engine == "cluster" else "warp_launches"] == 3
+
+
+@pytest.mark.parametrize("n", [13, 14, 15, 16, 17, 18, 19, 20, 21])
+@pytest.mark.parametrize("K", [1, 2, 6])
+def test_warp_evolve_parity(q, ctx, orc, n, K):
+    """13 <= n <= 21: all passes of the cyclic plan in ONE cooperative launch, one
+    warp per 2^9-amplitude tile, grid barriers between passes -- against the
+    oracle from a random state, random schedule."""
+    ctx.set_option(q.OPT_WARPTILE, 2)  # n > 16: the engine's test range
+    cl = instance(n)
+    psi0 = cnf.random_state(n, 60 + n)
+    sched = np.random.default_rng(n * 7 + K).uniform(0, 1, K)
+    got, want, _ = run_both(q, ctx, orc, n, cl, 1.3 * K, K, schedule=sched, psi0=psi0)
+    assert_close(got, want)
+    st = ctx.stats()
+    assert st["warp_launches"] == 1 and st["pass_launches"] == 1
 
 
 def test_cluster_evolve_matches_pass_kernels(q, orc):
@@ -252,6 +276,7 @@ def test_cluster_evolve_matches_pass_kernels(q, orc):
     out = []
     for cflag in (1, 0):
         with q.Context(0) as c:
+            c.set_option(q.OPT_WARPTILE, 0)
             c.set_option(q.OPT_CLUSTER, cflag)
             c.load_instance(n, cl)
             c.init_uniform()

@@ -26,10 +26,12 @@ def inst(n):
 
 
 for n in (8, 12, 13, 14, 15, 16, 18, 20, 21, 22):
-    modes = [("cluster", 1, 0), ("persist", 0, 1), ("passes", 0, 0)] if 13 <= n <= 16 else \
-        ([("persist", 0, 1), ("passes", 0, 0)] if n <= 21 else [("passes", 0, 0)])
-    for name, cflag, persist in modes:
+    modes = [("warp", 2, 0, 0)] if 13 <= n <= 21 else []
+    modes += [("cluster", 0, 1, 0)] if 13 <= n <= 16 else []
+    modes += [("persist", 0, 0, 1), ("passes", 0, 0, 0)] if 13 <= n <= 21 else [("default", 1, 1, 0)]
+    for name, wflag, cflag, persist in modes:
         with q.Context(0, stream=stream.cuda_stream) as c:
+            c.set_option(q.OPT_WARPTILE, wflag)
             c.set_option(q.OPT_CLUSTER, cflag)
             c.set_option(q.OPT_PERSIST, persist)
             c.load_instance(n, inst(n))
@@ -44,7 +46,8 @@ for n in (8, 12, 13, 14, 15, 16, 18, 20, 21, 22):
             ms = e0.elapsed_time(e1)
             st = c.stats()
         print(json.dumps({"n": n, "mode": name, "K": K, "us_per_step": ms * 1e3 / K, "steps_per_s": K / (ms / 1e3),
-                          "cluster_launches": st["cluster_launches"], "persist_launches": st["persist_launches"],
+                          "warp_launches": st["warp_launches"], "cluster_launches": st["cluster_launches"],
+                          "persist_launches": st["persist_launches"],
                           "pass_launches": st["pass_launches"]}), flush=True)
 # F1 sweep: 16 replicas, T = 1..200 at dt = 0.05 (configs[1]'s sweep style)
 Ts = np.array([1, 2, 5, 10, 20, 50, 100, 200, 3, 7, 15, 30, 70, 150, 40, 60], dtype=float)
