@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(CE_THREADS, 1) qaa_cluster_evolve(const Cluste
     const int l = t | (r << 8);
     v[r] = a.psi ? a.psi[((int64_t)q << 12) | l] : make_double2(a.amp0, 0.0);
   }
-  __syncthreads();
+  cl.sync();  // every CTA of the cluster is running before any DSMEM store reaches it
   int layout = 0;
   double2* cur = buf0;
   double2* nxt = buf1;

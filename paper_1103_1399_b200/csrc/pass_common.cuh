@@ -48,8 +48,26 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Wait bounds are in TIME (%globaltimer, checked every 4096 polls), not poll
+// counts, so slow tool runs (compute-sanitizer racecheck serialises warps) do not
+// trip them: a wait longer than WAIT_LIMIT_NS is a lost arrival -> trap (launch
+// error) instead of a hang.
+constexpr unsigned long long WAIT_LIMIT_NS = 60ull * 1000000000ull;
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// call with the poll count; traps once the wait started >= WAIT_LIMIT_NS ago
+__device__ __forceinline__ void wait_bound(uint32_t it, unsigned long long& t0) {
+  if ((it & 4095u) != 4095u) return;
+  const unsigned long long now = globaltimer_ns();
+  if (t0 == 0) t0 = now;
+  else if (now - t0 > WAIT_LIMIT_NS) __trap();
+}
 // bounded wait: a lost arrival becomes a trap (launch error) instead of a hang
 __device__ __forceinline__ void mbar_wait_bounded(uint64_t* b, uint32_t parity) {
+  unsigned long long t0 = 0;
   for (uint32_t it = 0;; it++) {
     uint32_t ok;
     asm volatile(
@@ -60,7 +78,7 @@ __device__ __forceinline__ void mbar_wait_bounded(uint64_t* b, uint32_t parity) 
         : "r"(sa(b)), "r"(parity)
         : "memory");
     if (ok) return;
-    if (it > (1u << 26)) __trap();
+    wait_bound(it, t0);
   }
 }
 

@@ -392,9 +392,10 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
       publish();
       if (DIAG & 8) __trap();  // super_issue never defers in this variant
       if (gtid == 0) {
+        unsigned long long t0 = 0;
         for (uint32_t it = 0; ld_acquire(&a.done[m.c]) < chunk_done; it++) {
           __nanosleep(32);
-          if (it > (1u << 26)) __trap();
+          wait_bound(it, t0);
         }
         fence_async_global();
         load_gk<BD>(&kmap, a, m.T, xb, es, &late[g], pol_dead);
@@ -406,12 +407,13 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
       // issued chunk c - L (a throttle on the L2 live set, not a data dependency)
       if (gtid == 0) {
         const int L = 1 + (a.lag > 1 ? a.lag : 1);
+        unsigned long long t0 = 0;
         for (uint32_t it = 0;; it++) {
           unsigned nb;
           asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(nb) : "l"(&a.doneB[m.c - L]) : "memory");
           if (nb >= (1u << a.tpc_bits)) break;
           __nanosleep(64);
-          if (it > (1u << 26)) __trap();
+          wait_bound(it, t0);
         }
         mbar_expect_tx(&late[g], TILE * 16u);
         bulk_g2s_hint(xb, a.g0.psi + tbase(a.g0, m.T), TILE * 16u, &late[g], pol_dead);
@@ -489,9 +491,10 @@ __device__ __forceinline__ void pw_issue_b(const CUtensorMap* kmap, const SuperA
   const uint32_t T = pdep32(i, a.k_imask) | pdep32(c, a.k_cmask);
   const unsigned target = 1u << a.tpc_bits;
   const long long t0 = (a.tm_flags & 8) ? clock64() : 0;
+  unsigned long long tw = 0;
   for (uint32_t it = 0; ld_acquire(&a.done[c]) < target; it++) {
     __nanosleep(64);
-    if (it > (1u << 28)) __trap();
+    wait_bound(it, tw);
   }
   if (a.tm_flags & 8) atomicAdd(&a.dbg[2], (unsigned long long)(clock64() - t0));
   fence_async_global();  // generic-proxy stores of chunk c -> this async-proxy read
