@@ -375,7 +375,9 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
     const int s = (int)(J % TMA_SLOTS);
     // never block with an unpublished tile: the landed tile may wait on a load
     // whose issuer waits for this chunk (the refill order is not J order)
-    if (V2 && pend >= 0 && !mbar_test(&full[NG * s + g], (uint32_t)((J / period<NG>()) & 1))) publish();
+    // (warp-uniform decision: publish() contains a __syncwarp)
+    if (V2 && pend >= 0 && __any_sync(FULLM, !mbar_test(&full[NG * s + g], (uint32_t)((J / period<NG>()) & 1))))
+      publish();
     mbar_wait_bounded(&full[NG * s + g], (uint32_t)((J / period<NG>()) & 1));
     const SlotMeta m = meta[s];
     if (m.kind == SK_END) {
