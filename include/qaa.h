@@ -293,7 +293,9 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        a grid barrier between passes; takes precedence over
  *                        QAA_OPT_CLUSTER (measured 4.1-5.0 vs 5.3-8.3 us per step at
  *                        n = 13..16). 2: also for 17 <= n <= 21 (there slower than the
- *                        per-pass kernels; a test hook). 0: off.
+ *                        per-pass kernels; a test hook), and qaa_sweep on teams of
+ *                        warp-tile CTAs (n <= 21; at n = 13..16 no faster than the
+ *                        default cluster-resident sweep). 0: off.
  *  QAA_OPT_WARP_GRID     tuning hook for the warp-tile launch: ctas * 16 + warps per CTA
  *                        (1..8); 0 (default) = automatic.
  *  QAA_OPT_DIAG          timing diagnostics ONLY (results are wrong by design): the

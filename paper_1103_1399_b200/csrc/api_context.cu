@@ -87,6 +87,7 @@ void qaa_destroy(qaa_ctx* ctx) {
   if (ctx->d_persist) cudaFree(ctx->d_persist);
   for (int g = 0; g < 4; g++)
     if (ctx->Ewt[g]) cudaFree(ctx->Ewt[g]);
+  if (ctx->d_wsweep) cudaFree(ctx->d_wsweep);
   if (ctx->coef_done) cudaEventDestroy(ctx->coef_done);
   for (auto& p : ctx->ev_pool) {
     cudaEventDestroy(p.first);

@@ -249,7 +249,7 @@ static bool try_persist(qaa_ctx* ctx, const std::vector<PassPlan>& plan, const s
 // Warp-tile groups (warp_evolve.cu): group 0 = bits 0..8; group g >= 1 = bits
 // {0, 1} + fillers {2, ...} (not rotated) + the next <= 7 bits (rotated)
 int warp_group_count(int L) { return 1 + (L - 9 + 6) / 7; }
-static void build_warp_geo(int L, WarpGeo* out, int* ngroups) {
+void build_warp_geo(int L, WarpGeo* out, int* ngroups) {
   int ng = 0;
   WarpGeo g0;
   memset(&g0, 0, sizeof g0);
@@ -279,8 +279,7 @@ static void build_warp_geo(int L, WarpGeo* out, int* ngroups) {
   *ngroups = ng;
 }
 
-static qaa_status run_warp_evolve(qaa_ctx* ctx, const WarpPass* dplan, int64_t npass, const double2* dphi,
-                                  const double* dcoef, const int32_t* dform, int n_phi) {
+qaa_status ensure_warp_tables(qaa_ctx* ctx) {
   if (!ctx->wt_built) {
     build_warp_geo(ctx->L, ctx->wgeo, &ctx->wt_groups);
     for (int g = 0; g < ctx->wt_groups; g++) {
@@ -292,8 +291,15 @@ static qaa_status run_warp_evolve(qaa_ctx* ctx, const WarpPass* dplan, int64_t n
     }
     ctx->wt_built = true;
   }
+  return QAA_OK;
+}
+
+static qaa_status run_warp_evolve(qaa_ctx* ctx, const WarpPass* dplan, int64_t npass, const double2* dphi,
+                                  const double* dcoef, const int32_t* dform, int n_phi) {
   {
-    qaa_status st = ensure_buffer(ctx, &ctx->d_persist, &ctx->d_persist_cap, 256);
+    qaa_status st = ensure_warp_tables(ctx);
+    if (st) return st;
+    st = ensure_buffer(ctx, &ctx->d_persist, &ctx->d_persist_cap, 256);
     if (st) return st;
   }
   WarpEvolveArgs wa;
@@ -311,13 +317,6 @@ static qaa_status run_warp_evolve(qaa_ctx* ctx, const WarpPass* dplan, int64_t n
   wa.coef = dcoef;
   wa.form = dform;
   wa.bar = (unsigned*)ctx->d_persist;
-  if (ctx->super_tm_flags & 8) {  // QAA_OPT_SUPER bit 10: phase cycle counters into tm_diag
-    if (!ctx->d_tm_diag) {
-      CUDA_TRY(cudaMalloc(&ctx->d_tm_diag, 8 * sizeof(unsigned long long)));
-      CUDA_TRY(cudaMemsetAsync(ctx->d_tm_diag, 0, 8 * sizeof(unsigned long long), ctx->stream));
-    }
-    wa.dbg = ctx->d_tm_diag;
-  }
   CUDA_TRY(cudaMemsetAsync(ctx->d_persist, 0, 16, ctx->stream));
   size_t ev = ctx->ev_used;
   if (ctx->profile) {

@@ -78,7 +78,9 @@ qaa_status qaa_time_energy_table(qaa_ctx* ctx, int reps, double* ms) {
 qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, double* out) {
   CHECK_CTX();
   if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "sweep before load_instance");
-  if (ctx->world != 1 || ctx->L > SWEEP_MAX_L)
+  const bool wide = ctx->warptile == 2 && ctx->L <= WARP_MAX_L &&
+                    (((int64_t)1 << (ctx->L - 9)) + 7) / 8 <= ctx->num_sms;  // warp-tile teams (test hook)
+  if (ctx->world != 1 || (ctx->L > SWEEP_MAX_L && !wide))
     return fail(ctx, QAA_E_USAGE, "sweep needs world = 1 and n <= %d (state resident in one CTA or cluster)",
                 SWEEP_MAX_L);
   if (nrep < 1 || !T || !K || !out) return fail(ctx, QAA_E_USAGE, "sweep needs nrep >= 1 and non-NULL arrays");
@@ -154,7 +156,78 @@ qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, 
   a.final_d = ctx->order == 2 ? 1 : 0;
   double* dout = (double*)(db + ((used + 15) & ~(size_t)15));
   a.out = dout;
-  if (ctx->cluster_evolve && ctx->L >= 13 && ctx->L <= 16) {
+  const int wteam = ctx->L >= WARP_MIN_L ? (int)((((int64_t)1 << (ctx->L - 9)) + 7) / 8) : 0;
+  if (ctx->warptile == 2 && ctx->L >= WARP_MIN_L && ctx->L <= WARP_MAX_L && wteam <= ctx->num_sms) {
+    // teams of warp-tile CTAs, one replica at a time per team (warp_evolve.cu
+    // qaa_warp_sweep; QAA_OPT_WARPTILE 2: measured no faster than the clusters below
+    // at n = 13..16 -- a replica's team shares each SM among 8 tiles -- and it
+    // extends the sweep to n <= 21)
+    qaa_status st = ensure_warp_tables(ctx);
+    if (st) return st;
+    const int P = warp_group_count(ctx->L);
+    const int nteams = std::min(nrep, ctx->num_sms / wteam);
+    std::vector<WarpPass> recs;
+    std::vector<int64_t> poff((size_t)nrep), plen((size_t)nrep);
+    std::vector<PassPlan> plan;
+    for (int i = 0; i < nrep; i++) {
+      build_pass_schedule(P, hK[i], 1, &plan);
+      if (ctx->order == 2) plan.back().d_step = hK[i];
+      poff[(size_t)i] = (int64_t)recs.size();
+      plen[(size_t)i] = (int64_t)plan.size();
+      for (const PassPlan& pp : plan) {
+        WarpPass w{pp.group, 0, 0, 0.0, 0.0};
+        if (pp.pre_step >= 0) {
+          w.flags |= WP_PRE | (hform[hoff[i] + pp.pre_step] ? 8 : 0);
+          w.cpre = hcoef[hoff[i] + pp.pre_step];
+        }
+        if (pp.d_step >= 0) {
+          w.flags |= WP_D;
+          w.d = hoff[i] + pp.d_step;
+        }
+        if (pp.post_step >= 0) {
+          w.flags |= WP_POST | (hform[hoff[i] + pp.post_step] ? 16 : 0);
+          w.cpost = hcoef[hoff[i] + pp.post_step];
+        }
+        recs.push_back(w);
+      }
+    }
+    const size_t rec_b = recs.size() * sizeof(WarpPass), arr_b = (size_t)nrep * sizeof(int64_t);
+    const size_t state_b = (size_t)nteams << ctx->L << 4;
+    const size_t part_b = (size_t)nteams * wteam * 8 * sizeof(double), bar_b = (size_t)nteams * 128;
+    const size_t o_off = (rec_b + 255) & ~(size_t)255, o_len = o_off + ((arr_b + 255) & ~(size_t)255),
+                 o_state = o_len + ((arr_b + 255) & ~(size_t)255), o_part = o_state + state_b,
+                 o_bar = o_part + ((part_b + 255) & ~(size_t)255), need = o_bar + bar_b;
+    st = ensure_buffer(ctx, &ctx->d_wsweep, &ctx->d_wsweep_cap, need);
+    if (st) return st;
+    char* wb = (char*)ctx->d_wsweep;
+    CUDA_TRY(cudaMemcpyAsync(wb, recs.data(), rec_b, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(wb + o_off, poff.data(), arr_b, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(wb + o_len, plen.data(), arr_b, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(wb + o_bar, 0, bar_b, ctx->stream));
+    WarpSweepArgs wa;
+    memset(&wa, 0, sizeof wa);
+    wa.L = ctx->L;
+    wa.amp0 = a.amp0;
+    for (int g = 0; g < ctx->wt_groups; g++) {
+      wa.geo[g] = ctx->wgeo[g];
+      wa.Eg[g] = ctx->Ewt[g];
+    }
+    wa.plan = (const WarpPass*)wb;
+    wa.plan_off = (const int64_t*)(wb + o_off);
+    wa.plan_len = (const int64_t*)(wb + o_len);
+    wa.nrep = nrep;
+    wa.phi_all = a.phi_all;
+    wa.n_phi = n_phi;
+    wa.team = wteam;
+    wa.scratch = (double2*)(wb + o_state);
+    wa.partial = (double*)(wb + o_part);
+    wa.bar = (unsigned*)(wb + o_bar);
+    wa.out = dout;
+    CUDA_TRY(launch_warp_sweep(wa, nteams * wteam, ctx->stream));
+    ctx->stats.warp_launches++;
+    // the host vectors above must outlive the async copies
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  } else if (ctx->cluster_evolve && ctx->L >= 13 && ctx->L <= 16) {
     // one register-resident cluster of 2^(n-12) CTAs per replica (cluster_evolve.cu)
     ClusterArgs ca;
     memset(&ca, 0, sizeof ca);

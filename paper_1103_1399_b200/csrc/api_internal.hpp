@@ -44,6 +44,8 @@ static_assert(sizeof(ClauseRecHost) == 32, "clause record layout");
 constexpr int WARP_MIN_L = 13, WARP_MAX_L = 21;  // warp_evolve.cu range (QAA_OPT_WARPTILE 2)
 constexpr int WARP_AUTO_MAX_L = 16;               // default range: faster than the per-pass kernels up to here
 int warp_group_count(int L);
+struct qaa_ctx;
+qaa_status ensure_warp_tables(qaa_ctx* ctx);  // warp-tile geometry + per-group energy tables
 
 struct qaa_ctx {
   int device = 0;
@@ -115,6 +117,8 @@ struct qaa_ctx {
   int wt_groups = 0;
   WarpGeo wgeo[4];
   uint8_t* Ewt[4] = {nullptr, nullptr, nullptr, nullptr};
+  void* d_wsweep = nullptr;  // warp-tile sweep: plans, offsets, team states, partials, barriers
+  size_t d_wsweep_cap = 0;
   int super_v2 = 1;  // split-phase WAR guards + deferred publish (QAA_OPT_SUPER bit 15 clears it)
   int super_grid = 0;  // 0: one CTA per SM
   int super_split = 0;

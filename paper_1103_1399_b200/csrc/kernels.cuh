@@ -239,8 +239,26 @@ struct WarpEvolveArgs {
   const double* coef;
   const int32_t* form;
   unsigned* bar;          // grid barrier arrivals (zeroed before launch)
-  unsigned long long* dbg;  // diagnostics (QAA_OPT_DIAG bit 16 via the tm_diag stats), or nullptr
 };
+// F1 sweep on warp tiles: teams of `team` CTAs, one replica at a time per team
+struct WarpSweepArgs {
+  int L;
+  double amp0;             // 2^{-n/2}
+  WarpGeo geo[4];
+  const uint8_t* Eg[4];
+  const WarpPass* plan;    // all replicas' pass records
+  const int64_t* plan_off; // [nrep] first record of replica r
+  const int64_t* plan_len; // [nrep]
+  int nrep;
+  const double2* phi_all;
+  int n_phi;
+  int team;                // CTAs per team (grid = nteams * team)
+  double2* scratch;        // nteams states of 2^L amplitudes
+  double* partial;         // nteams * team * 8 per-warp partial sums
+  unsigned* bar;           // nteams barrier counters, 128 bytes apart (zeroed)
+  double* out;             // [nrep] P_succ
+};
+cudaError_t launch_warp_sweep(const WarpSweepArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_warp_energy(const uint8_t* E, uint8_t* Eg, const WarpGeo& g, int L, int num_sms, cudaStream_t st);
 cudaError_t launch_warp_evolve(const WarpEvolveArgs& a, int grid, int warps, cudaStream_t st);
 // 10 <= L <= 12: register-phase variant (2-3x faster than the per-qubit loop)

@@ -115,6 +115,69 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
   __syncthreads();
 }
 
+// One pass of the plan over the tiles T = wid, wid + nwarps, ... < ntiles of the
+// state psi (the tile program of the header comment).
+__device__ __forceinline__ void we_pass(const WarpGeo& g, const WarpPass& ps, double2* psi, const uint8_t* Eg,
+                                        const double2* phi_all, int n_phi, int64_t wid, int64_t nwarps,
+                                        int64_t ntiles, int lane, double2* xb) {
+  // per-thread offsets of the load/store pattern PL: lane part + 4 register strides
+  int64_t thrL = 0, sL[4];
+#pragma unroll
+  for (int b = 0; b < 5; b++)
+    if ((lane >> b) & 1) thrL += (int64_t)1 << g.phys[b];
+#pragma unroll
+  for (int i = 0; i < 4; i++) sL[i] = (int64_t)1 << g.phys[5 + i];
+  const bool pre = ps.flags & WP_PRE, d = ps.flags & WP_D, post = ps.flags & WP_POST;
+  const int fpre = (ps.flags >> 3) & 1, fpost = (ps.flags >> 4) & 1;
+  const double2* phi = phi_all + ps.d * n_phi;
+  const uint32_t rot = g.rot;
+  for (int64_t T = wid; T < ntiles; T += nwarps) {
+    // tile base: the tile-id bits scattered to the group's free physical bits
+    int64_t base = 0;
+    for (int i = 0; i < g.nfree; i++)
+      if ((T >> i) & 1) base += (int64_t)1 << g.free_bits[i];
+    double2 v[16];
+    const double2* src = psi + base + thrL;
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      int64_t o = 0;
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+        if ((r >> i) & 1) o += sL[i];
+      v[r] = ldcg2(src + o);
+    }
+    uint4 pk = make_uint4(0, 0, 0, 0);
+    if (d) pk = __ldg(reinterpret_cast<const uint4*>(Eg + (T << 9) + (lane << 4)));
+    if (pre) we_rot(v, rot, ps.cpre, fpre, true);
+    we_xchg<true>(xb, v, lane);
+    double2 f[16];
+    if (d) {  // the D factors: loads issued before the PX rotations that precede their use
+#pragma unroll
+      for (int r = 0; r < 16; r++) {
+        const uint32_t w = r < 4 ? pk.x : (r < 8 ? pk.y : (r < 12 ? pk.z : pk.w));
+        f[r] = __ldg(phi + ((w >> (8 * (r & 3))) & 0xffu));
+      }
+    }
+    if (pre) we_rot(v, rot, ps.cpre, fpre, false);
+    if (d) {
+#pragma unroll
+      for (int r = 0; r < 16; r++) v[r] = cmul(f[r], v[r]);
+    }
+    if (post) we_rot(v, rot, ps.cpost, fpost, false);
+    we_xchg<false>(xb, v, lane);
+    if (post) we_rot(v, rot, ps.cpost, fpost, true);
+    double2* dst = psi + base + thrL;
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      int64_t o = 0;
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+        if ((r >> i) & 1) o += sL[i];
+      __stcg(dst + o, v[r]);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(WE_WARPS * 32, 1) qaa_warp_evolve(const WarpEvolveArgs a) {
   const int nw = blockDim.x >> 5;  // warps per CTA (<= WE_WARPS)
   extern __shared__ __align__(16) double2 xbuf[];  // WE_WARPS x WE_BUF
@@ -129,82 +192,71 @@ __global__ void __launch_bounds__(WE_WARPS * 32, 1) qaa_warp_evolve(const WarpEv
   for (int64_t p = 0; p < a.npass; p++) {
     const WarpPass ps = nx;
     if (p + 1 < a.npass) nx = a.plan[p + 1];
-    const WarpGeo& g = a.geo[ps.group];
-    // per-thread offsets of the load/store pattern PL: lane part + 4 register strides
-    int64_t thrL = 0, sL[4];
-#pragma unroll
-    for (int b = 0; b < 5; b++)
-      if ((lane >> b) & 1) thrL += (int64_t)1 << g.phys[b];
-#pragma unroll
-    for (int i = 0; i < 4; i++) sL[i] = (int64_t)1 << g.phys[5 + i];
-    const bool pre = ps.flags & WP_PRE, d = ps.flags & WP_D, post = ps.flags & WP_POST;
-    const int fpre = (ps.flags >> 3) & 1, fpost = (ps.flags >> 4) & 1;
-    const double2* phi = a.phi_all + ps.d * a.n_phi;
-    const uint8_t* Eg = a.Eg[ps.group];
-    const uint32_t rot = g.rot;
-    long long tt0 = clock64(), tt1 = 0, tt2 = 0, tt3 = 0;
+    we_pass(a.geo[ps.group], ps, a.psi, a.Eg[ps.group], a.phi_all, a.n_phi, wid, nwarps, ntiles, lane, xb);
+    if (p + 1 < a.npass) grid_barrier(a.bar, (unsigned)(p + 1) * gridDim.x);
+  }
+}
+
+// F1 sweep on warp tiles: the grid is split into teams of `team` CTAs; team j
+// evolves replicas j, j + nteams, ... (longest first, host order) from the
+// uniform state in its own state buffer, with a team-wide barrier (its own
+// monotone counter) between passes, and leaves P_succ = sum_{E = 0} |psi|^2 of
+// each replica in out[] (fixed-order reduction: lanes, then warps in id order).
+__global__ void __launch_bounds__(WE_WARPS * 32, 1) qaa_warp_sweep(const WarpSweepArgs a) {
+  const int nw = blockDim.x >> 5;
+  extern __shared__ __align__(16) double2 xbuf[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2* xb = xbuf + warp * WE_BUF;
+  const int team = a.team, nteams = gridDim.x / team;
+  const int j = blockIdx.x / team, lc = blockIdx.x % team;
+  if (j >= nteams) return;
+  const int64_t ntiles = (int64_t)1 << (a.L - 9);
+  const int64_t nwarps = (int64_t)team * nw;
+  const int64_t wid = (int64_t)warp * team + lc;
+  double2* psi = a.scratch + ((int64_t)j << a.L);
+  double* part = a.partial + (int64_t)j * nwarps;  // per warp of the team
+  unsigned* ctr = a.bar + 32 * j;                    // one 128-byte line per team
+  unsigned epoch = 0;
+  const int64_t N = (int64_t)1 << a.L;
+  for (int rep = j; rep < a.nrep; rep += nteams) {
+    // uniform start, every team warp on its slice
+    for (int64_t i = (wid << 5) + lane; i < N; i += nwarps << 5) __stcg(psi + i, make_double2(a.amp0, 0.0));
+    grid_barrier(ctr, ++epoch * (unsigned)team);
+    const WarpPass* plan = a.plan + a.plan_off[rep];
+    const int64_t np = a.plan_len[rep];
+    for (int64_t p = 0; p < np; p++) {
+      const WarpPass ps = plan[p];
+      we_pass(a.geo[ps.group], ps, psi, a.Eg[ps.group], a.phi_all, a.n_phi, wid, nwarps, ntiles, lane, xb);
+      grid_barrier(ctr, ++epoch * (unsigned)team);
+    }
+    // P_succ: this warp's tiles of group 0 (PX order matches Eg[0])
+    double acc = 0.0;
+    const WarpGeo& g0 = a.geo[0];
     for (int64_t T = wid; T < ntiles; T += nwarps) {
-      // tile base: the tile-id bits scattered to the group's free physical bits
       int64_t base = 0;
-      for (int i = 0; i < g.nfree; i++)
-        if ((T >> i) & 1) base += (int64_t)1 << g.free_bits[i];
-      double2 v[16];
-      const double2* src = a.psi + base + thrL;
+      for (int i = 0; i < g0.nfree; i++)
+        if ((T >> i) & 1) base += (int64_t)1 << g0.free_bits[i];
+      const uint4 pk = __ldg(reinterpret_cast<const uint4*>(a.Eg[0] + (T << 9) + (lane << 4)));
 #pragma unroll
       for (int r = 0; r < 16; r++) {
-        int64_t o = 0;
-#pragma unroll
-        for (int i = 0; i < 4; i++)
-          if ((r >> i) & 1) o += sL[i];
-        v[r] = ldcg2(src + o);
-      }
-      uint4 pk = make_uint4(0, 0, 0, 0);
-      if (d) pk = __ldg(reinterpret_cast<const uint4*>(Eg + (T << 9) + (lane << 4)));
-      if (a.dbg) {
-        double s0 = v[0].x + v[15].y;
-        tt1 = clock64() + (s0 == 12345.678 ? 1 : 0);
-      }
-      if (pre) we_rot(v, rot, ps.cpre, fpre, true);
-      we_xchg<true>(xb, v, lane);
-      double2 f[16];
-      if (d) {  // the D factors: loads issued before the PX rotations that precede their use
-#pragma unroll
-        for (int r = 0; r < 16; r++) {
-          const uint32_t w = r < 4 ? pk.x : (r < 8 ? pk.y : (r < 12 ? pk.z : pk.w));
-          f[r] = __ldg(phi + ((w >> (8 * (r & 3))) & 0xffu));
+        const uint32_t w = r < 4 ? pk.x : (r < 8 ? pk.y : (r < 12 ? pk.z : pk.w));
+        if (((w >> (8 * (r & 3))) & 0xffu) == 0) {
+          const int l = r | (lane << 4);  // group 0: tile bit b = physical bit b
+          const double2 v = ldcg2(psi + base + l);
+          acc += fma(v.x, v.x, v.y * v.y);
         }
       }
-      if (pre) we_rot(v, rot, ps.cpre, fpre, false);
-      if (d) {
-#pragma unroll
-        for (int r = 0; r < 16; r++) v[r] = cmul(f[r], v[r]);
-      }
-      if (post) we_rot(v, rot, ps.cpost, fpost, false);
-      we_xchg<false>(xb, v, lane);
-      if (post) we_rot(v, rot, ps.cpost, fpost, true);
-      if (a.dbg) {
-        double s0 = v[0].x + v[15].y;
-        tt2 = clock64() + (s0 == 12345.678 ? 1 : 0);
-      }
-      double2* dst = a.psi + base + thrL;
-#pragma unroll
-      for (int r = 0; r < 16; r++) {
-        int64_t o = 0;
-#pragma unroll
-        for (int i = 0; i < 4; i++)
-          if ((r >> i) & 1) o += sL[i];
-        __stcg(dst + o, v[r]);
-      }
     }
-    tt3 = clock64();
-    if (p + 1 < a.npass) grid_barrier(a.bar, (unsigned)(p + 1) * gridDim.x);
-    if (a.dbg && lane == 0 && warp == 0 && blockIdx.x < 2 && tt1) {
-      atomicAdd(&a.dbg[0], (unsigned long long)(tt1 - tt0));  // pass start -> tile loaded
-      atomicAdd(&a.dbg[1], (unsigned long long)(tt2 - tt1));  // compute
-      atomicAdd(&a.dbg[2], (unsigned long long)(tt3 - tt2));  // stores issued
-      atomicAdd(&a.dbg[3], (unsigned long long)(clock64() - tt3));  // barrier
-      atomicAdd(&a.dbg[4], 1ull);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) part[wid] = acc;
+    grid_barrier(ctr, ++epoch * (unsigned)team);
+    if (lc == 0 && threadIdx.x == 0) {
+      double sum = 0.0;
+      for (int64_t w = 0; w < nwarps; w++) sum += __ldcg(part + w);  // other SMs wrote them: bypass L1
+      a.out[rep] = sum;
     }
+    grid_barrier(ctr, ++epoch * (unsigned)team);  // part[] and psi are reused by the next replica
   }
 }
 
@@ -246,6 +298,23 @@ cudaError_t launch_warp_evolve(const WarpEvolveArgs& a, int grid, int warps, cud
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, qaa_warp_evolve, a);
+}
+
+cudaError_t launch_warp_sweep(const WarpSweepArgs& a, int grid, cudaStream_t st) {
+  const int smem = WE_WARPS * WE_BUF * (int)sizeof(double2);
+  cudaError_t e = cudaFuncSetAttribute(qaa_warp_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(WE_WARPS * 32);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, qaa_warp_sweep, a);
 }
 
 }  // namespace qaa

@@ -414,6 +414,40 @@ def test_unsat_success_zero(q, ctx):
     assert ctx.success_prob() == 0.0
 
 
+@pytest.mark.parametrize("n,wt", [(14, 0), (16, 1), (16, 0)])
+def test_small_engines_edge_cases(q, ctx, orc, n, wt):
+    """The single-launch small-state engines (warp-tile: wt = 1, cluster-resident:
+    wt = 0) on the degenerate cases: T = 0 (identity, bit for bit), K = 1, m = 0
+    (E = 0, every assignment a solution), s = 1 (closed form 2^{-n/2} e^{-i T E}),
+    s = 0 from the uniform state (its H_B eigenvalue-0 state: unchanged)."""
+    ctx.set_option(q.OPT_WARPTILE, wt)
+    key = "warp_launches" if wt else "cluster_launches"
+    cl = instance(n)
+    E = orc.energy_table(n, cl)
+    ctx.load_instance(n, cl)
+    psi0 = cnf.random_state(n, 11)
+    ctx.set_state(psi0)
+    ctx.evolve(0.0, 3)
+    assert np.array_equal(ctx.state(), psi0)
+    ctx.set_state(psi0)
+    ctx.evolve(0.9, 1)
+    assert_close(ctx.state(), orc.evolve(n, E, psi0, 0.9, 1))
+    ctx.init_uniform()
+    ctx.evolve(0.41, 5, np.ones(5))
+    want = 2.0 ** (-n / 2) * np.exp(-1j * 0.41 * E.astype(float))
+    assert_close(ctx.state(), want, atol=1e-15, rtol_l2=1e-12)
+    ctx.init_uniform()
+    ctx.reset_stats()
+    ctx.evolve(3.0, 4, np.zeros(4))
+    assert_close(ctx.state(), orc.init_uniform(n), atol=1e-15, rtol_l2=1e-12)
+    assert ctx.stats()[key] == 1
+    ctx.load_instance(n, [])
+    ctx.set_state(psi0)
+    ctx.evolve(1.0, 3)
+    assert_close(ctx.state(), orc.evolve(n, orc.energy_table(n, []), psi0, 1.0, 3))
+    assert abs(ctx.success_prob() - ctx.norm2()) < 1e-13
+
+
 def test_T_zero_identity(q, ctx):
     for n in (9, 20):
         ctx.load_instance(n, instance(n))
@@ -617,18 +651,20 @@ def test_strang_parity(q, ctx, orc, n, span, kernel):
     ctx.set_option(q.OPT_ORDER, 1)
 
 
-@pytest.mark.parametrize("n,cluster", [(6, 1), (8, 1), (10, 1), (11, 1), (12, 1), (13, 1), (14, 1), (15, 1),
-                                       (16, 1), (13, 0), (14, 0), (15, 0), (16, 0)])
+@pytest.mark.parametrize("n,engine", [(6, "cluster"), (8, "cluster"), (10, "cluster"), (11, "cluster"), (12, "cluster")] +
+                         [(n, e) for n in (13, 14, 15, 16) for e in ("warp2", "cluster", "smem")] + [(18, "warp2")])
 @pytest.mark.parametrize("order", [1, 2])
-def test_sweep_parity(q, ctx, orc, n, cluster, order):
+def test_sweep_parity(q, ctx, orc, n, engine, order):
     """NEXT F1: batched T sweep (one CTA per replica up to n = 12 -- per-qubit
     loop below n = 10, 16-amplitude register phases from 10 --; for n = 13..16 one
     register-resident cluster of 2^(n-12) CTAs per replica (default), or with
     QAA_OPT_CLUSTER 0 the shared-memory cluster of 2^(n-13) CTAs with per-bit DSMEM
-    phases) against one oracle run per replica (configs[1]-style sweep T in
-    {1,2,5,10,20} at dt = 0.05)."""
+    phases, or with QAA_OPT_WARPTILE 2 teams of warp-tile CTAs, one replica per team
+    at a time -- also n = 18) against one oracle run per replica (configs[1]-style
+    sweep T in {1,2,5,10,20} at dt = 0.05)."""
     cl = cnf.paper_instance()[1] if n == 6 else instance(n)
-    ctx.set_option(q.OPT_CLUSTER, cluster)
+    ctx.set_option(q.OPT_WARPTILE, {"warp": 1, "warp2": 2}.get(engine, 0))
+    ctx.set_option(q.OPT_CLUSTER, 1 if engine == "cluster" else 0)
     ctx.set_option(q.OPT_ORDER, order)
     ctx.load_instance(n, cl)
     Ts = np.array([1.0, 2.0, 5.0, 10.0, 20.0])

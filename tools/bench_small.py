@@ -53,8 +53,9 @@ for n in (8, 12, 13, 14, 15, 16, 18, 20, 21, 22):
 Ts = np.array([1, 2, 5, 10, 20, 50, 100, 200, 3, 7, 15, 30, 70, 150, 40, 60], dtype=float)
 Ks = (Ts / 0.05).astype(np.int64)
 for n in (13, 14, 15, 16):
-    for name, cflag in (("cluster", 1), ("smem-cluster", 0)):
+    for name, wflag, cflag in (("warp-teams", 2, 0), ("cluster", 0, 1), ("smem-cluster", 0, 0)):
         with q.Context(0, stream=stream.cuda_stream) as c:
+            c.set_option(q.OPT_WARPTILE, wflag)
             c.set_option(q.OPT_CLUSTER, cflag)
             c.load_instance(n, inst(n))
             c.sweep(Ts[:2], Ks[:2])  # warm
