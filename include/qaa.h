@@ -259,7 +259,8 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        bits 7-10 and 13: its A/B switches and diagnostics counters
  *                        (SuperArgs.tm_flags; with the default kernel bit 7 = publish a
  *                        group-0 tile after the next landed read, bit 8 = right after its
- *                        stores); bits 11-12: chunk lag - 1 (default lag 1: two chunks
+ *                        stores, bit 9 = store each group-k tile with one TMA tensor store
+ *                        from shared memory -- bitwise equal, measured 2 % slower); bits 11-12: chunk lag - 1 (default lag 1: two chunks
  *                        live in L2; 2-3 measured slower); bit 14: producer-warp variant;
  *                        bit 15: the round-1 synchronisation (a group barrier before every
  *                        exchange write and before each group-0 tile's publish) instead of

@@ -193,7 +193,7 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       ctx->cluster_evolve = (int)value;
       return QAA_OK;
     case QAA_OPT_DIAG:
-      if (value < 0 || value > 15) return fail(ctx, QAA_E_USAGE, "diag must be in 0..15");
+      if (value < 0 || value > 127) return fail(ctx, QAA_E_USAGE, "diag must be in 0..127");
       ctx->diag = (int)value;
       return QAA_OK;
     case QAA_OPT_TMA_GROUPS:

@@ -183,6 +183,44 @@ __device__ __forceinline__ void tma_load_hint(void* dst, const CUtensorMap* map,
   }
 }
 
+// TMA tensor store of a tile from shared memory (bulk group of the issuing thread)
+__device__ __forceinline__ void tma_store_hint(const CUtensorMap* map, const int (&c)[5], int rank, const void* src,
+                                               uint64_t pol) {
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  switch (rank) {
+    case 2:
+      asm volatile(
+          "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(m),
+          "r"(c[0]), "r"(c[1]), "r"(sa(src)), "l"(pol)
+          : "memory");
+      break;
+    case 3:
+      asm volatile(
+          "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;" ::"l"(
+              m),
+          "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(sa(src)), "l"(pol)
+          : "memory");
+      break;
+    case 4:
+      asm volatile(
+          "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4}], [%5], %6;" ::"l"(
+              m),
+          "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(sa(src)), "l"(pol)
+          : "memory");
+      break;
+    default:
+      asm volatile(
+          "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4, %5}], [%6], "
+          "%7;" ::"l"(m),
+          "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(sa(src)), "l"(pol)
+          : "memory");
+      break;
+  }
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // L2 eviction-priority hints (createpolicy + .L2::cache_hint), used by the
 // L2-blocked step to keep the chunk data that is read again and stream out the rest
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -490,7 +528,10 @@ __device__ void super_issue(const CUtensorMap* kmap, const SuperArgs& a, int64_t
   if ((a.diag & 8) || ld_acquire(&a.done[c]) >= (1u << (a.tpc_bits + a.done_shift))) {
     fence_async_global();  // generic-proxy stores of chunk c -> this async-proxy read
     meta[s] = SlotMeta{SK_B, (int)c, T, 0};
-    load_gk<BD>(kmap, a, T, slots + (size_t)s * FAST_XBUF, eslots + (size_t)s * TILE, fb, pol_dead);
+    if (a.diag & 16)  // timing diagnostic: the group-k tile "lands" without a load
+      mbar_arrive_notx(fb);
+    else
+      load_gk<BD>(kmap, a, T, slots + (size_t)s * FAST_XBUF, eslots + (size_t)s * TILE, fb, pol_dead);
   } else {
     meta[s] = SlotMeta{SK_B_DEFERRED, (int)c, T, 0};
     mbar_arrive_notx(fb);

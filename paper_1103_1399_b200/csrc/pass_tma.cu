@@ -434,6 +434,33 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
       program<FP_G0_PRE, false, V2, DIAG>(a.g0, v, xb, nullptr, phis, lane, lw, g, war);
     }
     publish();  // the previous group-0 tile's stores have drained by now
+    // group-k tile stored by ONE TMA tensor store from the slot (tm_flags 4, v2):
+    // write-after-read guard, tile-local STS, proxy fence, group barrier; the
+    // storing thread refills the slot once the store has read it
+    const bool tstore = V2 && BD && isb && (a.tm_flags & 4) && !a.gk.contiguous && !(DIAG & 32);
+    if (tstore) {
+      war_arrive<true>(war);  // the final rotations consumed every value read from the slot
+      mbar_wait(war.bar, war.ph & 1);
+      war.ph++;
+      const int tl = pat_tl<PA>(lane, lw);
+#pragma unroll
+      for (int r = 0; r < RPT; r++) xb[tl | (r << reg_shift<PA>())] = v[r];
+      fence_async_shared();
+      group_bar(g);
+      if (gtid == 0) {
+        int cc[5];
+#pragma unroll
+        for (int d = 0; d < 5; d++) {
+          const int sg = a.gk.dim_seg[d];
+          cc[d] = sg < 0 ? 0 : (int)((m.T >> a.gk.seg_src[sg]) & ((1u << a.gk.seg_len[sg]) - 1));
+        }
+        tma_store_hint(&kmap, cc, a.gk.ndims, xb, pol_dead);
+        bulk_commit();
+        bulk_wait_read0();
+        super_issue<NG, BD>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
+      }
+      continue;
+    }
     __syncwarp();
     if (lane == 0 && last_warp_out(&cnt[s])) super_issue<NG, BD>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
     if (isb) {
@@ -445,15 +472,17 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
         double2* dst = a.peers[j] + (tb - (j << a.gshift) + ((int64_t)a.rank << a.gshift));
 #pragma unroll
         for (int r = 0; r < RPT; r++) dst[roff(psk, r)] = v[r];
-      } else {
+      } else if (!(DIAG & 32)) {
         double2* dst = a.gk.psi + tb;
 #pragma unroll
         for (int r = 0; r < RPT; r++) st_hint(dst + roff(psk, r), v[r], pol_dead);
       }
     } else {
       double2* dst = a.g0.psi + tbase(a.g0, m.T);
+      if (!(DIAG & 64)) {
 #pragma unroll
-      for (int r = 0; r < RPT; r++) st_hint(dst + roff(ps0, r), v[r], pol_keep);
+        for (int r = 0; r < RPT; r++) st_hint(dst + roff(ps0, r), v[r], pol_keep);
+      }
       if (V2) {
         pend = m.c;  // published one tile later (publish() above)
         if (a.tm_flags & 2) publish();
@@ -467,6 +496,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
     }
   }
   if (!BD && a.remote) __threadfence_system();
+  if (V2 && BD && (a.tm_flags & 4) && gtid == 0) bulk_wait0();  // every tensor store has landed
 }
 
 
@@ -651,7 +681,8 @@ SuperKernel pick_super_bd(bool lane3, int ng) {
 }
 // diagnostic variants (QAA_OPT_DIAG, bench configuration only; results are wrong
 // by design): 1 = no rotations, 2 = no shared-memory exchanges, 4 = no D,
-// 8 = group-k tiles ignore the chunk dependency (super_issue)
+// 8 = group-k tiles ignore the chunk dependency (super_issue), with 7: 16 = no
+// group-k tile loads, 32 = no group-k stores, 64 = no group-0 stores
 SuperKernel pick_super_diag(int diag) {
   switch (diag) {
     case 1: return qaa_superpass<true, 2, true, true, 1>;
@@ -661,6 +692,9 @@ SuperKernel pick_super_diag(int diag) {
     case 7: return qaa_superpass<true, 2, true, true, 7>;
     case 8: return qaa_superpass<true, 2, true, true, 8>;
     case 15: return qaa_superpass<true, 2, true, true, 15>;
+    case 23: return qaa_superpass<true, 2, true, true, 23>;
+    case 39: return qaa_superpass<true, 2, true, true, 39>;
+    case 71: return qaa_superpass<true, 2, true, true, 71>;
     default: return nullptr;
   }
 }
@@ -741,7 +775,7 @@ cudaError_t pass_tma_setup() {
                                                (int)TMA_SMEM_BYTES);
           if (e != cudaSuccess) return e;
         }
-  for (int d = 1; d < 16; d++)
+  for (int d = 1; d < 128; d++)
     if (pick_super_diag(d)) {
       cudaError_t e = cudaFuncSetAttribute(pick_super_diag(d), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)TMA_SMEM_BYTES);

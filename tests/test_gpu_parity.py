@@ -487,7 +487,7 @@ def test_error_codes(q, ctx):
 
 
 def test_option_ranges(q, ctx):
-    for key, bad in ((q.OPT_SUPER, 65536), (q.OPT_SUPER, -1), (q.OPT_DIAG, 16), (q.OPT_DIAG, -1)):
+    for key, bad in ((q.OPT_SUPER, 65536), (q.OPT_SUPER, -1), (q.OPT_DIAG, 128), (q.OPT_DIAG, -1)):
         with pytest.raises(q.QaaError) as e:
             ctx.set_option(key, bad)
         assert e.value.status == 1
@@ -504,7 +504,7 @@ def test_super_v2_sync_bitwise(q, n):
     cl = instance(n)
     sched = np.random.default_rng(7 * n).uniform(0, 1, 5)
     out = []
-    for sup in (17, 17 | 32768):
+    for sup in (17, 17 | 32768, 17 | 512):
         with q.Context(0) as c:
             c.set_option(q.OPT_SUPER, sup)
             c.load_instance(n, cl)
@@ -513,6 +513,7 @@ def test_super_v2_sync_bitwise(q, n):
             assert c.stats()["super_launches"] == 5
             out.append(c.state())
     assert np.array_equal(out[0].view(np.uint64), out[1].view(np.uint64))
+    assert np.array_equal(out[0].view(np.uint64), out[2].view(np.uint64))  # TMA tensor stores (bit 9)
 
 
 def test_torch_owned_state(q, orc):
