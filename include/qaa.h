@@ -299,6 +299,10 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        default cluster-resident sweep). 0: off.
  *  QAA_OPT_WARP_GRID     tuning hook for the warp-tile launch: ctas * 16 + warps per CTA
  *                        (1..8); 0 (default) = automatic.
+ *  QAA_OPT_SUPER_REV     1: the L2-blocked step with its two sub-passes in the other order
+ *                        (three tile groups): [group k: rotate, D, rotate] tiles first (strided
+ *                        rows from HBM, output kept in L2), then [group 0: rotate] (contiguous
+ *                        from L2, the step's only HBM write-back contiguous). 0 (default).
  *  QAA_OPT_DIAG          timing diagnostics ONLY (results are wrong by design): the
  *                        L2-blocked step at the bench configuration with work removed --
  *                        1 = no rotations, 2 = no shared-memory exchanges, 4 = no D,
@@ -327,7 +331,8 @@ enum {
   QAA_OPT_DIAG = 14,
   QAA_OPT_CLUSTER = 16,
   QAA_OPT_WARPTILE = 17,
-  QAA_OPT_WARP_GRID = 18
+  QAA_OPT_WARP_GRID = 18,
+  QAA_OPT_SUPER_REV = 19
 };
 qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value);
 

@@ -63,7 +63,7 @@ bool super_usable(qaa_ctx* ctx) {
 }
 
 static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_pre, double t_post,
-                                    const double2* phi, int n_phi) {
+                                    const double2* phi, int n_phi, bool rev = false) {
   int64_t nch = 0;
   for (size_t g = 1; g < ctx->geom.groups.size() && g < 4; g++) nch = std::max(nch, ctx->super_static[g].nchunks);
   const size_t need = 2 * (size_t)nch * sizeof(unsigned) + 256;
@@ -109,6 +109,7 @@ static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_p
   a.v2 = ctx->super_v2 && !ctx->super_split;
   a.tm_flags = ctx->super_tm_flags;  // v2: 1 = publish after the next landed read, 2 = right after the stores
   a.diag = ctx->diag;
+  a.rev = rev ? 1 : 0;
   a.done_shift = a.v2 ? 3 : 0;
   CUDA_TRY(cudaMemsetAsync(ctx->d_super, 0, 256 + 2 * (size_t)a.nchunks * sizeof(unsigned), ctx->stream));
   // phi == nullptr: the plain pair of a four-group plan (kernel variant without D)
@@ -527,9 +528,35 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
   const bool prefetch = ctx->ctas_per_sm == 1;
   const int fast_grid_cap = ctx->num_sms * (prefetch ? 1 : 2);
   const bool sup = super_usable(ctx) && ctx->step_spanning == 2 && ctx->order == 1;
+  const bool rev = sup && ctx->super_rev && ctx->geom.groups.size() == 3 && ctx->super_groups == 2 && ctx->super_v2 &&
+                   !ctx->super_tm && !ctx->super_pw && !ctx->super_split && !ctx->diag;
   for (size_t pi = 0; pi < plan.size(); pi++) {
     const PassPlan& pp = plan[pi];
-    if (sup && pi + 1 < plan.size()) {
+    if (rev && pi + 1 < plan.size()) {
+      // reversed pair [group k: (pre j), D_{j+1}, post j+1][group 0: pre j+1] -> one launch
+      const PassPlan& pn = plan[pi + 1];
+      if (pp.group >= 1 && pp.d_step >= 0 && pp.post_step >= 0 && pn.group == 0 && pn.pre_step == pp.post_step &&
+          pn.d_step < 0 && pn.post_step < 0 && ctx->super_ok[(size_t)pp.group] &&
+          (pp.pre_step < 0 || sc[(size_t)pp.pre_step].form == 0) && sc[(size_t)pp.post_step].form == 0) {
+        if (ctx->profile) CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, ctx->stream));
+        qaa_status st = launch_super_pair(ctx, pp.group, sc[(size_t)pn.pre_step].coef,
+                                          pp.pre_step >= 0 ? sc[(size_t)pp.pre_step].coef : 0.0,
+                                          sc[(size_t)pp.post_step].coef, dphi + (size_t)pp.d_step * n_phi, n_phi, true);
+        if (st) return st;
+        if (ctx->profile) {
+          CUDA_TRY(cudaEventRecord(ctx->ev_pool[ctx->ev_used].second, ctx->stream));
+          if (ctx->ev_super.size() < ctx->ev_pool.size()) ctx->ev_super.resize(ctx->ev_pool.size(), 0);
+          ctx->ev_super[ctx->ev_used] = 1;
+          ctx->ev_used++;
+        }
+        ctx->stats.pass_launches++;
+        ctx->stats.super_launches++;
+        ctx->stats.kernel_launches_total++;
+        pi++;
+        continue;
+      }
+    }
+    if (sup && !rev && pi + 1 < plan.size()) {
       // [group 0: pre j] [group k: pre j, D_{j+1}, post j+1] -> one L2-blocked launch
       const PassPlan& pn = plan[pi + 1];
       const bool with_d = pn.d_step >= 0 && pn.post_step >= 0;

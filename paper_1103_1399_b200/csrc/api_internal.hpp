@@ -119,7 +119,8 @@ struct qaa_ctx {
   uint8_t* Ewt[4] = {nullptr, nullptr, nullptr, nullptr};
   void* d_wsweep = nullptr;  // warp-tile sweep: plans, offsets, team states, partials, barriers
   size_t d_wsweep_cap = 0;
-  int super_v2 = 1;  // split-phase WAR guards + deferred publish (QAA_OPT_SUPER bit 15 clears it)
+  int super_v2 = 1;
+  int super_rev = 0;  // QAA_OPT_SUPER_REV: reversed pairs [group k rotate/D/rotate][group 0 rotate]  // split-phase WAR guards + deferred publish (QAA_OPT_SUPER bit 15 clears it)
   int super_grid = 0;  // 0: one CTA per SM
   int super_split = 0;
   int persist = 0;  // persistent evolve for 13 <= L <= 21 (opt-in: measured slower)

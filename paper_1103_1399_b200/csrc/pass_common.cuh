@@ -473,7 +473,10 @@ __device__ __forceinline__ void load_gk(const CUtensorMap* kmap, const SuperArgs
 }
 
 // fetch the next work item for slot J % 3 (tile J of this CTA) and start its load
-template <int NG, bool BD>
+// REV (reversed pair, SuperArgs-compatible): the first sub-pass (A items) runs the
+// group-k tiles -- strided rows from HBM, with D -- and the second (B items) the
+// group-0 tiles, contiguous from L2, so the step's HBM write-back is contiguous.
+template <int NG, bool BD, bool REV = false>
 __device__ void super_issue(const CUtensorMap* kmap, const SuperArgs& a, int64_t J, double2* slots, uint8_t* eslots,
                             uint64_t* full, SlotMeta* meta, uint64_t pol_dead) {
   const int s = (int)(J % TMA_SLOTS);
@@ -518,20 +521,31 @@ __device__ void super_issue(const CUtensorMap* kmap, const SuperArgs& a, int64_t
     }
   }
   if (kind == SK_A) {
+    if (REV) {
+      const uint32_t T = pdep32(i, a.k_imask) | pdep32((uint32_t)c, a.k_cmask);
+      meta[s] = SlotMeta{SK_A, (int)c, T, 0};
+      load_gk<BD>(kmap, a, T, slots + (size_t)s * FAST_XBUF, eslots + (size_t)s * TILE, fb, pol_dead);
+      return;
+    }
     const uint32_t T = pdep32(i, a.z_imask) | pdep32((uint32_t)c, a.z_cmask);
     meta[s] = SlotMeta{SK_A, (int)c, T, 0};
     mbar_expect_tx(fb, TILE * 16u);
     bulk_g2s_hint(slots + (size_t)s * FAST_XBUF, a.g0.psi + tbase(a.g0, T), TILE * 16u, fb, pol_dead);
     return;
   }
-  const uint32_t T = pdep32(i, a.k_imask) | pdep32((uint32_t)c, a.k_cmask);
+  const uint32_t T = REV ? (pdep32(i, a.z_imask) | pdep32((uint32_t)c, a.z_cmask))
+                         : (pdep32(i, a.k_imask) | pdep32((uint32_t)c, a.k_cmask));
   if ((a.diag & 8) || ld_acquire(&a.done[c]) >= (1u << (a.tpc_bits + a.done_shift))) {
     fence_async_global();  // generic-proxy stores of chunk c -> this async-proxy read
     meta[s] = SlotMeta{SK_B, (int)c, T, 0};
-    if (a.diag & 16)  // timing diagnostic: the group-k tile "lands" without a load
+    if (a.diag & 16) {  // timing diagnostic: the group-k tile "lands" without a load
       mbar_arrive_notx(fb);
-    else
+    } else if (REV) {
+      mbar_expect_tx(fb, TILE * 16u);
+      bulk_g2s_hint(slots + (size_t)s * FAST_XBUF, a.g0.psi + tbase(a.g0, T), TILE * 16u, fb, pol_dead);
+    } else {
       load_gk<BD>(kmap, a, T, slots + (size_t)s * FAST_XBUF, eslots + (size_t)s * TILE, fb, pol_dead);
+    }
   } else {
     meta[s] = SlotMeta{SK_B_DEFERRED, (int)c, T, 0};
     mbar_arrive_notx(fb);

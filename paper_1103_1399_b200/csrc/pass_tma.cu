@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_pass_tma(const __grid_co
 // its 1/8 of the tile to done[c] (red.release) at its next tile's first exchange,
 // when its stores have drained -- or before any wait on a chunk and at the end,
 // so a chunk's count can never wait on a warp that waits for it.
-template <bool LANE3, int NG, bool BD, bool V2, int DIAG = 0>
+template <bool LANE3, int NG, bool BD, bool V2, int DIAG = 0, bool REV = false>
 __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_constant__ CUtensorMap kmap,
                                                                  const SuperArgs a) {
   constexpr int BPROG = BD ? FP_GK_PRE_D_POST : FP_GK_PRE;
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
     if (V2)
       for (int g = 0; g < NG; g++) mbar_init(&slot_consumed(sm)[g], NTHREADS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int64_t J = 0; J < TMA_SLOTS; J++) super_issue<NG, BD>(&kmap, a, J, slots, eslots, full, meta, pol_dead);
+    for (int64_t J = 0; J < TMA_SLOTS; J++) super_issue<NG, BD, REV>(&kmap, a, J, slots, eslots, full, meta, pol_dead);
   }
   if (BD)
     for (int e = tid; e < a.gk.n_phi * PHI_COPIES; e += NG * NTHREADS) phis[e] = a.gk.phi[e / PHI_COPIES];
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
       // tile J+3 belongs to the other group and is only ever issued by the
       // finisher of J: pass the end marker on before leaving
       group_bar(g);
-      if (gtid == 0) super_issue<NG, BD>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
+      if (gtid == 0) super_issue<NG, BD, REV>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
       break;
     }
     double2* xb = slots + (size_t)s * FAST_XBUF;
@@ -400,7 +400,12 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
           wait_bound(it, t0);
         }
         fence_async_global();
-        load_gk<BD>(&kmap, a, m.T, xb, es, &late[g], pol_dead);
+        if (REV) {
+          mbar_expect_tx(&late[g], TILE * 16u);
+          bulk_g2s_hint(xb, a.g0.psi + tbase(a.g0, m.T), TILE * 16u, &late[g], pol_dead);
+        } else {
+          load_gk<BD>(&kmap, a, m.T, xb, es, &late[g], pol_dead);
+        }
       }
       mbar_wait_bounded(&late[g], late_phase & 1);
       late_phase++;
@@ -424,7 +429,8 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
       late_phase++;
     }
     const bool isb = m.kind != SK_A && m.kind != SK_A_DEFERRED;
-    if (isb) {
+    const bool gkt = REV ? !isb : isb;  // a group-k tile (rotate/D/rotate)
+    if (gkt) {
       load_landed<Info<BPROG>::load_pat>(v, xb, lane, lw);
       if (a.tm_flags & 1) publish();
       program<BPROG, LANE3, V2, DIAG>(a.gk, v, xb, es, phis, lane, lw, g, war);
@@ -437,7 +443,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
     // group-k tile stored by ONE TMA tensor store from the slot (tm_flags 4, v2):
     // write-after-read guard, tile-local STS, proxy fence, group barrier; the
     // storing thread refills the slot once the store has read it
-    const bool tstore = V2 && BD && isb && (a.tm_flags & 4) && !a.gk.contiguous && !(DIAG & 32);
+    const bool tstore = !REV && V2 && BD && isb && (a.tm_flags & 4) && !a.gk.contiguous && !(DIAG & 32);
     if (tstore) {
       war_arrive<true>(war);  // the final rotations consumed every value read from the slot
       mbar_wait(war.bar, war.ph & 1);
@@ -457,12 +463,27 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
         tma_store_hint(&kmap, cc, a.gk.ndims, xb, pol_dead);
         bulk_commit();
         bulk_wait_read0();
-        super_issue<NG, BD>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
+        super_issue<NG, BD, REV>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
       }
       continue;
     }
     __syncwarp();
-    if (lane == 0 && last_warp_out(&cnt[s])) super_issue<NG, BD>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
+    if (lane == 0 && last_warp_out(&cnt[s])) super_issue<NG, BD, REV>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
+    if (REV) {
+      // group-k tiles (A items) keep their output in L2 for the group-0 sub-pass;
+      // group-0 tiles (B items) are the step's final, contiguous HBM write-back
+      if (gkt) {
+        double2* dst = a.gk.psi + tbase(a.gk, m.T);
+#pragma unroll
+        for (int r = 0; r < RPT; r++) st_hint(dst + roff(psk, r), v[r], pol_keep);
+        pend = m.c;
+      } else {
+        double2* dst = a.g0.psi + tbase(a.g0, m.T);
+#pragma unroll
+        for (int r = 0; r < RPT; r++) st_hint(dst + roff(ps0, r), v[r], pol_dead);
+      }
+      continue;
+    }
     if (isb) {
       const int64_t tb = tbase(a.gk, m.T);
       if (!BD && a.remote) {
@@ -698,6 +719,9 @@ SuperKernel pick_super_diag(int diag) {
     default: return nullptr;
   }
 }
+SuperKernel pick_super_rev(bool lane3) {
+  return lane3 ? qaa_superpass<true, 2, true, true, 0, true> : qaa_superpass<false, 2, true, true, 0, true>;
+}
 SuperKernel pick_super(bool lane3, int ng, bool bd, bool v2) {
   if (v2) return bd ? pick_super_bd<true, true>(lane3, ng) : pick_super_bd<false, true>(lane3, ng);
   return bd ? pick_super_bd<true, false>(lane3, ng) : pick_super_bd<false, false>(lane3, ng);
@@ -726,6 +750,10 @@ TmaKernel pick(int prog, bool lane3, int ng) { return ng == 1 ? pick_ng<1>(prog,
 cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool lane3, int ngroups, bool bd, int grid,
                              cudaStream_t st) {
   SuperKernel k = pick_super(lane3, ngroups, bd, a.v2 != 0);  // shared-memory attribute set in pass_tma_setup
+  if (a.rev) {  // reversed pair: [group k rotate/D/rotate][group 0 rotate] (v2, two groups, with D)
+    if (!bd || !a.v2 || ngroups != 2) return cudaErrorInvalidValue;
+    k = pick_super_rev(lane3);
+  }
   if (a.diag && bd) {  // the D-less closing pair keeps the real kernel
     if (!lane3 || ngroups != 2 || !a.v2 || !pick_super_diag(a.diag)) return cudaErrorInvalidValue;
     k = pick_super_diag(a.diag);
@@ -775,6 +803,11 @@ cudaError_t pass_tma_setup() {
                                                (int)TMA_SMEM_BYTES);
           if (e != cudaSuccess) return e;
         }
+  for (int l = 0; l < 2; l++) {
+    cudaError_t e = cudaFuncSetAttribute(pick_super_rev(l), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)TMA_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+  }
   for (int d = 1; d < 128; d++)
     if (pick_super_diag(d)) {
       cudaError_t e = cudaFuncSetAttribute(pick_super_diag(d), cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -516,6 +516,26 @@ def test_super_v2_sync_bitwise(q, n):
     assert np.array_equal(out[0].view(np.uint64), out[2].view(np.uint64))  # TMA tensor stores (bit 9)
 
 
+@pytest.mark.parametrize("n", [22, 25])
+def test_super_rev_bitwise_equals_two_pass(q, n):
+    """QAA_OPT_SUPER_REV: the L2-blocked pairs fused the other way round
+    ([group k rotate/D/rotate][group 0 rotate]) run the same pass sequence, so the
+    state after 5 random-schedule steps equals the two-pass plan's bit for bit."""
+    cl = instance(n)
+    sched = np.random.default_rng(3 * n).uniform(0, 1, 5)
+    out = []
+    for sup, rev in ((17, 1), (0, 0)):
+        with q.Context(0) as c:
+            c.set_option(q.OPT_SUPER, sup)
+            c.set_option(q.OPT_SUPER_REV, rev)
+            c.load_instance(n, cl)
+            c.set_state(cnf.random_state(n, 9 + n))
+            c.evolve(1.3, 5, sched)
+            assert c.stats()["super_launches"] == (5 if sup else 0)
+            out.append(c.state())
+    assert np.array_equal(out[0].view(np.uint64), out[1].view(np.uint64))
+
+
 def test_torch_owned_state(q, orc):
     import torch
     c = q.Context(0, n_max=14, torch_state=True)
