@@ -218,6 +218,7 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
 }
 
 qaa_status qaa_load_instance(qaa_ctx* ctx, int n, int m, const int32_t* lits) {
+  QAA_NVTX("qaa_load_instance");
   CHECK_CTX();
   if (n < 1 || n > 40) return fail(ctx, QAA_E_USAGE, "n must be in 1..40, got %d", n);
   if (m < 0) return fail(ctx, QAA_E_USAGE, "m must be >= 0, got %d", m);
@@ -377,6 +378,7 @@ qaa_status qaa_load_instance(qaa_ctx* ctx, int n, int m, const int32_t* lits) {
 }
 
 qaa_status qaa_init_uniform(qaa_ctx* ctx) {
+  QAA_NVTX("qaa_init_uniform");
   CHECK_CTX();
   if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "init_uniform before load_instance");
   const double a = 1.0 / std::sqrt(std::ldexp(1.0, ctx->n));
@@ -387,6 +389,7 @@ qaa_status qaa_init_uniform(qaa_ctx* ctx) {
 }
 
 qaa_status qaa_init_basis(qaa_ctx* ctx, uint64_t x) {
+  QAA_NVTX("qaa_init_basis");
   CHECK_CTX();
   if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "init_basis before load_instance");
   if (ctx->n < 64 && x >= (1ull << ctx->n)) return fail(ctx, QAA_E_USAGE, "basis index %llu >= 2^n", (unsigned long long)x);

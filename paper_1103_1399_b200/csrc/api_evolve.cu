@@ -64,6 +64,7 @@ bool super_usable(qaa_ctx* ctx) {
 
 static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_pre, double t_post,
                                     const double2* phi, int n_phi, bool rev = false) {
+  QAA_NVTX(phi ? "qaa_superpass (Trotter step)" : "qaa_superpass (plain pair)");
   int64_t nch = 0;
   for (size_t g = 1; g < ctx->geom.groups.size() && g < 4; g++) nch = std::max(nch, ctx->super_static[g].nchunks);
   const size_t need = 2 * (size_t)nch * sizeof(unsigned) + 256;
@@ -297,6 +298,7 @@ qaa_status ensure_warp_tables(qaa_ctx* ctx) {
 
 static qaa_status run_warp_evolve(qaa_ctx* ctx, const WarpPass* dplan, int64_t npass, const double2* dphi,
                                   const double* dcoef, const int32_t* dform, int n_phi) {
+  QAA_NVTX("qaa_warp_evolve (all passes)");
   {
     qaa_status st = ensure_warp_tables(ctx);
     if (st) return st;
@@ -346,6 +348,7 @@ static qaa_status run_warp_evolve(qaa_ctx* ctx, const WarpPass* dplan, int64_t n
 extern "C" {
 
 qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule) {
+  QAA_NVTX("qaa_evolve");
   CHECK_CTX();
   if (!ctx->loaded || !ctx->initialized) return fail(ctx, QAA_E_STATE, "evolve before load_instance/init");
   if (!(T >= 0.0) || !std::isfinite(T)) return fail(ctx, QAA_E_USAGE, "T must be finite and >= 0, got %g", T);

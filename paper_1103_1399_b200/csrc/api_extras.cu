@@ -7,6 +7,7 @@
 extern "C" {
 
 qaa_status qaa_spectrum(qaa_ctx* ctx, double s, int kmax, int nev, double* evals, double* overlap, int* iters) {
+  QAA_NVTX("qaa_spectrum");
   CHECK_CTX();
   if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "spectrum before load_instance");
   if (!(s >= 0.0 && s <= 1.0)) return fail(ctx, QAA_E_USAGE, "s = %g outside [0, 1]", s);
@@ -47,6 +48,7 @@ qaa_status qaa_spectrum(qaa_ctx* ctx, double s, int kmax, int nev, double* evals
 }
 
 qaa_status qaa_time_energy_table(qaa_ctx* ctx, int reps, double* ms) {
+  QAA_NVTX("qaa_time_energy_table");
   CHECK_CTX();
   if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "time_energy_table before load_instance");
   if (reps < 1 || !ms) return fail(ctx, QAA_E_USAGE, "reps must be >= 1 and ms non-NULL");
@@ -76,6 +78,7 @@ qaa_status qaa_time_energy_table(qaa_ctx* ctx, int reps, double* ms) {
 }
 
 qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, double* out) {
+  QAA_NVTX("qaa_sweep");
   CHECK_CTX();
   if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "sweep before load_instance");
   const bool wide = ctx->warptile == 2 && ctx->L <= WARP_MAX_L &&

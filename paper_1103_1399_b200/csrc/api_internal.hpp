@@ -2,6 +2,7 @@
 // (api_*.cu) of libqaa: the opaque context, error helpers, and the internal
 // functions one unit calls in another. Not part of the public ABI (include/qaa.h).
 #pragma once
+#include <nvtx3/nvToolsExt.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -40,6 +41,16 @@ struct ClauseRecHost {
 };
 static_assert(sizeof(ClauseRecHost) == 32, "clause record layout");
 }  // namespace
+
+// NVTX ranges around the C-ABI calls and the kernel launches of an evolve (header-only
+// NVTX v3: free when no tool is attached; visible in nsys / ncu --nvtx)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define QAA_NVTX(name) NvtxRange qaa_nvtx_range_(name)
 
 constexpr int WARP_MIN_L = 13, WARP_MAX_L = 21;  // warp_evolve.cu range (QAA_OPT_WARPTILE 2)
 constexpr int WARP_AUTO_MAX_L = 16;               // default range: faster than the per-pass kernels up to here

@@ -105,6 +105,7 @@ static qaa_status obs_sigma_local(qaa_ctx* ctx, double* sx, bool only_top) {
 }
 
 qaa_status qaa_success_prob(qaa_ctx* ctx, double* out) {
+  QAA_NVTX("qaa_success_prob");
   CHECK_CTX();
   if (!out) return fail(ctx, QAA_E_USAGE, "out is NULL");
   if (!ctx->loaded || !ctx->initialized) return fail(ctx, QAA_E_STATE, "success_prob before init");
@@ -135,6 +136,7 @@ qaa_status qaa_success_prob(qaa_ctx* ctx, double* out) {
 }
 
 qaa_status qaa_norm2(qaa_ctx* ctx, double* out) {
+  QAA_NVTX("qaa_norm2");
   CHECK_CTX();
   if (!out) return fail(ctx, QAA_E_USAGE, "out is NULL");
   if (!ctx->loaded || !ctx->initialized) return fail(ctx, QAA_E_STATE, "norm2 before init");
@@ -146,6 +148,7 @@ qaa_status qaa_norm2(qaa_ctx* ctx, double* out) {
 }
 
 qaa_status qaa_sigma_x(qaa_ctx* ctx, double* out) {
+  QAA_NVTX("qaa_sigma_x");
   CHECK_CTX();
   if (!out) return fail(ctx, QAA_E_USAGE, "out is NULL");
   if (!ctx->loaded || !ctx->initialized) return fail(ctx, QAA_E_STATE, "sigma_x before init");
@@ -153,6 +156,7 @@ qaa_status qaa_sigma_x(qaa_ctx* ctx, double* out) {
 }
 
 qaa_status qaa_energy(qaa_ctx* ctx, double s, double* out) {
+  QAA_NVTX("qaa_energy");
   CHECK_CTX();
   if (!out) return fail(ctx, QAA_E_USAGE, "out is NULL");
   if (!(s >= 0.0 && s <= 1.0)) return fail(ctx, QAA_E_USAGE, "s = %g outside [0, 1]", s);
@@ -193,6 +197,7 @@ static bool local_range(qaa_ctx* ctx, uint64_t first, uint64_t count, uint64_t* 
 }
 
 qaa_status qaa_copy_state(qaa_ctx* ctx, uint64_t first, uint64_t count, double* dst) {
+  QAA_NVTX("qaa_copy_state");
   CHECK_CTX();
   if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "copy_state before load_instance");
   if (count && !dst) return fail(ctx, QAA_E_USAGE, "dst is NULL");
@@ -210,6 +215,7 @@ qaa_status qaa_copy_state(qaa_ctx* ctx, uint64_t first, uint64_t count, double* 
 }
 
 qaa_status qaa_set_state(qaa_ctx* ctx, uint64_t first, uint64_t count, const double* src) {
+  QAA_NVTX("qaa_set_state");
   CHECK_CTX();
   if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "set_state before load_instance");
   if (count && !src) return fail(ctx, QAA_E_USAGE, "src is NULL");
