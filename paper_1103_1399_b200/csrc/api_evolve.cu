@@ -152,6 +152,13 @@ static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_p
                             ctx->super_grid ? ctx->super_grid : ctx->num_sms, ctx->stream);
     ctx->stats.pw_launches++;
   } else {
+    if (a.tm_flags & 8) {  // diagnostics: deferred group-k tiles and their wait cycles (tm_diag[5..7])
+      if (!ctx->d_tm_diag) {
+        CUDA_TRY(cudaMalloc(&ctx->d_tm_diag, 8 * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMemsetAsync(ctx->d_tm_diag, 0, 8 * sizeof(unsigned long long), ctx->stream));
+      }
+      a.dbg = ctx->d_tm_diag;
+    }
     e = launch_superpass(&ctx->tmaps[(size_t)k], a, (gk.rot_local >> 3) & 1, ctx->super_groups, bd,
                          ctx->super_grid ? ctx->super_grid : ctx->num_sms, ctx->stream);
   }

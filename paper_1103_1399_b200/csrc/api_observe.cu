@@ -27,22 +27,44 @@ static qaa_status obs_basic(qaa_ctx* ctx, double* basic) {
   return comm_sum(ctx, basic, 3);
 }
 
-// sx[phys + phys_offset] = local pair sums of sigma^x on the rotated bits of
-// every group (only_top: the top group's bits >= L - g, after a swap to layout B)
-static qaa_status obs_sigma_local(qaa_ctx* ctx, double* sx, bool only_top);
+// sx[phys] = local pair sums of sigma^x on the rotated bits of every group
+static qaa_status obs_sigma_local(qaa_ctx* ctx, double* sx);
 
-// sx[j] = <sigma^x_j> for all n qubits (collective when sharded: the global
-// qubits are measured in layout B, between two layout swaps)
+// the rank qubits (logical L..n-1, layout A): every rank dots its shard with
+// each partner rank's shard read in place over NVLink (16 B/amp per rank qubit,
+// nothing moved; round 1 swapped layouts twice: 2 x 16 B/amp of peer stores).
+// Device-side barriers on both sides: the peers' states are final before the
+// reads, and nobody overwrites its buffer before every rank has read it.
+static qaa_status obs_sigma_global(qaa_ctx* ctx, double* sx) {
+  const int64_t N = (int64_t)1 << ctx->L;
+  PeerDotArgs a;
+  memset(&a, 0, sizeof a);
+  a.g = ctx->gbits;
+  for (int t = 0; t < ctx->gbits; t++) a.peer[t] = ctx->peers[ctx->cur][ctx->rank ^ (1 << t)];
+  int grid = ctx->num_sms * RED_BLOCKS_PER_SM;
+  if ((int64_t)grid * 256 > N) grid = (int)std::max<int64_t>(1, (N + 255) / 256);
+  qaa_status st = ensure_part(ctx, (size_t)grid * 3);
+  if (st) return st;
+  st = shard_barrier(ctx);
+  if (st) return st;
+  CUDA_TRY(launch_obs_peer_dot(ctx->state, a, N, ctx->d_part, grid, ctx->stream));
+  st = shard_barrier(ctx);
+  if (st) return st;
+  CUDA_TRY(launch_reduce_partials(ctx->d_part, grid, 3, 3, ctx->d_out, ctx->stream));
+  ctx->stats.kernel_launches_total += 2;
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_out, ctx->d_out, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  for (int t = 0; t < ctx->gbits; t++) sx[ctx->L + t] = ctx->h_out[t];
+  return QAA_OK;
+}
+
+// sx[j] = <sigma^x_j> for all n qubits (collective when sharded)
 static qaa_status obs_sigma(qaa_ctx* ctx, double* sx) {
   for (int j = 0; j < ctx->n; j++) sx[j] = 0.0;
-  qaa_status st = obs_sigma_local(ctx, sx, false);
+  qaa_status st = obs_sigma_local(ctx, sx);
   if (st) return st;
   if (ctx->world > 1) {
-    st = shard_remap(ctx);
-    if (st) return st;
-    st = obs_sigma_local(ctx, sx, true);
-    if (st) return st;
-    st = shard_remap(ctx);
+    st = obs_sigma_global(ctx, sx);
     if (st) return st;
     st = comm_sum(ctx, sx, ctx->n);
     if (st) return st;
@@ -50,7 +72,7 @@ static qaa_status obs_sigma(qaa_ctx* ctx, double* sx) {
   return QAA_OK;
 }
 
-static qaa_status obs_sigma_local(qaa_ctx* ctx, double* sx, bool only_top) {
+static qaa_status obs_sigma_local(qaa_ctx* ctx, double* sx) {
   std::vector<SigmaArgs> jobs;
   if (ctx->L <= RESIDENT_MAX_L) {
     SigmaArgs a;
@@ -65,17 +87,11 @@ static qaa_status obs_sigma_local(qaa_ctx* ctx, double* sx, bool only_top) {
   } else {
     for (size_t gi = 0; gi < ctx->geom.groups.size(); gi++) {
       const Group& g = ctx->geom.groups[gi];
-      if (only_top && gi + 1 != ctx->geom.groups.size()) continue;
       SigmaArgs a;
       memset(&a, 0, sizeof a);
       a.psi = ctx->state;
       a.k = TILE_BITS;
       a.mask = g.rot_local;
-      if (only_top) {
-        a.mask = 0;
-        for (int b = 0; b < TILE_BITS; b++)
-          if (g.phys[b] >= ctx->L - ctx->gbits) a.mask |= 1u << b;
-      }
       for (int b = 0; b < TILE_BITS; b++) a.phys[b] = g.phys[b];
       a.nseg = g.nseg;
       for (int s = 0; s < g.nseg; s++) {
@@ -96,10 +112,8 @@ static qaa_status obs_sigma_local(qaa_ctx* ctx, double* sx, bool only_top) {
     ctx->stats.kernel_launches_total += 2;
     CUDA_TRY(cudaMemcpyAsync(ctx->h_out, ctx->d_out, TILE_BITS * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    // layout B keeps the rank qubits of layout A (logical L..n-1) at local L-g..L-1
-    const int off = only_top ? ctx->gbits : 0;
     for (int j = 0; j < a.k; j++)
-      if (a.mask >> j & 1) sx[a.phys[j] + off] = 2.0 * ctx->h_out[j];
+      if (a.mask >> j & 1) sx[a.phys[j]] = 2.0 * ctx->h_out[j];
   }
   return QAA_OK;
 }

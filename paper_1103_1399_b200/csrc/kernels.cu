@@ -826,6 +826,30 @@ cudaError_t launch_obs_basic(const double2* psi, const uint8_t* E, int64_t N, do
   return cudaGetLastError();
 }
 
+__global__ void __launch_bounds__(256) obs_peer_dot_kernel(const double2* psi, const PeerDotArgs a, int64_t N,
+                                                            double* partial) {
+  __shared__ double sh[32 * 3];
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < N; x += (int64_t)gridDim.x * blockDim.x) {
+    const double2 u = psi[x];
+#pragma unroll
+    for (int t = 0; t < 3; t++)
+      if (t < a.g) {
+        const double2 w = __ldcg(a.peer[t] + x);  // another GPU's memory: no L1 reuse
+        acc[t] += fma(u.x, w.x, u.y * w.y);
+      }
+  }
+  block_reduce<3>(acc, sh);
+  if (threadIdx.x == 0)
+    for (int j = 0; j < 3; j++) partial[blockIdx.x * 3 + j] = acc[j];
+}
+
+cudaError_t launch_obs_peer_dot(const double2* psi, const PeerDotArgs& a, int64_t N, double* partial, int grid,
+                                cudaStream_t st) {
+  obs_peer_dot_kernel<<<grid, 256, 0, st>>>(psi, a, N, partial);
+  return cudaGetLastError();
+}
+
 __global__ void __launch_bounds__(256) obs_sigma_kernel(const SigmaArgs a, double* partial) {
   extern __shared__ double2 tile[];
   __shared__ double sh[32 * TILE_BITS];

@@ -329,6 +329,15 @@ struct SigmaArgs {
   int64_t ntiles;
 };
 cudaError_t launch_obs_sigma(const SigmaArgs& a, double* partial, int grid, cudaStream_t st);
+// <sigma^x> of the rank qubits of a sharded state (layout A): partial[b*3 + t] =
+// this rank's part of sum_x Re(conj(psi[x]) psi[x ^ 2^(L+t)]), the partner being
+// the same local index on rank r ^ 2^t, read over NVLink through its IPC mapping.
+struct PeerDotArgs {
+  const double2* peer[3];  // rank r ^ 2^t's current shard buffer, t < g
+  int g;                   // rank qubits (1..3)
+};
+cudaError_t launch_obs_peer_dot(const double2* psi, const PeerDotArgs& a, int64_t N, double* partial, int grid,
+                                cudaStream_t st);
 // sum of |psi[Z[i]]|^2 over a sorted list (1 block).
 cudaError_t launch_gather_success(const double2* psi, const uint64_t* Z, int64_t nz, uint64_t x_offset,
                                   double* out, cudaStream_t st);

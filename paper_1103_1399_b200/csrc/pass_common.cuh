@@ -548,8 +548,10 @@ __device__ void super_issue(const CUtensorMap* kmap, const SuperArgs& a, int64_t
     }
   } else {
     meta[s] = SlotMeta{SK_B_DEFERRED, (int)c, T, 0};
+    if (a.dbg) atomicAdd(&a.dbg[5], 1ull);  // diagnostics (tm_flags 8): deferred group-k tiles
     mbar_arrive_notx(fb);
   }
+  if (a.dbg) atomicAdd(&a.dbg[6], 1ull);  // group-k tiles issued
 }
 
 }  // namespace pc

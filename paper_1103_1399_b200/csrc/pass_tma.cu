@@ -393,6 +393,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
     if (m.kind == SK_B_DEFERRED) {
       publish();
       if (DIAG & 8) __trap();  // super_issue never defers in this variant
+      const long long dt0 = a.dbg ? clock64() : 0;
       if (gtid == 0) {
         unsigned long long t0 = 0;
         for (uint32_t it = 0; ld_acquire(&a.done[m.c]) < chunk_done; it++) {
@@ -409,6 +410,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
       }
       mbar_wait_bounded(&late[g], late_phase & 1);
       late_phase++;
+      if (a.dbg && gtid == 0) atomicAdd(&a.dbg[7], (unsigned long long)(clock64() - dt0));
     } else if (m.kind == SK_A_DEFERRED) {
       // split roles: the group-0 side ran ahead; wait until the group-k side has
       // issued chunk c - L (a throttle on the L2 live set, not a data dependency)
