@@ -290,13 +290,17 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        kernels through HBM/L2.
  *  QAA_OPT_WARPTILE      1 (default): for 13 <= n <= 16 on one GPU with the automatic kernel
  *                        choice, all passes of the cyclic step-spanning plan run as ONE
- *                        cooperative launch, one warp per 2^9-amplitude tile (state in L2),
- *                        a grid barrier between passes; takes precedence over
- *                        QAA_OPT_CLUSTER (measured 4.1-5.0 vs 5.3-8.3 us per step at
- *                        n = 13..16). 2: also for 17 <= n <= 21 (there slower than the
- *                        per-pass kernels; a test hook), and qaa_sweep on teams of
- *                        warp-tile CTAs (n <= 21; at n = 13..16 no faster than the
- *                        default cluster-resident sweep). 0: off.
+ *                        cooperative launch over 2^9-amplitude tiles (state in L2), a grid
+ *                        barrier between passes, FOUR warps per tile (one 128-thread CTA,
+ *                        4 amplitudes per lane: the tile's work spread over the SM's four
+ *                        sub-partitions); takes precedence over QAA_OPT_CLUSTER (measured
+ *                        3.5-3.9 us per step at n = 13..16, vs 4.4-5.0 with one warp per
+ *                        tile and 5.4-8.3 cluster-resident). 2: ONE warp per tile (16
+ *                        amplitudes per lane), also for 17 <= n <= 21 (there slower than the
+ *                        per-pass kernels; a test hook), and qaa_sweep on teams of warp-tile
+ *                        CTAs (n <= 21; at n = 13..16 no faster than the default
+ *                        cluster-resident sweep). 3: four warps per tile, 13 <= n <= 21
+ *                        (test hook above 16). 0: off.
  *  QAA_OPT_WARP_GRID     tuning hook for the warp-tile launch: ctas * 16 + warps per CTA
  *                        (1..8); 0 (default) = automatic.
  *  QAA_OPT_SUPER_REV     1: the L2-blocked step with its two sub-passes in the other order

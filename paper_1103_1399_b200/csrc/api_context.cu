@@ -180,7 +180,7 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       ctx->super_hints = ((value >> 2) & 3) == 1 ? 0 : (((value >> 2) & 3) == 2 ? 1 : 2);
       return QAA_OK;
     case QAA_OPT_WARPTILE:
-      if (value < 0 || value > 2) return fail(ctx, QAA_E_USAGE, "warptile must be 0, 1 or 2");
+      if (value < 0 || value > 3) return fail(ctx, QAA_E_USAGE, "warptile must be 0, 1, 2 or 3");
       ctx->warptile = (int)value;
       return QAA_OK;
     case QAA_OPT_WARP_GRID:

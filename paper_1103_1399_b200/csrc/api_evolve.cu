@@ -341,7 +341,16 @@ static qaa_status run_warp_evolve(qaa_ctx* ctx, const WarpPass* dplan, int64_t n
     grid = std::min(ctx->num_sms, ctx->warp_grid >> 4);
     warps = ctx->warp_grid & 15;
   }
-  CUDA_TRY(launch_warp_evolve(wa, grid, warps, ctx->stream));
+  if (ctx->warptile == 3 || ctx->warptile == 1) {
+    // quad-warp tiles: one 128-thread CTA per tile while they fit co-resident
+    const int64_t ntiles = (int64_t)1 << (ctx->L - 9);
+    const int cap = ctx->num_sms * std::max(1, quad_evolve_max_active());
+    grid = (int)std::min<int64_t>(ntiles, cap);
+    if (ctx->warp_grid) grid = std::min(grid, ctx->warp_grid >> 4);
+    CUDA_TRY(launch_quad_evolve(wa, grid, ctx->stream));
+  } else {
+    CUDA_TRY(launch_warp_evolve(wa, grid, warps, ctx->stream));
+  }
   if (ctx->profile) {
     CUDA_TRY(cudaEventRecord(ctx->ev_pool[ev].second, ctx->stream));
     ctx->ev_used = ev + 1;
@@ -372,7 +381,7 @@ qaa_status qaa_evolve(qaa_ctx* ctx, double T, int64_t K, const double* schedule)
   const size_t form_bytes = (size_t)K * sizeof(int32_t);
   // the warp-tile path stages its pass records behind the coefficients
   const bool use_warp = ctx->warptile && ctx->world == 1 && ctx->kernel_mode == 2 && ctx->L >= WARP_MIN_L &&
-                        ctx->L <= (ctx->warptile == 2 ? WARP_MAX_L : WARP_AUTO_MAX_L);
+                        ctx->L <= (ctx->warptile >= 2 ? WARP_MAX_L : WARP_AUTO_MAX_L);
   std::vector<PassPlan> wplan;
   if (use_warp) {
     build_pass_schedule(warp_group_count(ctx->L), K, 1, &wplan);

@@ -262,6 +262,9 @@ struct WarpSweepArgs {
 cudaError_t launch_warp_sweep(const WarpSweepArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_warp_energy(const uint8_t* E, uint8_t* Eg, const WarpGeo& g, int L, int num_sms, cudaStream_t st);
 cudaError_t launch_warp_evolve(const WarpEvolveArgs& a, int grid, int warps, cudaStream_t st);
+// the same plan with four warps per tile (QAA_OPT_WARPTILE 3; grid <= SMs x quad_evolve_max_active())
+cudaError_t launch_quad_evolve(const WarpEvolveArgs& a, int grid, cudaStream_t st);
+int quad_evolve_max_active();
 // 10 <= L <= 12: register-phase variant (2-3x faster than the per-qubit loop)
 cudaError_t launch_resident_phases(const ResidentArgs& a, cudaStream_t st);
 

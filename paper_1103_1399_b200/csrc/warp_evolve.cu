@@ -197,6 +197,120 @@ __global__ void __launch_bounds__(WE_WARPS * 32, 1) qaa_warp_evolve(const WarpEv
   }
 }
 
+// ---------------------------------------------------------------------------
+// Quad-warp tiles (QAA_OPT_WARPTILE 3): the same tiles, tile groups, pass records
+// and grid barriers as qaa_warp_evolve, but each 2^9-amplitude tile is processed
+// by FOUR warps (one 128-thread CTA, 4 amplitudes per lane), so the tile's fp64
+// work and shuffles are spread over the SM's four sub-partitions instead of one:
+// the per-pass critical path (one tile per SM at L = 16) is about a quarter as
+// long. Patterns (w = warp of the quad, r = register):
+//   P1 (load / store, coalesced): l = lane | r << 5 | w << 7
+//   P2 (D):                       l = lane | w << 5 | r << 7
+// The lane bits (tile bits 0..4) are rotated with shuffles in either pattern; a
+// P1 <-> P2 exchange through shared memory (every warp access is 32 consecutive
+// amplitudes: conflict-free, no padding) swaps bits 5,6 <-> 7,8 between the
+// registers and the warps. Energies come from the same per-group table as the
+// warp-tile kernel (tile-local order): 4 coalesced byte loads per thread.
+constexpr int QW_THREADS = 128;
+
+template <int FORM>
+__device__ __forceinline__ void qw_lane(double2 (&v)[4], int j, double c) {
+#pragma unroll
+  for (int r = 0; r < 4; r++) {
+    const double px = __shfl_xor_sync(0xffffffffu, v[r].x, 1 << j);
+    const double py = __shfl_xor_sync(0xffffffffu, v[r].y, 1 << j);
+    v[r] = FORM == 0 ? make_double2(fma(-c, py, v[r].x), fma(c, px, v[r].y))
+                     : make_double2(fma(c, v[r].x, -py), fma(c, v[r].y, px));
+  }
+}
+// rotate the register bits (mask bit i = register bit i) and, if lanes, the
+// lane bits selected by rot bits 0..4
+template <int FORM>
+__device__ __forceinline__ void qw_rot_t(double2 (&v)[4], uint32_t regmask, uint32_t lanemask, double c) {
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+    if ((regmask >> i) & 1)
+#pragma unroll
+      for (int r = 0; r < 4; r++)
+        if (!(r & (1 << i))) we_pair<FORM>(v[r], v[r | (1 << i)], c);
+#pragma unroll
+  for (int j = 0; j < 5; j++)
+    if ((lanemask >> j) & 1) qw_lane<FORM>(v, j, c);
+}
+__device__ __forceinline__ void qw_rot(double2 (&v)[4], uint32_t regmask, uint32_t lanemask, double c, int form) {
+  if (form == 0) qw_rot_t<0>(v, regmask, lanemask, c);
+  else qw_rot_t<1>(v, regmask, lanemask, c);
+}
+template <bool TO_P2>
+__device__ __forceinline__ void qw_xchg(double2* xb, double2 (&v)[4], int lane, int w) {
+  __syncthreads();  // every thread's reads of the previous exchange are done
+#pragma unroll
+  for (int r = 0; r < 4; r++) xb[TO_P2 ? (lane | (r << 5) | (w << 7)) : (lane | (w << 5) | (r << 7))] = v[r];
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 4; r++) v[r] = xb[TO_P2 ? (lane | (w << 5) | (r << 7)) : (lane | (r << 5) | (w << 7))];
+}
+
+__global__ void __launch_bounds__(QW_THREADS) qaa_quad_evolve(const WarpEvolveArgs a) {
+  __shared__ __align__(16) double2 xb[512];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t ntiles = (int64_t)1 << (a.L - 9);
+  WarpPass nx = a.plan[0];
+  for (int64_t p = 0; p < a.npass; p++) {
+    const WarpPass ps = nx;
+    if (p + 1 < a.npass) nx = a.plan[p + 1];
+    const WarpGeo& g = a.geo[ps.group];
+    const uint8_t* Eg = a.Eg[ps.group];
+    const bool pre = ps.flags & WP_PRE, d = ps.flags & WP_D, post = ps.flags & WP_POST;
+    const int fpre = (ps.flags >> 3) & 1, fpost = (ps.flags >> 4) & 1;
+    const double2* phi = a.phi_all + ps.d * a.n_phi;
+    const uint32_t rot = g.rot;
+    const uint32_t lm = rot & 31u, r1 = (rot >> 5) & 3u, r2 = (rot >> 7) & 3u;
+    // P1 offsets: lane part + warp part; register strides (tile bits 5, 6)
+    int64_t thr = 0;
+#pragma unroll
+    for (int b = 0; b < 5; b++)
+      if ((lane >> b) & 1) thr += (int64_t)1 << g.phys[b];
+#pragma unroll
+    for (int b = 0; b < 2; b++)
+      if ((w >> b) & 1) thr += (int64_t)1 << g.phys[7 + b];
+    const int64_t s5 = (int64_t)1 << g.phys[5], s6 = (int64_t)1 << g.phys[6];
+    for (int64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
+      int64_t base = 0;
+      for (int i = 0; i < g.nfree; i++)
+        if ((T >> i) & 1) base += (int64_t)1 << g.free_bits[i];
+      const double2* src = a.psi + base + thr;
+      double2 v[4];
+      v[0] = ldcg2(src);
+      v[1] = ldcg2(src + s5);
+      v[2] = ldcg2(src + s6);
+      v[3] = ldcg2(src + s5 + s6);
+      unsigned e[4] = {0, 0, 0, 0};
+      if (d) {
+        const uint8_t* et = Eg + (T << 9) + lane + (w << 5);
+#pragma unroll
+        for (int r = 0; r < 4; r++) e[r] = __ldg(et + (r << 7));
+      }
+      if (pre) qw_rot(v, r1, lm, ps.cpre, fpre);
+      qw_xchg<true>(xb, v, lane, w);
+      if (pre) qw_rot(v, r2, 0u, ps.cpre, fpre);
+      if (d) {
+#pragma unroll
+        for (int r = 0; r < 4; r++) v[r] = cmul(__ldg(phi + e[r]), v[r]);
+      }
+      if (post) qw_rot(v, r2, lm, ps.cpost, fpost);
+      qw_xchg<false>(xb, v, lane, w);
+      if (post) qw_rot(v, r1, 0u, ps.cpost, fpost);
+      double2* dst = a.psi + base + thr;
+      __stcg(dst, v[0]);
+      __stcg(dst + s5, v[1]);
+      __stcg(dst + s6, v[2]);
+      __stcg(dst + s5 + s6, v[3]);
+    }
+    if (p + 1 < a.npass) grid_barrier(a.bar, (unsigned)(p + 1) * gridDim.x);
+  }
+}
+
 // F1 sweep on warp tiles: the grid is split into teams of `team` CTAs; team j
 // evolves replicas j, j + nteams, ... (longest first, host order) from the
 // uniform state in its own state buffer, with a team-wide barrier (its own
@@ -298,6 +412,24 @@ cudaError_t launch_warp_evolve(const WarpEvolveArgs& a, int grid, int warps, cud
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, qaa_warp_evolve, a);
+}
+
+cudaError_t launch_quad_evolve(const WarpEvolveArgs& a, int grid, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(QW_THREADS);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, qaa_quad_evolve, a);
+}
+int quad_evolve_max_active() {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, qaa_quad_evolve, QW_THREADS, 0) != cudaSuccess) return 0;
+  return nb;
 }
 
 cudaError_t launch_warp_sweep(const WarpSweepArgs& a, int grid, cudaStream_t st) {

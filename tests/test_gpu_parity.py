@@ -226,12 +226,12 @@ def test_cluster_evolve_parity(q, ctx, orc, n, K):
 
 
 @pytest.mark.parametrize("n,engine", [(13, "cluster"), (16, "cluster"), (13, "warp"), (16, "warp"), (17, "warp"),
-                                      (21, "warp")])
+                                      (21, "warp"), (13, "quad"), (16, "quad"), (19, "quad")])
 def test_small_engines_forms_and_orders(q, ctx, orc, n, engine):
     """The single-launch small-state engines (cluster-resident, n <= 16; warp-tile
     cooperative, n <= 21) with the cot form (|beta| > pi/4), Strang splitting
     (closing half step after the last pass) and the driving term."""
-    ctx.set_option(q.OPT_WARPTILE, 2 if engine == "warp" else 0)
+    ctx.set_option(q.OPT_WARPTILE, {"warp": 2, "quad": 3}.get(engine, 0))
     ctx.set_option(q.OPT_CLUSTER, 1 if engine == "cluster" else 0)
     cl = instance(n)
     E = orc.energy_table(n, cl)
@@ -254,11 +254,12 @@ def test_small_engines_forms_and_orders(q, ctx, orc, n, engine):
 
 @pytest.mark.parametrize("n", [13, 14, 15, 16, 17, 18, 19, 20, 21])
 @pytest.mark.parametrize("K", [1, 2, 6])
-def test_warp_evolve_parity(q, ctx, orc, n, K):
+@pytest.mark.parametrize("wt", [2, 3])
+def test_warp_evolve_parity(q, ctx, orc, n, K, wt):
     """13 <= n <= 21: all passes of the cyclic plan in ONE cooperative launch, one
-    warp per 2^9-amplitude tile, grid barriers between passes -- against the
-    oracle from a random state, random schedule."""
-    ctx.set_option(q.OPT_WARPTILE, 2)  # n > 16: the engine's test range
+    warp (wt 2) or four warps (wt 3, quad-warp tiles) per 2^9-amplitude tile, grid
+    barriers between passes -- against the oracle from a random state, random schedule."""
+    ctx.set_option(q.OPT_WARPTILE, wt)  # n > 16: the engine's test range
     cl = instance(n)
     psi0 = cnf.random_state(n, 60 + n)
     sched = np.random.default_rng(n * 7 + K).uniform(0, 1, K)

@@ -25,8 +25,9 @@ def inst(n):
         n, int(round(4.3 * n)), 1000 + n)
 
 
-for n in (8, 12, 13, 14, 15, 16, 18, 20, 21, 22):
-    modes = [("warp", 2, 0, 0)] if 13 <= n <= 21 else []
+NS = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [8, 12, 13, 14, 15, 16, 18, 20, 21, 22]
+for n in NS:
+    modes = [("warp", 2, 0, 0), ("quad", 3, 0, 0)] if 13 <= n <= 21 else []
     modes += [("cluster", 0, 1, 0)] if 13 <= n <= 16 else []
     modes += [("persist", 0, 0, 1), ("passes", 0, 0, 0)] if 13 <= n <= 21 else [("default", 1, 1, 0)]
     for name, wflag, cflag, persist in modes:
@@ -52,7 +53,7 @@ for n in (8, 12, 13, 14, 15, 16, 18, 20, 21, 22):
 # F1 sweep: 16 replicas, T = 1..200 at dt = 0.05 (configs[1]'s sweep style)
 Ts = np.array([1, 2, 5, 10, 20, 50, 100, 200, 3, 7, 15, 30, 70, 150, 40, 60], dtype=float)
 Ks = (Ts / 0.05).astype(np.int64)
-for n in (13, 14, 15, 16):
+for n in ([] if len(sys.argv) > 3 else (13, 14, 15, 16)):
     for name, wflag, cflag in (("warp-teams", 2, 0), ("cluster", 0, 1), ("smem-cluster", 0, 0)):
         with q.Context(0, stream=stream.cuda_stream) as c:
             c.set_option(q.OPT_WARPTILE, wflag)
