@@ -300,7 +300,8 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        per-pass kernels; a test hook), and qaa_sweep on teams of warp-tile
  *                        CTAs (n <= 21; at n = 13..16 no faster than the default
  *                        cluster-resident sweep). 3: four warps per tile, 13 <= n <= 21
- *                        (test hook above 16). 0: off.
+ *                        (test hook above 16), and qaa_sweep on teams of quad-warp CTAs
+ *                        (n <= 21; test hook: not reliably faster than the clusters). 0: off.
  *  QAA_OPT_WARP_GRID     tuning hook for the warp-tile launch: ctas * 16 + warps per CTA
  *                        (1..8); 0 (default) = automatic.
  *  QAA_OPT_SUPER_REV     1: the L2-blocked step with its two sub-passes in the other order
@@ -314,6 +315,9 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        Other configurations return QAA_E_CUDA at evolve. Default 0.
  *  QAA_OPT_ENERGY_W64    test hook: 1 = the 64-bit energy-table kernel even when every
  *                        assignment fits 32 bits (default 0: 32-bit kernel for n <= 32).
+ *  QAA_OPT_SWEEP_TUNE    tuning hook for the quad-warp team sweep: poll_ns * 16 + log2(tiles
+ *                        per CTA) + 1 (poll_ns = __nanosleep between team-barrier polls,
+ *                        <= 4095; low 4 bits 0 = automatic tiles per CTA). Default 0.
  *  QAA_OPT_ORDER         1 (default) = first-order Lie-Trotter, D then X (R7);
  *                        2 = second-order Strang splitting, D^{1/2} X D^{1/2} per step, at
  *                        the same HBM cost (the half D's of adjacent steps are merged, the
@@ -336,7 +340,8 @@ enum {
   QAA_OPT_CLUSTER = 16,
   QAA_OPT_WARPTILE = 17,
   QAA_OPT_WARP_GRID = 18,
-  QAA_OPT_SUPER_REV = 19
+  QAA_OPT_SUPER_REV = 19,
+  QAA_OPT_SWEEP_TUNE = 20
 };
 qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value);
 

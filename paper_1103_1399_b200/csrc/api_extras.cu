@@ -81,8 +81,9 @@ qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, 
   QAA_NVTX("qaa_sweep");
   CHECK_CTX();
   if (!ctx->loaded) return fail(ctx, QAA_E_STATE, "sweep before load_instance");
-  const bool wide = ctx->warptile == 2 && ctx->L <= WARP_MAX_L &&
-                    (((int64_t)1 << (ctx->L - 9)) + 7) / 8 <= ctx->num_sms;  // warp-tile teams (test hook)
+  const bool wide = (ctx->warptile == 2 && ctx->L <= WARP_MAX_L &&
+                     (((int64_t)1 << (ctx->L - 9)) + 7) / 8 <= ctx->num_sms) ||  // warp-tile teams (test hook)
+                    (ctx->warptile == 3 && ctx->L <= WARP_MAX_L);                  // quad-warp teams (test hook)
   if (ctx->world != 1 || (ctx->L > SWEEP_MAX_L && !wide))
     return fail(ctx, QAA_E_USAGE, "sweep needs world = 1 and n <= %d (state resident in one CTA or cluster)",
                 SWEEP_MAX_L);
@@ -160,15 +161,37 @@ qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, 
   double* dout = (double*)(db + ((used + 15) & ~(size_t)15));
   a.out = dout;
   const int wteam = ctx->L >= WARP_MIN_L ? (int)((((int64_t)1 << (ctx->L - 9)) + 7) / 8) : 0;
-  if (ctx->warptile == 2 && ctx->L >= WARP_MIN_L && ctx->L <= WARP_MAX_L && wteam <= ctx->num_sms) {
-    // teams of warp-tile CTAs, one replica at a time per team (warp_evolve.cu
-    // qaa_warp_sweep; QAA_OPT_WARPTILE 2: measured no faster than the clusters below
-    // at n = 13..16 -- a replica's team shares each SM among 8 tiles -- and it
-    // extends the sweep to n <= 21)
+  // quad-warp teams (QAA_OPT_WARPTILE 3, n = 13..21; a test hook: at n = 13..16 measured
+  // 4-7e5 replica-steps/s against 4.2-5.3e5 for the default clusters below, but with
+  // run-to-run outliers 3-5x slower -- team barriers of ~1000 co-resident CTAs)
+  const bool quad = ctx->L >= WARP_MIN_L && ctx->warptile == 3 && ctx->L <= WARP_MAX_L;
+  if (quad || (ctx->warptile == 2 && ctx->L >= WARP_MIN_L && ctx->L <= WARP_MAX_L && wteam <= ctx->num_sms)) {
+    // teams of CTAs, one replica at a time per team (warp_evolve.cu). Quad-warp
+    // teams (qaa_quad_sweep): 128-thread CTAs, several per SM, `tpc` tiles per CTA
+    // and pass, tpc chosen to maximise concurrent replicas / (tpc + one barrier).
+    // Single-warp teams (qaa_warp_sweep, QAA_OPT_WARPTILE 2): 8 tiles per CTA;
+    // measured no faster than the clusters below at n = 13..16, extends to n <= 21.
     qaa_status st = ensure_warp_tables(ctx);
     if (st) return st;
     const int P = warp_group_count(ctx->L);
-    const int nteams = std::min(nrep, ctx->num_sms / wteam);
+    int team = wteam, nteams = std::min(nrep, ctx->num_sms / std::max(1, wteam));
+    if (quad) {
+      const int64_t ntiles = (int64_t)1 << (ctx->L - 9);
+      const int64_t slots = (int64_t)ctx->num_sms * std::max(1, quad_sweep_max_active());
+      double best = -1.0;
+      const int64_t force = (ctx->sweep_tune & 15) ? ((int64_t)1 << ((ctx->sweep_tune & 15) - 1)) : 0;
+      for (int64_t tpc = 1; tpc <= ntiles; tpc *= 2) {
+        if (force && tpc != force) continue;
+        const int64_t tm = ntiles / tpc, nt = std::min<int64_t>(nrep, slots / tm);
+        if (nt < 1) continue;
+        const double score = (double)nt / (double)(tpc + 1);
+        if (score > best) {
+          best = score;
+          team = (int)tm;
+          nteams = (int)nt;
+        }
+      }
+    }
     std::vector<WarpPass> recs;
     std::vector<int64_t> poff((size_t)nrep), plen((size_t)nrep);
     std::vector<PassPlan> plan;
@@ -196,7 +219,7 @@ qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, 
     }
     const size_t rec_b = recs.size() * sizeof(WarpPass), arr_b = (size_t)nrep * sizeof(int64_t);
     const size_t state_b = (size_t)nteams << ctx->L << 4;
-    const size_t part_b = (size_t)nteams * wteam * 8 * sizeof(double), bar_b = (size_t)nteams * 128;
+    const size_t part_b = (size_t)nteams * team * 8 * sizeof(double), bar_b = (size_t)nteams * 128;
     const size_t o_off = (rec_b + 255) & ~(size_t)255, o_len = o_off + ((arr_b + 255) & ~(size_t)255),
                  o_state = o_len + ((arr_b + 255) & ~(size_t)255), o_part = o_state + state_b,
                  o_bar = o_part + ((part_b + 255) & ~(size_t)255), need = o_bar + bar_b;
@@ -221,12 +244,16 @@ qaa_status qaa_sweep(qaa_ctx* ctx, int nrep, const double* T, const int64_t* K, 
     wa.nrep = nrep;
     wa.phi_all = a.phi_all;
     wa.n_phi = n_phi;
-    wa.team = wteam;
+    wa.team = team;
+    wa.poll_ns = ctx->sweep_tune >> 4;
     wa.scratch = (double2*)(wb + o_state);
     wa.partial = (double*)(wb + o_part);
     wa.bar = (unsigned*)(wb + o_bar);
     wa.out = dout;
-    CUDA_TRY(launch_warp_sweep(wa, nteams * wteam, ctx->stream));
+    if (quad)
+      CUDA_TRY(launch_quad_sweep(wa, nteams * team, ctx->stream));
+    else
+      CUDA_TRY(launch_warp_sweep(wa, nteams * team, ctx->stream));
     ctx->stats.warp_launches++;
     // the host vectors above must outlive the async copies
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));

@@ -258,6 +258,7 @@ struct WarpSweepArgs {
   double* partial;         // nteams * team * 8 per-warp partial sums
   unsigned* bar;           // nteams barrier counters, 128 bytes apart (zeroed)
   double* out;             // [nrep] P_succ
+  int poll_ns;             // quad sweep: __nanosleep between team-barrier polls (0 = spin)
 };
 cudaError_t launch_warp_sweep(const WarpSweepArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_warp_energy(const uint8_t* E, uint8_t* Eg, const WarpGeo& g, int L, int num_sms, cudaStream_t st);
@@ -265,6 +266,9 @@ cudaError_t launch_warp_evolve(const WarpEvolveArgs& a, int grid, int warps, cud
 // the same plan with four warps per tile (QAA_OPT_WARPTILE 3; grid <= SMs x quad_evolve_max_active())
 cudaError_t launch_quad_evolve(const WarpEvolveArgs& a, int grid, cudaStream_t st);
 int quad_evolve_max_active();
+// F1 sweep on teams of quad-warp CTAs (WarpSweepArgs.team CTAs per replica, partial: nteams * team doubles)
+cudaError_t launch_quad_sweep(const WarpSweepArgs& a, int grid, cudaStream_t st);
+int quad_sweep_max_active();
 // 10 <= L <= 12: register-phase variant (2-3x faster than the per-qubit loop)
 cudaError_t launch_resident_phases(const ResidentArgs& a, cudaStream_t st);
 

@@ -102,7 +102,7 @@ __device__ __forceinline__ double2 ldcg2(const double2* p) {
   asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
-__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target, int poll_ns = 0) {
   __syncthreads();
   if (threadIdx.x == 0) {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
@@ -110,6 +110,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
       unsigned v;
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
       if (v >= target) break;
+      if (poll_ns) __nanosleep(poll_ns);  // many teams polling: keep the L2 slices free
     }
   }
   __syncthreads();
@@ -251,6 +252,59 @@ __device__ __forceinline__ void qw_xchg(double2* xb, double2 (&v)[4], int lane, 
   for (int r = 0; r < 4; r++) v[r] = xb[TO_P2 ? (lane | (w << 5) | (r << 7)) : (lane | (r << 5) | (w << 7))];
 }
 
+// one pass of the plan over tiles T = t0, t0 + tstep, ... < ntiles (the quad's
+// tile program of the comment above)
+__device__ __forceinline__ void qw_pass(const WarpGeo& g, const WarpPass& ps, double2* psi, const uint8_t* Eg,
+                                        const double2* phi_all, int n_phi, int64_t t0, int64_t tstep,
+                                        int64_t ntiles, int lane, int w, double2* xb) {
+  const bool pre = ps.flags & WP_PRE, d = ps.flags & WP_D, post = ps.flags & WP_POST;
+  const int fpre = (ps.flags >> 3) & 1, fpost = (ps.flags >> 4) & 1;
+  const double2* phi = phi_all + ps.d * n_phi;
+  const uint32_t rot = g.rot;
+  const uint32_t lm = rot & 31u, r1 = (rot >> 5) & 3u, r2 = (rot >> 7) & 3u;
+  // P1 offsets: lane part + warp part; register strides (tile bits 5, 6)
+  int64_t thr = 0;
+#pragma unroll
+  for (int b = 0; b < 5; b++)
+    if ((lane >> b) & 1) thr += (int64_t)1 << g.phys[b];
+#pragma unroll
+  for (int b = 0; b < 2; b++)
+    if ((w >> b) & 1) thr += (int64_t)1 << g.phys[7 + b];
+  const int64_t s5 = (int64_t)1 << g.phys[5], s6 = (int64_t)1 << g.phys[6];
+  for (int64_t T = t0; T < ntiles; T += tstep) {
+    int64_t base = 0;
+    for (int i = 0; i < g.nfree; i++)
+      if ((T >> i) & 1) base += (int64_t)1 << g.free_bits[i];
+    const double2* src = psi + base + thr;
+    double2 v[4];
+    v[0] = ldcg2(src);
+    v[1] = ldcg2(src + s5);
+    v[2] = ldcg2(src + s6);
+    v[3] = ldcg2(src + s5 + s6);
+    unsigned e[4] = {0, 0, 0, 0};
+    if (d) {
+      const uint8_t* et = Eg + (T << 9) + lane + (w << 5);
+#pragma unroll
+      for (int r = 0; r < 4; r++) e[r] = __ldg(et + (r << 7));
+    }
+    if (pre) qw_rot(v, r1, lm, ps.cpre, fpre);
+    qw_xchg<true>(xb, v, lane, w);
+    if (pre) qw_rot(v, r2, 0u, ps.cpre, fpre);
+    if (d) {
+#pragma unroll
+      for (int r = 0; r < 4; r++) v[r] = cmul(__ldg(phi + e[r]), v[r]);
+    }
+    if (post) qw_rot(v, r2, lm, ps.cpost, fpost);
+    qw_xchg<false>(xb, v, lane, w);
+    if (post) qw_rot(v, r1, 0u, ps.cpost, fpost);
+    double2* dst = psi + base + thr;
+    __stcg(dst, v[0]);
+    __stcg(dst + s5, v[1]);
+    __stcg(dst + s6, v[2]);
+    __stcg(dst + s5 + s6, v[3]);
+  }
+}
+
 __global__ void __launch_bounds__(QW_THREADS) qaa_quad_evolve(const WarpEvolveArgs a) {
   __shared__ __align__(16) double2 xb[512];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -259,55 +313,68 @@ __global__ void __launch_bounds__(QW_THREADS) qaa_quad_evolve(const WarpEvolveAr
   for (int64_t p = 0; p < a.npass; p++) {
     const WarpPass ps = nx;
     if (p + 1 < a.npass) nx = a.plan[p + 1];
-    const WarpGeo& g = a.geo[ps.group];
-    const uint8_t* Eg = a.Eg[ps.group];
-    const bool pre = ps.flags & WP_PRE, d = ps.flags & WP_D, post = ps.flags & WP_POST;
-    const int fpre = (ps.flags >> 3) & 1, fpost = (ps.flags >> 4) & 1;
-    const double2* phi = a.phi_all + ps.d * a.n_phi;
-    const uint32_t rot = g.rot;
-    const uint32_t lm = rot & 31u, r1 = (rot >> 5) & 3u, r2 = (rot >> 7) & 3u;
-    // P1 offsets: lane part + warp part; register strides (tile bits 5, 6)
-    int64_t thr = 0;
-#pragma unroll
-    for (int b = 0; b < 5; b++)
-      if ((lane >> b) & 1) thr += (int64_t)1 << g.phys[b];
-#pragma unroll
-    for (int b = 0; b < 2; b++)
-      if ((w >> b) & 1) thr += (int64_t)1 << g.phys[7 + b];
-    const int64_t s5 = (int64_t)1 << g.phys[5], s6 = (int64_t)1 << g.phys[6];
-    for (int64_t T = blockIdx.x; T < ntiles; T += gridDim.x) {
-      int64_t base = 0;
-      for (int i = 0; i < g.nfree; i++)
-        if ((T >> i) & 1) base += (int64_t)1 << g.free_bits[i];
-      const double2* src = a.psi + base + thr;
-      double2 v[4];
-      v[0] = ldcg2(src);
-      v[1] = ldcg2(src + s5);
-      v[2] = ldcg2(src + s6);
-      v[3] = ldcg2(src + s5 + s6);
-      unsigned e[4] = {0, 0, 0, 0};
-      if (d) {
-        const uint8_t* et = Eg + (T << 9) + lane + (w << 5);
-#pragma unroll
-        for (int r = 0; r < 4; r++) e[r] = __ldg(et + (r << 7));
-      }
-      if (pre) qw_rot(v, r1, lm, ps.cpre, fpre);
-      qw_xchg<true>(xb, v, lane, w);
-      if (pre) qw_rot(v, r2, 0u, ps.cpre, fpre);
-      if (d) {
-#pragma unroll
-        for (int r = 0; r < 4; r++) v[r] = cmul(__ldg(phi + e[r]), v[r]);
-      }
-      if (post) qw_rot(v, r2, lm, ps.cpost, fpost);
-      qw_xchg<false>(xb, v, lane, w);
-      if (post) qw_rot(v, r1, 0u, ps.cpost, fpost);
-      double2* dst = a.psi + base + thr;
-      __stcg(dst, v[0]);
-      __stcg(dst + s5, v[1]);
-      __stcg(dst + s6, v[2]);
-      __stcg(dst + s5 + s6, v[3]);
-    }
+    qw_pass(a.geo[ps.group], ps, a.psi, a.Eg[ps.group], a.phi_all, a.n_phi, blockIdx.x, gridDim.x, ntiles, lane,
+            w, xb);
     if (p + 1 < a.npass) grid_barrier(a.bar, (unsigned)(p + 1) * gridDim.x);
+  }
+}
+
+// F1 sweep on quad-warp tiles: teams of `team` 128-thread CTAs (several per SM),
+// team j evolves replicas j, j + nteams, ... (longest first) from the uniform
+// state in its own buffer, a team barrier between passes, and leaves P_succ in
+// out[] (fixed-order reduction: lanes, warps, then CTAs in id order).
+__global__ void __launch_bounds__(QW_THREADS) qaa_quad_sweep(const WarpSweepArgs a) {
+  __shared__ __align__(16) double2 xb[512];
+  __shared__ double red[4];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int team = a.team, nteams = gridDim.x / team;
+  const int j = blockIdx.x / team, lc = blockIdx.x % team;
+  if (j >= nteams) return;
+  const int64_t ntiles = (int64_t)1 << (a.L - 9);
+  double2* psi = a.scratch + ((int64_t)j << a.L);
+  double* part = a.partial + (int64_t)j * team;
+  unsigned* ctr = a.bar + 32 * j;
+  unsigned epoch = 0;
+  const int64_t N = (int64_t)1 << a.L;
+  for (int rep = j; rep < a.nrep; rep += nteams) {
+    for (int64_t i = (int64_t)lc * QW_THREADS + threadIdx.x; i < N; i += (int64_t)team * QW_THREADS)
+      __stcg(psi + i, make_double2(a.amp0, 0.0));
+    grid_barrier(ctr, ++epoch * (unsigned)team, a.poll_ns);
+    const WarpPass* plan = a.plan + a.plan_off[rep];
+    const int64_t np = a.plan_len[rep];
+    for (int64_t p = 0; p < np; p++) {
+      const WarpPass ps = plan[p];
+      qw_pass(a.geo[ps.group], ps, psi, a.Eg[ps.group], a.phi_all, a.n_phi, lc, team, ntiles, lane, w, xb);
+      grid_barrier(ctr, ++epoch * (unsigned)team, a.poll_ns);
+    }
+    // P_succ over this CTA's group-0 tiles (group 0: tile bit b = physical bit b)
+    double acc = 0.0;
+    const WarpGeo& g0 = a.geo[0];
+    for (int64_t T = lc; T < ntiles; T += team) {
+      int64_t base = 0;
+      for (int i = 0; i < g0.nfree; i++)
+        if ((T >> i) & 1) base += (int64_t)1 << g0.free_bits[i];
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const int l = threadIdx.x + QW_THREADS * r;
+        if (__ldg(a.Eg[0] + (T << 9) + l) == 0) {
+          const double2 v = ldcg2(psi + base + l);
+          acc += fma(v.x, v.x, v.y * v.y);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[w] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) part[lc] = ((red[0] + red[1]) + red[2]) + red[3];
+    grid_barrier(ctr, ++epoch * (unsigned)team, a.poll_ns);
+    if (lc == 0 && threadIdx.x == 0) {
+      double sum = 0.0;
+      for (int c = 0; c < team; c++) sum += __ldcg(part + c);  // other SMs wrote them: bypass L1
+      a.out[rep] = sum;
+    }
+    grid_barrier(ctr, ++epoch * (unsigned)team, a.poll_ns);  // part[] and psi are reused by the next replica
   }
 }
 
@@ -425,6 +492,23 @@ cudaError_t launch_quad_evolve(const WarpEvolveArgs& a, int grid, cudaStream_t s
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, qaa_quad_evolve, a);
+}
+cudaError_t launch_quad_sweep(const WarpSweepArgs& a, int grid, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(QW_THREADS);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, qaa_quad_sweep, a);
+}
+int quad_sweep_max_active() {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, qaa_quad_sweep, QW_THREADS, 0) != cudaSuccess) return 0;
+  return nb;
 }
 int quad_evolve_max_active() {
   int nb = 0;

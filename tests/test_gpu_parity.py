@@ -674,7 +674,8 @@ def test_strang_parity(q, ctx, orc, n, span, kernel):
 
 
 @pytest.mark.parametrize("n,engine", [(6, "cluster"), (8, "cluster"), (10, "cluster"), (11, "cluster"), (12, "cluster")] +
-                         [(n, e) for n in (13, 14, 15, 16) for e in ("warp2", "cluster", "smem")] + [(18, "warp2")])
+                         [(n, e) for n in (13, 14, 15, 16) for e in ("quad3", "warp2", "cluster", "smem")] +
+                         [(18, "warp2"), (18, "quad3"), (21, "quad3")])
 @pytest.mark.parametrize("order", [1, 2])
 def test_sweep_parity(q, ctx, orc, n, engine, order):
     """NEXT F1: batched T sweep (one CTA per replica up to n = 12 -- per-qubit
@@ -682,10 +683,11 @@ def test_sweep_parity(q, ctx, orc, n, engine, order):
     register-resident cluster of 2^(n-12) CTAs per replica (default), or with
     QAA_OPT_CLUSTER 0 the shared-memory cluster of 2^(n-13) CTAs with per-bit DSMEM
     phases, or with QAA_OPT_WARPTILE 2 teams of warp-tile CTAs, one replica per team
-    at a time -- also n = 18) against one oracle run per replica (configs[1]-style
-    sweep T in {1,2,5,10,20} at dt = 0.05)."""
+    at a time -- also n = 18; or with QAA_OPT_WARPTILE 3 teams of quad-warp CTAs,
+    n = 13..21) against one oracle run per replica (configs[1]-style sweep T in
+    {1,2,5,10,20} at dt = 0.05)."""
     cl = cnf.paper_instance()[1] if n == 6 else instance(n)
-    ctx.set_option(q.OPT_WARPTILE, {"warp": 1, "warp2": 2}.get(engine, 0))
+    ctx.set_option(q.OPT_WARPTILE, {"quad": 1, "warp2": 2, "quad3": 3}.get(engine, 0))
     ctx.set_option(q.OPT_CLUSTER, 1 if engine == "cluster" else 0)
     ctx.set_option(q.OPT_ORDER, order)
     ctx.load_instance(n, cl)

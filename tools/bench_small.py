@@ -54,7 +54,7 @@ for n in NS:
 Ts = np.array([1, 2, 5, 10, 20, 50, 100, 200, 3, 7, 15, 30, 70, 150, 40, 60], dtype=float)
 Ks = (Ts / 0.05).astype(np.int64)
 for n in ([] if len(sys.argv) > 3 else (13, 14, 15, 16)):
-    for name, wflag, cflag in (("warp-teams", 2, 0), ("cluster", 0, 1), ("smem-cluster", 0, 0)):
+    for name, wflag, cflag in (("quad-teams", 3, 0), ("warp-teams", 2, 0), ("cluster", 0, 1), ("smem-cluster", 0, 0)):
         with q.Context(0, stream=stream.cuda_stream) as c:
             c.set_option(q.OPT_WARPTILE, wflag)
             c.set_option(q.OPT_CLUSTER, cflag)
