@@ -1,5 +1,6 @@
-"""One evolve of the warp-tile launch (n = 16, K = 200) and one of the
-cluster-resident launch (n = 14, K = 200), for ncu (tools/gpu_profile_round.sh)."""
+"""One evolve of the quad-warp-tile launch (default, n = 16, K = 200), of the
+single-warp-tile launch (n = 16) and of the cluster-resident launch (n = 14),
+for ncu (tools/gpu_profile_round.sh)."""
 import os
 import sys
 
@@ -8,7 +9,7 @@ sys.path.insert(0, ROOT)
 import paper_1103_1399_b200 as q  # noqa: E402
 from inputs import cnf  # noqa: E402
 
-for n, wt in ((16, 1), (14, 0)):
+for n, wt in ((16, 1), (16, 2), (14, 0)):
     with q.Context(0) as c:
         c.set_option(q.OPT_WARPTILE, wt)
         c.load_instance(n, cnf.load_instance(n)[0])
