@@ -315,6 +315,9 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        Other configurations return QAA_E_CUDA at evolve. Default 0.
  *  QAA_OPT_ENERGY_W64    test hook: 1 = the 64-bit energy-table kernel even when every
  *                        assignment fits 32 bits (default 0: 32-bit kernel for n <= 32).
+ *  QAA_OPT_SUPER_PUB     L2-blocked step: group-0 tiles of one chunk a warp publishes with ONE
+ *                        gpu-scope release (1..8, default 1; each release's fence waits for
+ *                        all of the warp's earlier stores).
  *  QAA_OPT_SWEEP_TUNE    tuning hook for the quad-warp team sweep: poll_ns * 16 + log2(tiles
  *                        per CTA) + 1 (poll_ns = __nanosleep between team-barrier polls,
  *                        <= 4095; low 4 bits 0 = automatic tiles per CTA). Default 0.
@@ -341,7 +344,8 @@ enum {
   QAA_OPT_WARPTILE = 17,
   QAA_OPT_WARP_GRID = 18,
   QAA_OPT_SUPER_REV = 19,
-  QAA_OPT_SWEEP_TUNE = 20
+  QAA_OPT_SWEEP_TUNE = 20,
+  QAA_OPT_SUPER_PUB = 21
 };
 qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value);
 

@@ -188,6 +188,10 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
         return fail(ctx, QAA_E_USAGE, "warp grid must be 0 or ctas * 16 + warps (1..8)");
       ctx->warp_grid = (int)value;
       return QAA_OK;
+    case QAA_OPT_SUPER_PUB:
+      if (value < 1 || value > 8) return fail(ctx, QAA_E_USAGE, "super pub must be in 1..8");
+      ctx->super_pub = (int)value;
+      return QAA_OK;
     case QAA_OPT_SWEEP_TUNE:
       if (value < 0 || value >= (4096 << 4)) return fail(ctx, QAA_E_USAGE, "sweep tune must be in 0..65535");
       ctx->sweep_tune = (int)value;

@@ -124,6 +124,7 @@ struct qaa_ctx {
   int cluster_evolve = 1;  // QAA_OPT_CLUSTER: 13 <= L <= 16 in one cluster-resident launch
   int warptile = 1;        // QAA_OPT_WARPTILE: 13 <= L <= 21 in one warp-tile cooperative launch
   int warp_grid = 0;       // QAA_OPT_WARP_GRID: ctas * 16 + warps (0 = automatic)
+  int super_pub = 1;       // QAA_OPT_SUPER_PUB: group-0 tiles per release in the L2-blocked step
   int sweep_tune = 0;      // QAA_OPT_SWEEP_TUNE: poll_ns * 16 + log2(tiles per CTA) + 1 (0 = automatic)
   bool wt_built = false;   // Ewt / wgeo match the loaded instance
   int wt_groups = 0;

@@ -362,13 +362,18 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
   uint32_t late_phase = 0;
   double2 v[RPT];
   War war{V2 ? &slot_consumed(sm)[g] : nullptr, 0};
-  int pend = -1;  // V2: chunk of this warp's unpublished group-0 tile
+  int pend = -1;        // V2: chunk of this warp's unpublished group-0 tiles
+  unsigned pcnt = 0;    // ... and how many (all of chunk pend)
   const unsigned chunk_done = 1u << (a.tpc_bits + a.done_shift);
+  // one gpu-scope release per publish: its fence waits for ALL of the warp's
+  // earlier stores, so batching pub_batch tiles of a chunk into one release cuts
+  // the fence stalls (at the price of completing a chunk up to a tile later)
   auto publish = [&]() {
     if (V2 && pend >= 0) {
       __syncwarp();
-      if (lane == 0) red_release_add(&a.done[pend], 1u);
+      if (lane == 0) red_release_add(&a.done[pend], pcnt);
       pend = -1;
+      pcnt = 0;
     }
   };
   for (int64_t J = g;; J += NG) {
@@ -441,7 +446,9 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
       if (a.tm_flags & 1) publish();
       program<FP_G0_PRE, false, V2, DIAG>(a.g0, v, xb, nullptr, phis, lane, lw, g, war);
     }
-    publish();  // the previous group-0 tile's stores have drained by now
+    // the previous group-0 tiles' stores have drained by now; keep batching while
+    // this tile is a group-0 tile of the same chunk
+    if (!(pcnt < (unsigned)a.pub_batch && !gkt && !REV && m.c == pend)) publish();
     // group-k tile stored by ONE TMA tensor store from the slot (tm_flags 4, v2):
     // write-after-read guard, tile-local STS, proxy fence, group barrier; the
     // storing thread refills the slot once the store has read it
@@ -479,6 +486,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
 #pragma unroll
         for (int r = 0; r < RPT; r++) st_hint(dst + roff(psk, r), v[r], pol_keep);
         pend = m.c;
+        pcnt++;
       } else {
         double2* dst = a.g0.psi + tbase(a.g0, m.T);
 #pragma unroll
@@ -508,6 +516,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
       }
       if (V2) {
         pend = m.c;  // published one tile later (publish() above)
+        pcnt++;
         if (a.tm_flags & 2) publish();
       } else {
         // publish: the group's stores of this group-0 tile happen before the

@@ -242,9 +242,12 @@ __device__ __forceinline__ void qw_rot(double2 (&v)[4], uint32_t regmask, uint32
   if (form == 0) qw_rot_t<0>(v, regmask, lanemask, c);
   else qw_rot_t<1>(v, regmask, lanemask, c);
 }
+// Two buffers (P1 -> P2 in xb, P2 -> P1 in xb + 512): a thread's last read of one
+// buffer precedes its arrival at the other buffer's barrier, so each exchange
+// needs only the barrier between its stores and its loads.
 template <bool TO_P2>
 __device__ __forceinline__ void qw_xchg(double2* xb, double2 (&v)[4], int lane, int w) {
-  __syncthreads();  // every thread's reads of the previous exchange are done
+  if (!TO_P2) xb += 512;
 #pragma unroll
   for (int r = 0; r < 4; r++) xb[TO_P2 ? (lane | (r << 5) | (w << 7)) : (lane | (w << 5) | (r << 7))] = v[r];
   __syncthreads();
@@ -281,18 +284,20 @@ __device__ __forceinline__ void qw_pass(const WarpGeo& g, const WarpPass& ps, do
     v[1] = ldcg2(src + s5);
     v[2] = ldcg2(src + s6);
     v[3] = ldcg2(src + s5 + s6);
-    unsigned e[4] = {0, 0, 0, 0};
+    // D factors: looked up as soon as the energies land, so the (per-pass, L1-cold)
+    // phi row load overlaps the pre rotations and the first exchange
+    double2 f[4];
     if (d) {
       const uint8_t* et = Eg + (T << 9) + lane + (w << 5);
 #pragma unroll
-      for (int r = 0; r < 4; r++) e[r] = __ldg(et + (r << 7));
+      for (int r = 0; r < 4; r++) f[r] = __ldg(phi + __ldg(et + (r << 7)));
     }
     if (pre) qw_rot(v, r1, lm, ps.cpre, fpre);
     qw_xchg<true>(xb, v, lane, w);
     if (pre) qw_rot(v, r2, 0u, ps.cpre, fpre);
     if (d) {
 #pragma unroll
-      for (int r = 0; r < 4; r++) v[r] = cmul(__ldg(phi + e[r]), v[r]);
+      for (int r = 0; r < 4; r++) v[r] = cmul(f[r], v[r]);
     }
     if (post) qw_rot(v, r2, lm, ps.cpost, fpost);
     qw_xchg<false>(xb, v, lane, w);
@@ -306,7 +311,7 @@ __device__ __forceinline__ void qw_pass(const WarpGeo& g, const WarpPass& ps, do
 }
 
 __global__ void __launch_bounds__(QW_THREADS) qaa_quad_evolve(const WarpEvolveArgs a) {
-  __shared__ __align__(16) double2 xb[512];
+  __shared__ __align__(16) double2 xb[1024];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t ntiles = (int64_t)1 << (a.L - 9);
   WarpPass nx = a.plan[0];
@@ -324,7 +329,7 @@ __global__ void __launch_bounds__(QW_THREADS) qaa_quad_evolve(const WarpEvolveAr
 // state in its own buffer, a team barrier between passes, and leaves P_succ in
 // out[] (fixed-order reduction: lanes, warps, then CTAs in id order).
 __global__ void __launch_bounds__(QW_THREADS) qaa_quad_sweep(const WarpSweepArgs a) {
-  __shared__ __align__(16) double2 xb[512];
+  __shared__ __align__(16) double2 xb[1024];
   __shared__ double red[4];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int team = a.team, nteams = gridDim.x / team;

@@ -19,7 +19,7 @@ __all__ = [
     "qaa_init_basis", "qaa_evolve", "qaa_sweep", "qaa_time_energy_table", "qaa_set_driver", "qaa_spectrum", "qaa_success_prob", "qaa_energy", "qaa_norm2", "qaa_sigma_x",
     "qaa_num_solutions", "qaa_max_energy", "qaa_copy_state", "qaa_set_state", "qaa_copy_energy_table",
     "qaa_state_ptr", "qaa_set_option", "qaa_get_stats", "qaa_reset_stats", "qaa_plan_describe",
-    "qaa_version", "OPT_ROW_BITS", "OPT_PROFILE", "OPT_STEP_SPANNING", "OPT_CTAS_PER_SM", "OPT_KERNEL", "OPT_TMA_GROUPS", "OPT_SUPER", "OPT_ORDER", "OPT_ENERGY_W64", "OPT_SUPER_GRID", "OPT_SUPER_SPLIT", "OPT_SHARD_SYNC", "OPT_PERSIST", "OPT_DIAG", "OPT_CLUSTER", "OPT_WARPTILE", "OPT_WARP_GRID", "OPT_SUPER_REV", "OPT_SWEEP_TUNE",
+    "qaa_version", "OPT_ROW_BITS", "OPT_PROFILE", "OPT_STEP_SPANNING", "OPT_CTAS_PER_SM", "OPT_KERNEL", "OPT_TMA_GROUPS", "OPT_SUPER", "OPT_ORDER", "OPT_ENERGY_W64", "OPT_SUPER_GRID", "OPT_SUPER_SPLIT", "OPT_SHARD_SYNC", "OPT_PERSIST", "OPT_DIAG", "OPT_CLUSTER", "OPT_WARPTILE", "OPT_WARP_GRID", "OPT_SUPER_REV", "OPT_SWEEP_TUNE", "OPT_SUPER_PUB",
     "PLAN_RECORD", "SHARD_RECORD", "TorchComm", "qaa_plan_describe_sharded",
 ]
 
@@ -41,6 +41,7 @@ OPT_WARPTILE = 17
 OPT_WARP_GRID = 18
 OPT_SUPER_REV = 19
 OPT_SWEEP_TUNE = 20
+OPT_SUPER_PUB = 21
 PLAN_RECORD = 10
 SHARD_RECORD = 10
 
