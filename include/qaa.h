@@ -315,9 +315,11 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        Other configurations return QAA_E_CUDA at evolve. Default 0.
  *  QAA_OPT_ENERGY_W64    test hook: 1 = the 64-bit energy-table kernel even when every
  *                        assignment fits 32 bits (default 0: 32-bit kernel for n <= 32).
- *  QAA_OPT_SUPER_PUB     L2-blocked step: group-0 tiles of one chunk a warp publishes with ONE
- *                        gpu-scope release (1..8, default 1; each release's fence waits for
- *                        all of the warp's earlier stores).
+ *  QAA_OPT_SUPER_PUB     L2-blocked step: batch + 16 * early. batch = group-0 tiles of one
+ *                        chunk a warp publishes with ONE gpu-scope release (1..8, default 1;
+ *                        each release's fence waits for all of the warp's earlier stores);
+ *                        early = 1: a tile's shared-memory slot is released before the last
+ *                        three register-bit rotations of its program (refill starts earlier).
  *  QAA_OPT_SWEEP_TUNE    tuning hook for the quad-warp team sweep: poll_ns * 16 + log2(tiles
  *                        per CTA) + 1 (poll_ns = __nanosleep between team-barrier polls,
  *                        <= 4095; low 4 bits 0 = automatic tiles per CTA). Default 0.

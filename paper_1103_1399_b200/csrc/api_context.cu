@@ -189,7 +189,8 @@ qaa_status qaa_set_option(qaa_ctx* ctx, int key, int64_t value) {
       ctx->warp_grid = (int)value;
       return QAA_OK;
     case QAA_OPT_SUPER_PUB:
-      if (value < 1 || value > 8) return fail(ctx, QAA_E_USAGE, "super pub must be in 1..8");
+      if ((value & 15) < 1 || (value & 15) > 8 || value > 31)
+        return fail(ctx, QAA_E_USAGE, "super pub must be batch (1..8) + 16 * early (0/1)");
       ctx->super_pub = (int)value;
       return QAA_OK;
     case QAA_OPT_SWEEP_TUNE:

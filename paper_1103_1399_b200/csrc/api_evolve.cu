@@ -108,7 +108,8 @@ static qaa_status launch_super_pair(qaa_ctx* ctx, int k, double t_g0, double t_p
   a.doneB = a.done + a.nchunks;
   a.split_a = ctx->super_split;
   a.v2 = ctx->super_v2 && !ctx->super_split;
-  a.pub_batch = ctx->super_pub;
+  a.pub_batch = ctx->super_pub & 15;
+  a.early = (ctx->super_pub >> 4) & 1;
   a.tm_flags = ctx->super_tm_flags;  // v2: 1 = publish after the next landed read, 2 = right after the stores
   a.diag = ctx->diag;
   a.rev = rev ? 1 : 0;

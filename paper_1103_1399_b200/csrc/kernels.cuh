@@ -146,6 +146,7 @@ struct SuperArgs {
   int done_shift;      // done[c] counts 2^done_shift arrivals per tile (3: one per warp: pass_tmem.cu, v2)
   int v2;              // qaa_superpass: split-phase WAR guards + deferred per-warp publish (default 1)
   int pub_batch;       // v2: group-0 tiles of one chunk a warp publishes with ONE release (default 1)
+  int early;           // v2 with D: release a slot before the final 3 register-bit rotations (EARLY)
   int diag;            // QAA_OPT_DIAG: diagnostic kernel variant (work removed; wrong results by design)
   int rev;             // reversed pair: A items = group-k rotate/D/rotate tiles, B items = group-0 tiles
   int tm_flags;        // pass_tmem.cu A/B switches: 1 = group-0 slot released at the tile's end,

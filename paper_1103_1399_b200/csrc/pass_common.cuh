@@ -342,6 +342,17 @@ __device__ __forceinline__ Off make_off(const A& a, int lane, int warp) {
   return make_off_tl(a, pat_tl<P>(lane, warp), rb);
 }
 // rotate the 4 register bits of pattern P with per-tile-bit coefficients t[.]
+// register bits I0 <= i < I1 of pattern P only (rot_regs = 0..4)
+template <int P, int I0, int I1>
+__device__ __forceinline__ void rot_regs_range(double2 (&v)[RPT], const double (&t)[TILE_BITS]) {
+#pragma unroll
+  for (int i = I0; i < I1; i++) {
+    const double c = t[reg_shift<P>() + i];
+#pragma unroll
+    for (int r = 0; r < RPT; r++)
+      if (!(r & (1 << i))) rot2(v[r], v[r | (1 << i)], c);
+  }
+}
 template <int P>
 __device__ __forceinline__ void rot_regs(double2 (&v)[RPT], const double (&t)[TILE_BITS]) {
 #pragma unroll

@@ -128,7 +128,11 @@ __device__ __forceinline__ void diag(double2 (&v)[RPT], const uint8_t* es, const
   }
 }
 
-template <int PROG, bool LANE3, bool SPLIT = false, int DIAG = 0>
+// EARLY: the final PA rotation stops after its first register bit (which reads
+// every register, so the last exchange's loads have landed); the caller releases
+// the slot and then applies bits 1..3 (program_tail) -- the slot's refill starts
+// that much earlier
+template <int PROG, bool LANE3, bool SPLIT = false, int DIAG = 0, bool EARLY = false>
 __device__ __forceinline__ void program(const TmaArgs& a, double2 (&v)[RPT], double2* xb, const uint8_t* es,
                                         const double2* phis, int lane, int warp, int g, War& w) {
   static_assert(!SPLIT || PROG == FP_G0_PRE || PROG == FP_GK_PRE || PROG == FP_GK_PRE_D_POST,
@@ -149,7 +153,7 @@ __device__ __forceinline__ void program(const TmaArgs& a, double2 (&v)[RPT], dou
     if (!(DIAG & 2)) war_arrive<SPLIT>(w);
     if (!(DIAG & 1)) rot_regs<PC>(v, t0);
     if (!(DIAG & 2)) xchg_s<PC, PA, SPLIT>(xb, v, lane, warp, g, w);
-    if (!(DIAG & 1)) rot_regs<PA>(v, t0);
+    if (!(DIAG & 1)) rot_regs_range<PA, 0, EARLY ? 1 : 4>(v, t0);
   } else if (PROG == FP_G0_PRE_D_POST) {
     rot_regs<PA>(v, t0);
     xchg<PA, PC>(xb, v, lane, warp, g);
@@ -188,8 +192,14 @@ __device__ __forceinline__ void program(const TmaArgs& a, double2 (&v)[RPT], dou
       if (!(DIAG & 1)) rot_regs<PB>(v, t1);
     }
     if (!(DIAG & 2)) xchg_s<PB, PA, SPLIT>(xb, v, lane, warp, g, w);
-    if (!(DIAG & 1)) rot_regs<PA>(v, t1);
+    if (!(DIAG & 1)) rot_regs_range<PA, 0, EARLY ? 1 : 4>(v, t1);
   }
+}
+// the rest of an EARLY program's final PA rotation
+template <int PROG>
+__device__ __forceinline__ void program_tail(const TmaArgs& a, double2 (&v)[RPT]) {
+  static_assert(PROG == FP_G0_PRE || PROG == FP_GK_PRE_D_POST, "EARLY: L2-blocked step programs only");
+  rot_regs_range<PA, 1, 4>(v, PROG == FP_G0_PRE ? a.t[0] : a.t[1]);
 }
 
 template <int PROG>
@@ -327,9 +337,10 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_pass_tma(const __grid_co
 // its 1/8 of the tile to done[c] (red.release) at its next tile's first exchange,
 // when its stores have drained -- or before any wait on a chunk and at the end,
 // so a chunk's count can never wait on a warp that waits for it.
-template <bool LANE3, int NG, bool BD, bool V2, int DIAG = 0, bool REV = false>
+template <bool LANE3, int NG, bool BD, bool V2, int DIAG = 0, bool REV = false, bool EARLY = false>
 __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_constant__ CUtensorMap kmap,
                                                                  const SuperArgs a) {
+  static_assert(!EARLY || (BD && V2 && !REV && DIAG == 0), "EARLY slot release: default step only");
   constexpr int BPROG = BD ? FP_GK_PRE_D_POST : FP_GK_PRE;
   extern __shared__ __align__(128) unsigned char sm[];
   double2* slots = reinterpret_cast<double2*>(sm);
@@ -440,12 +451,18 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
     if (gkt) {
       load_landed<Info<BPROG>::load_pat>(v, xb, lane, lw);
       if (a.tm_flags & 1) publish();
-      program<BPROG, LANE3, V2, DIAG>(a.gk, v, xb, es, phis, lane, lw, g, war);
+      program<BPROG, LANE3, V2, DIAG, EARLY>(a.gk, v, xb, es, phis, lane, lw, g, war);
     } else {
       load_landed<Info<FP_G0_PRE>::load_pat>(v, xb, lane, lw);
       if (a.tm_flags & 1) publish();
-      program<FP_G0_PRE, false, V2, DIAG>(a.g0, v, xb, nullptr, phis, lane, lw, g, war);
+      program<FP_G0_PRE, false, V2, DIAG, EARLY>(a.g0, v, xb, nullptr, phis, lane, lw, g, war);
     }
+    auto tail = [&]() {
+      if (EARLY) {
+        if (gkt) program_tail<FP_GK_PRE_D_POST>(a.gk, v);
+        else program_tail<FP_G0_PRE>(a.g0, v);
+      }
+    };
     // the previous group-0 tiles' stores have drained by now; keep batching while
     // this tile is a group-0 tile of the same chunk
     if (!(pcnt < (unsigned)a.pub_batch && !gkt && !REV && m.c == pend)) publish();
@@ -454,6 +471,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
     // storing thread refills the slot once the store has read it
     const bool tstore = !REV && V2 && BD && isb && (a.tm_flags & 4) && !a.gk.contiguous && !(DIAG & 32);
     if (tstore) {
+      tail();
       war_arrive<true>(war);  // the final rotations consumed every value read from the slot
       mbar_wait(war.bar, war.ph & 1);
       war.ph++;
@@ -478,6 +496,7 @@ __global__ void __launch_bounds__(NG * NTHREADS, 1) qaa_superpass(const __grid_c
     }
     __syncwarp();
     if (lane == 0 && last_warp_out(&cnt[s])) super_issue<NG, BD, REV>(&kmap, a, J + TMA_SLOTS, slots, eslots, full, meta, pol_dead);
+    tail();
     if (REV) {
       // group-k tiles (A items) keep their output in L2 for the group-0 sub-pass;
       // group-0 tiles (B items) are the step's final, contiguous HBM write-back
@@ -733,6 +752,9 @@ SuperKernel pick_super_diag(int diag) {
 SuperKernel pick_super_rev(bool lane3) {
   return lane3 ? qaa_superpass<true, 2, true, true, 0, true> : qaa_superpass<false, 2, true, true, 0, true>;
 }
+SuperKernel pick_super_early(bool lane3) {
+  return lane3 ? qaa_superpass<true, 2, true, true, 0, false, true> : qaa_superpass<false, 2, true, true, 0, false, true>;
+}
 SuperKernel pick_super(bool lane3, int ng, bool bd, bool v2) {
   if (v2) return bd ? pick_super_bd<true, true>(lane3, ng) : pick_super_bd<false, true>(lane3, ng);
   return bd ? pick_super_bd<true, false>(lane3, ng) : pick_super_bd<false, false>(lane3, ng);
@@ -765,6 +787,7 @@ cudaError_t launch_superpass(const CUtensorMap* kmap, const SuperArgs& a, bool l
     if (!bd || !a.v2 || ngroups != 2) return cudaErrorInvalidValue;
     k = pick_super_rev(lane3);
   }
+  if (a.early && bd && a.v2 && ngroups == 2 && !a.rev && !a.diag) k = pick_super_early(lane3);
   if (a.diag && bd) {  // the D-less closing pair keeps the real kernel
     if (!lane3 || ngroups != 2 || !a.v2 || !pick_super_diag(a.diag)) return cudaErrorInvalidValue;
     k = pick_super_diag(a.diag);
@@ -817,6 +840,8 @@ cudaError_t pass_tma_setup() {
   for (int l = 0; l < 2; l++) {
     cudaError_t e = cudaFuncSetAttribute(pick_super_rev(l), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)TMA_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(pick_super_early(l), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM_BYTES);
     if (e != cudaSuccess) return e;
   }
   for (int d = 1; d < 128; d++)

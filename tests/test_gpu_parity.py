@@ -505,9 +505,10 @@ def test_super_v2_sync_bitwise(q, n):
     cl = instance(n)
     sched = np.random.default_rng(7 * n).uniform(0, 1, 5)
     out = []
-    for sup in (17, 17 | 32768, 17 | 512):
+    for sup, pub in ((17, 1), (17 | 32768, 1), (17 | 512, 1), (17, 3), (17, 16 + 2)):
         with q.Context(0) as c:
             c.set_option(q.OPT_SUPER, sup)
+            c.set_option(q.OPT_SUPER_PUB, pub)
             c.load_instance(n, cl)
             c.set_state(cnf.random_state(n, 5 + n))
             c.evolve(1.7, 5, sched)
@@ -515,6 +516,9 @@ def test_super_v2_sync_bitwise(q, n):
             out.append(c.state())
     assert np.array_equal(out[0].view(np.uint64), out[1].view(np.uint64))
     assert np.array_equal(out[0].view(np.uint64), out[2].view(np.uint64))  # TMA tensor stores (bit 9)
+    # batched publish (QAA_OPT_SUPER_PUB 3) and early slot release with batch 2 (16 + 2)
+    assert np.array_equal(out[0].view(np.uint64), out[3].view(np.uint64))
+    assert np.array_equal(out[0].view(np.uint64), out[4].view(np.uint64))
 
 
 @pytest.mark.parametrize("n", [22, 25])
