@@ -451,6 +451,14 @@ def run_ours(args):
                 "algorithmic_gbs_33B": 33 * amps * trotter / (ms / 1e3) / 1e9,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
                 "clocks": clocks, "p_succ_last": p_succ}
+        if world > 1:
+            # the global-qubit exchange: one layout swap per Trotter step, each GPU
+            # storing (W-1)/W of its 16 B/amp shard into the peers' buffers
+            nv = 16 * amps * (world - 1) / world * trotter
+            line["nvlink"] = {"bytes_per_step_per_gpu": 16 * amps * (world - 1) / world,
+                              "achieved_gbs_per_gpu": nv / (ms / 1e3) / 1e9, "peak_gbs_per_gpu": 900.0,
+                              "peak_source": "NVLink 5, 900 GB/s per direction per GPU (nominal)",
+                              "note": "peer stores fused into the swap launch; time is the whole step's"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
