@@ -405,7 +405,7 @@ def run_ours(args):
         h2d = 32 * len(cl) + chunk * ((emax + 1) * 16 + 12)
         d2h = 16 + 8
         e2e = {"value": world * e2e_steps * chunk / e2e_s,
-               "unit": "steps/s" if world == 1 else "shard-steps/s (2^30 amplitudes per shard)",
+               "unit": "steps/s" if world == 1 else f"shard-steps/s (2^{L} amplitudes per shard)",
                "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                "includes": "load_instance (H2D clauses, energy table, Z) + init + evolve(window) + success_prob (D2H)"}
@@ -427,7 +427,7 @@ def run_ours(args):
                    "sample": f"failed: {e}"}
     if rank == 0:
         line = {"metric": "trotter_steps_per_s", "value": value,
-                "unit": "steps/s" if world == 1 else "shard-steps/s (2^30 amplitudes per shard)",
+                "unit": "steps/s" if world == 1 else f"shard-steps/s (2^{L} amplitudes per shard)",
                 "state_steps_per_s": state_steps_per_s, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
