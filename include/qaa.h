@@ -294,7 +294,7 @@ qaa_status qaa_state_ptr(qaa_ctx* ctx, void** out, uint64_t* amps);
  *                        barrier between passes, FOUR warps per tile (one 128-thread CTA,
  *                        4 amplitudes per lane: the tile's work spread over the SM's four
  *                        sub-partitions); takes precedence over QAA_OPT_CLUSTER (measured
- *                        3.2-3.6 us per step at n = 13..16, vs 4.3-5.0 with one warp per
+ *                        3.2-3.5 us per step at n = 13..16, vs 4.3-5.0 with one warp per
  *                        tile and 5.4-8.3 cluster-resident). 2: ONE warp per tile (16
  *                        amplitudes per lane), also for 17 <= n <= 21 (there slower than the
  *                        per-pass kernels; a test hook), and qaa_sweep on teams of warp-tile

@@ -259,7 +259,8 @@ __device__ __forceinline__ void qw_xchg(double2* xb, double2 (&v)[4], int lane, 
 // tile program of the comment above)
 __device__ __forceinline__ void qw_pass(const WarpGeo& g, const WarpPass& ps, double2* psi, const uint8_t* Eg,
                                         const double2* phi_all, int n_phi, int64_t t0, int64_t tstep,
-                                        int64_t ntiles, int lane, int w, double2* xb) {
+                                        int64_t ntiles, int lane, int w, double2* xb, bool have_f0 = false,
+                                        const double2* f0 = nullptr) {
   const bool pre = ps.flags & WP_PRE, d = ps.flags & WP_D, post = ps.flags & WP_POST;
   const int fpre = (ps.flags >> 3) & 1, fpost = (ps.flags >> 4) & 1;
   const double2* phi = phi_all + ps.d * n_phi;
@@ -287,7 +288,10 @@ __device__ __forceinline__ void qw_pass(const WarpGeo& g, const WarpPass& ps, do
     // D factors: looked up as soon as the energies land, so the (per-pass, L1-cold)
     // phi row load overlaps the pre rotations and the first exchange
     double2 f[4];
-    if (d) {
+    if (d && have_f0 && T == t0) {  // prefetched before the grid barrier (qaa_quad_evolve)
+#pragma unroll
+      for (int r = 0; r < 4; r++) f[r] = f0[r];
+    } else if (d) {
       const uint8_t* et = Eg + (T << 9) + lane + (w << 5);
 #pragma unroll
       for (int r = 0; r < 4; r++) f[r] = __ldg(phi + __ldg(et + (r << 7)));
@@ -315,12 +319,25 @@ __global__ void __launch_bounds__(QW_THREADS) qaa_quad_evolve(const WarpEvolveAr
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t ntiles = (int64_t)1 << (a.L - 9);
   WarpPass nx = a.plan[0];
+  double2 fn[4];  // the next pass's D factors for this CTA's first tile
+  bool fn_ok = false;
   for (int64_t p = 0; p < a.npass; p++) {
     const WarpPass ps = nx;
     if (p + 1 < a.npass) nx = a.plan[p + 1];
     qw_pass(a.geo[ps.group], ps, a.psi, a.Eg[ps.group], a.phi_all, a.n_phi, blockIdx.x, gridDim.x, ntiles, lane,
-            w, xb);
-    if (p + 1 < a.npass) grid_barrier(a.bar, (unsigned)(p + 1) * gridDim.x);
+            w, xb, fn_ok, fn);
+    if (p + 1 < a.npass) {
+      // the energies and phi rows do not depend on the state: look the next pass's
+      // factors up now, so their two dependent loads land while the barrier waits
+      fn_ok = (nx.flags & WP_D) && (int64_t)blockIdx.x < ntiles;
+      if (fn_ok) {
+        const uint8_t* et = a.Eg[nx.group] + ((int64_t)blockIdx.x << 9) + lane + (w << 5);
+        const double2* phn = a.phi_all + nx.d * a.n_phi;
+#pragma unroll
+        for (int r = 0; r < 4; r++) fn[r] = __ldg(phn + __ldg(et + (r << 7)));
+      }
+      grid_barrier(a.bar, (unsigned)(p + 1) * gridDim.x);
+    }
   }
 }
 
