@@ -198,3 +198,16 @@ def test_sharded_plan_replay(q, n, world):
 def test_sharded_plan_rejects_small(q):
     with pytest.raises(q.QaaError):
         q.qaa_plan_describe_sharded(13, 2, 3, 1)  # L = 12: single tile group
+
+
+def test_binding_constants_match_header(q):
+    """Every QAA_OPT_* and qaa_status value the binding exposes equals the one
+    include/qaa.h declares (the binding hard-codes them; a drift would silently
+    set the wrong option)."""
+    hdr = open(os.path.join(ROOT, "include", "qaa.h")).read()
+    opts = dict((k, int(v)) for k, v in re.findall(r"\bQAA_OPT_([A-Z0-9_]+)\s*=\s*(\d+)", hdr))
+    assert opts, "no QAA_OPT_ enum in qaa.h"
+    for name, val in opts.items():
+        assert getattr(q, "OPT_" + name) == val, name
+    stats = dict((int(v), "QAA_" + k) for k, v in re.findall(r"\bQAA_(OK|E_[A-Z]+)\s*=\s*(\d+)", hdr))
+    assert stats == q.STATUS
